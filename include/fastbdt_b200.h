@@ -1,0 +1,152 @@
+/*
+ * fastbdt_b200.h — C ABI of the B200-native FastBDT hot path
+ * (libfastbdt_b200.so).  Plain pointers and sizes; no torch types.
+ *
+ * The reference (/root/reference/pkg, "binboost") is pure Python with no FFI,
+ * so its plugin surface is the Python signatures these entry points sit
+ * behind (INTEGRATION.md shows the ctypes binding):
+ *
+ *   bb_fit      replaces binboost.boosting.fit_forest
+ *               (pkg/src/binboost/boosting.py:117-173), reached from
+ *               binboost_bridge.fit (pkg/bridge/src/binboost_bridge/__init__.py:146-171)
+ *   bb_predict  replaces binboost.boosting.predict_batch
+ *               (boosting.py:196-219), reached from BoundModel.predict
+ *               (bridge __init__.py:85-93)
+ *   bb_bin      fit_binning + bin_values (pkg/src/binboost/binning.py:52-79)
+ *   bb_layer_hist / bb_split
+ *               accumulate_layer_histograms / find_best_cuts
+ *               (pkg/src/binboost/trees.py:139-204), exposed for parity tests
+ *   bb_subsample_masks
+ *               subsample (pkg/src/binboost/sample.py:120-132) driven by
+ *               numpy Generator(PCG64(seed)) (boosting.py:162); host only
+ *   bb_pairwise_sum
+ *               numpy's pairwise float64 sum used by prior (boosting.py:76-83);
+ *               host only
+ *
+ * Conventions: every function returns BB_OK (0) or an error code and sets a
+ * thread-local message readable with bb_last_error().  BB_EINVAL maps to the
+ * reference's ValueError, everything else to RuntimeError.  No host pointer
+ * is retained after a call returns.  Calls on one context are serialised by
+ * a mutex (one CUDA stream per context); use one context per thread for
+ * concurrency.
+ */
+#ifndef FASTBDT_B200_H
+#define FASTBDT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BB_ABI_VERSION 1
+
+enum { BB_OK = 0, BB_EINVAL = 1, BB_ECUDA = 2, BB_ESTATE = 3 };
+enum { BB_F32 = 0, BB_F64 = 1 };
+
+typedef struct bb_ctx bb_ctx;
+
+const char* bb_last_error(void);
+int bb_abi_version(void);
+int bb_device_count(int32_t* out);
+
+/* One context per device: owns a CUDA stream and, for multi-process row
+ * sharding, the rank's position in the job (rank, world). */
+int bb_ctx_create(int32_t device, bb_ctx** out);
+int bb_ctx_destroy(bb_ctx* ctx);
+
+/* FitConfig (boosting.py:36-57) plus the numpy PCG64(seed) state the
+ * subsample draws from (PCG64(seed).state["state"]: 128-bit state and
+ * increment split into hi/lo words, has_uint32, uinteger). */
+typedef struct {
+  int32_t n_trees;
+  int32_t depth;
+  int32_t binning_levels;
+  int32_t reserved0;
+  double shrinkage;
+  double subsample;
+  uint64_t pcg_state_hi, pcg_state_lo;
+  uint64_t pcg_inc_hi, pcg_inc_lo;
+  int32_t pcg_has_uint32;
+  uint32_t pcg_uinteger;
+} bb_fit_config;
+
+/* Teacher-forced parity protocol: at (tree, heap node)
+ * take this cut instead of the argmax. */
+typedef struct {
+  int32_t tree, node, valid, feature, cut_bin;
+} bb_forced_cut;
+
+/* Caller-allocated host outputs.  I = 2^depth - 1, N = 2^(depth+1) - 1,
+ * B = 2^binning_levels. */
+typedef struct {
+  double* boundaries;   /* [d][B-1]                                     */
+  int32_t* feature;     /* [T][I]  -1 where invalid (trees.py:64)       */
+  int32_t* cut_bin;     /* [T][I]                                       */
+  uint8_t* valid;       /* [T][I]                                       */
+  double* threshold;    /* [T][I]  NaN where invalid                    */
+  double* gain;         /* [T][I]                                       */
+  double* node_weight;  /* [T][N]  shrinkage applied (boosting.py:168)  */
+  double* node_purity;  /* [T][N]                                       */
+  double* f0;           /* [1]                                          */
+  int32_t* fixed_shift; /* [1]  S of the int64 fixed-point sums         */
+  int64_t* n_sig;       /* [1]  rows in the signal block                */
+  uint16_t* leaves;     /* optional [T][n] final node per row, class-block order */
+  double* scores;       /* optional [n] final F per row, class-block order */
+  double* timing_ms;    /* optional [8]: upload, binning, trees, download, total */
+} bb_fit_out;
+
+/* X: row-major (n, d) float32 (BB_F32) or float64 (BB_F64); y01: int8, > 0
+ * is signal; w: float64 or NULL (unit weights).  *_on_device != 0 means the
+ * pointer is CUDA device memory on the context's device. */
+int bb_fit(bb_ctx* ctx, const void* X, int32_t x_dtype, int32_t x_on_device, int64_t n, int32_t d,
+           const int8_t* y01, int32_t y_on_device, const double* w, int32_t w_on_device,
+           const bb_fit_config* cfg, const bb_forced_cut* forced, int32_t n_forced, bb_fit_out* out);
+
+/* A fitted forest (Forest, boosting.py:60-73), host arrays laid out as in
+ * bb_fit_out. */
+typedef struct {
+  int32_t n_trees;
+  int32_t depth;
+  int32_t n_features;
+  int32_t reserved0;
+  double f0;
+  const int32_t* feature;
+  const uint8_t* valid;
+  const double* threshold;
+  const double* node_weight;
+} bb_forest;
+
+/* Signal probabilities sigmoid(2F) (and optionally F) per row. */
+int bb_predict(bb_ctx* ctx, const bb_forest* forest, const void* X, int32_t x_dtype, int32_t x_on_device,
+               int64_t n, int32_t d, double* out_prob, double* out_score, int32_t out_on_device);
+
+/* Parity entry points ------------------------------------------------ */
+
+/* Boundaries [d][B-1] and codes [d][n] (int16, input row order). */
+int bb_bin(bb_ctx* ctx, const void* X, int32_t x_dtype, int64_t n, int32_t d, int32_t levels,
+           double* out_boundaries, int16_t* out_codes);
+
+/* One layer's integer histograms from host inputs in class-block order:
+ * codes [d][n] (uint16, 0 = missing), node [n] (uint16 heap ids), q [n]
+ * int64 fixed-point weights.  out_hist [2][2^(layer-1)][d][B] int64, slot
+ * b holds code b+1. */
+int bb_layer_hist(bb_ctx* ctx, const uint16_t* codes, const uint16_t* node, const int64_t* q, int64_t n,
+                  int64_t n_sig, int32_t d, int32_t levels, int32_t layer, int64_t* out_hist);
+
+/* Best cuts of one layer from integer histograms [2][nodes][d][B] (as
+ * produced by bb_layer_hist), fixed-point scale 2^-shift. */
+int bb_split(bb_ctx* ctx, const int64_t* hist, int32_t d, int32_t levels, int32_t layer, int32_t final_layer,
+             int32_t shift, const double* boundaries, uint8_t* out_valid, int32_t* out_feature,
+             int32_t* out_cut, double* out_gain, double* out_threshold);
+
+/* Host only (no GPU needed): active bits [T][ceil((n_sig+n_bkg)/32)]. */
+int bb_subsample_masks(int64_t n_sig, int64_t n_bkg, double rate, int32_t n_trees, const bb_fit_config* rng,
+                       uint32_t* out_bits);
+double bb_pairwise_sum(const double* a, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTBDT_B200_H */

@@ -1,0 +1,766 @@
+// C-ABI and host driver of the FastBDT B200 hot path (include/fastbdt_b200.h).
+//
+// bb_fit is the B200 restatement of fit_forest (reference
+// pkg/src/binboost/boosting.py:117-173): GPU binning, class-block layout,
+// then per tree one refresh kernel and per layer histogram -> split ->
+// advance kernels, all stream-ordered with no host synchronisation inside
+// the tree loop.  The host only generates the next tree's subsample bits
+// (exact numpy PCG64 restatement, bb_mask.cpp) while the GPU works.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fastbdt_b200.h"
+#include "bb_mask.h"
+#include "common.cuh"
+#include "kernels_apply.cuh"
+#include "kernels_binning.cuh"
+#include "kernels_tree.cuh"
+
+namespace bb {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+// numpy's pairwise float64 summation (numpy/_core/src/umath/loops_utils.h
+// pairwise_sum, PW_BLOCKSIZE 128, 8-way unroll); used by prior()
+// (boosting.py:79-80 calls np.sum).
+static double pairwise(const double* a, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res += a[i];
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i;
+    for (i = 8; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return pairwise(a, n2) + pairwise(a + n2, n - n2);
+}
+
+// S = 32 - ceil(log2(max|w|)) so |w*bw| * 2^S <= 2^32 (bw <= 1):
+// one returning 32-bit shared atomic per update for non-negative weights.
+static int fixed_shift_for(double max_abs_w) {
+  if (!(max_abs_w > 0.0)) return 32;
+  int e;
+  const double m = std::frexp(max_abs_w, &e);
+  const int ceil_log2 = (m == 0.5) ? e - 1 : e;
+  return 32 - ceil_log2;
+}
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  std::mutex mu;
+};
+
+// stream-ordered arena: every allocation of one call, freed at the end
+struct Arena {
+  cudaStream_t s;
+  std::vector<void*> ptrs;
+  explicit Arena(cudaStream_t st) : s(st) {}
+  template <typename T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    BB_CUDA(cudaMallocAsync(&p, count * sizeof(T), s));
+    ptrs.push_back(p);
+    return reinterpret_cast<T*>(p);
+  }
+  void release(void* p) {
+    for (auto& q : ptrs)
+      if (q == p) {
+        cudaFreeAsync(q, s);
+        q = nullptr;
+      }
+  }
+  ~Arena() {
+    for (void* p : ptrs)
+      if (p) cudaFreeAsync(p, s);
+  }
+};
+
+static int grid_for(int64_t n, int threads, int sm, int per_sm = 8) {
+  const int64_t want = ceil_div(n, threads);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm * per_sm));
+}
+
+static double elapsed_ms(std::chrono::steady_clock::time_point a) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+}
+
+// ------------------------------------------------------------- binning
+template <typename T>
+struct BinResult {
+  double* bounds;                       // device [d][B-1]
+  typename KeyOf<T>::K* bkeys;          // device [d][B-1]
+  std::vector<unsigned long long> finite, nans;
+};
+
+constexpr int kSmemHistBins = 8192;  // k_select_hist shared counters
+
+template <typename T>
+static void run_select(Ctx& c, Arena& A, const typename KeyOf<T>::K* keys, int64_t n, int d, int levels,
+                       const unsigned long long* finite_dev, double* bounds, typename KeyOf<T>::K* bkeys) {
+  using K = typename KeyOf<T>::K;
+  constexpr int KB = sizeof(K) * 8;
+  const int B = 1 << levels, nt = B - 1;
+  SelectState<K> st;
+  st.nt = nt;
+  st.hist_cap = std::max<int64_t>(4096, (int64_t)nt * 256);
+  st.tgt_prefix = A.alloc<K>((size_t)d * nt);
+  st.tgt_rank = A.alloc<unsigned long long>((size_t)d * nt);
+  st.tgt_group = A.alloc<int>((size_t)d * nt);
+  st.grp_prefix = A.alloc<K>((size_t)d * nt);
+  st.grp_first_tgt = A.alloc<int>((size_t)d * nt);
+  st.grp_count = A.alloc<int>(d);
+  st.hist = A.alloc<unsigned int>((size_t)d * st.hist_cap);
+  st.finite_cnt = finite_dev;
+  BB_CUDA(cudaMemsetAsync(st.hist, 0, (size_t)d * st.hist_cap * 4, c.stream));
+  k_select_init<K><<<d, 256, 0, c.stream>>>(st, B);
+  BB_LAUNCH_CHECK();
+  int resolved = 0;
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256 * 8), std::max(1, 2 * c.sm_count * 8 / d + 1)));
+  while (resolved < KB) {
+    int db = (resolved == 0) ? 12 : 8;
+    db = std::min(db, KB - resolved);
+    k_select_hist<K><<<dim3(gx, d), 256, kSmemHistBins * 4, c.stream>>>(keys, n, st, resolved, db, kSmemHistBins);
+    BB_LAUNCH_CHECK();
+    k_select_scan<K><<<d, 1024, 0, c.stream>>>(st, db);
+    BB_LAUNCH_CHECK();
+    resolved += db;
+  }
+  k_select_finish<K><<<d, 256, 0, c.stream>>>(st, bounds, bkeys);
+  BB_LAUNCH_CHECK();
+}
+
+template <typename T>
+static typename KeyOf<T>::K* make_keys(Ctx& c, Arena& A, const T* Xd, int64_t n, int d,
+                                       std::vector<unsigned long long>& finite, std::vector<unsigned long long>& nans,
+                                       unsigned long long** finite_dev_out) {
+  using K = typename KeyOf<T>::K;
+  K* keys = A.alloc<K>((size_t)n * d);
+  unsigned long long* cnt = A.alloc<unsigned long long>(2 * (size_t)d);
+  BB_CUDA(cudaMemsetAsync(cnt, 0, 2 * (size_t)d * 8, c.stream));
+  if (n > 0) {
+    k_transpose_keys<T><<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(d, 32)), dim3(32, 8), 0, c.stream>>>(
+        Xd, n, d, keys, cnt, cnt + d);
+    BB_LAUNCH_CHECK();
+  }
+  finite.assign(d, 0);
+  nans.assign(d, 0);
+  BB_CUDA(cudaMemcpyAsync(finite.data(), cnt, (size_t)d * 8, cudaMemcpyDeviceToHost, c.stream));
+  BB_CUDA(cudaMemcpyAsync(nans.data(), cnt + d, (size_t)d * 8, cudaMemcpyDeviceToHost, c.stream));
+  BB_CUDA(cudaStreamSynchronize(c.stream));
+  *finite_dev_out = cnt;
+  return keys;
+}
+
+// ------------------------------------------------------------- tree loop
+struct FitShape {
+  int64_t n, n_sig;
+  int d, levels, B, depth, n_internal, n_nodes, T;
+};
+
+static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, int64_t smem_budget) {
+  HistPlan p{};
+  p.nodes = 1 << (layer - 1);
+  p.start = p.nodes - 1;
+  const int64_t fn_budget = std::max<int64_t>(1, smem_budget / ((int64_t)s.B * 8));
+  if (p.nodes <= fn_budget) {
+    p.ngs = p.nodes;
+    p.n_ng = 1;
+    int fg = (int)std::min<int64_t>(s.d, fn_budget / p.nodes);
+    p.n_fg = (int)ceil_div(s.d, fg);
+    p.fg = (int)ceil_div(s.d, p.n_fg);
+  } else {
+    p.fg = 1;
+    p.n_fg = s.d;
+    p.ngs = (int)fn_budget;
+    p.n_ng = (int)ceil_div(p.nodes, p.ngs);
+  }
+  const int64_t items = (int64_t)p.n_fg * p.n_ng;
+  const int64_t target = (int64_t)sm_count * 2 * 2;
+  const int64_t chunks = std::max<int64_t>(2, ceil_div(target, items));
+  int64_t cr = std::max<int64_t>(8192, ceil_div(s.n, chunks));
+  cr = ceil_div(cr, 512) * 512;
+  p.chunk_rows = cr;
+  p.chunks_sig = (int)ceil_div(s.n_sig, cr);
+  p.chunks_bkg = (int)ceil_div(s.n - s.n_sig, cr);
+  return p;
+}
+
+constexpr int64_t kHistSmem = 96 * 1024;
+
+template <typename CodeT, typename NodeT>
+static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, int64_t stride, int code_off,
+                      const double* w_cb, double f0, int shift, const bb_fit_config& cfg,
+                      const bb_forced_cut* forced, int n_forced, const double* bounds_dev, bb_fit_out* out,
+                      double* t_trees_ms) {
+  const int64_t n = s.n;
+  cudaStream_t st = c.stream;
+  const double two_s = std::ldexp(1.0, shift), scale = std::ldexp(1.0, -shift);
+  double* F = A.alloc<double>(n);
+  NodeT* node = A.alloc<NodeT>(n);
+  long long* q = A.alloc<long long>(n);
+  const int64_t words = ceil_div(n, 32);
+  unsigned int* mask = A.alloc<unsigned int>(words);
+  const int max_nodes = 1 << (s.depth - 1);
+  unsigned long long* hist = A.alloc<unsigned long long>((size_t)2 * max_nodes * s.d * s.B);
+  BB_CUDA(cudaMemsetAsync(hist, 0, (size_t)2 * max_nodes * s.d * s.B * 8, st));
+  unsigned long long* sums = A.alloc<unsigned long long>((size_t)2 * s.n_nodes * 2);
+  BB_CUDA(cudaMemsetAsync(sums, 0, (size_t)2 * s.n_nodes * 2 * 8, st));
+  TreeArrays ta;
+  const size_t TI = (size_t)s.T * s.n_internal, TN = (size_t)s.T * s.n_nodes;
+  ta.feature = A.alloc<int>(TI);
+  ta.cut = A.alloc<int>(TI);
+  ta.valid = A.alloc<unsigned char>(TI);
+  ta.gain = A.alloc<double>(TI);
+  ta.thr = A.alloc<double>(TI);
+  ta.nw = A.alloc<double>(TN);
+  ta.pur = A.alloc<double>(TN);
+  ta.forced = nullptr;
+  if (n_forced > 0) {
+    std::vector<int> fh(TI, -2);
+    for (int k = 0; k < n_forced; ++k) {
+      const bb_forced_cut& fc = forced[k];
+      if (fc.tree < 0 || fc.tree >= s.T || fc.node < 0 || fc.node >= s.n_internal)
+        throw InvalidArg{"forced cut out of range"};
+      if (fc.valid && (fc.feature < 0 || fc.feature >= s.d || fc.cut_bin < 1 || fc.cut_bin > s.B - 1))
+        throw InvalidArg{"forced cut feature/cut_bin out of range"};
+      fh[(size_t)fc.tree * s.n_internal + fc.node] = fc.valid ? (fc.feature << 16) + fc.cut_bin : -1;
+    }
+    int* fd = A.alloc<int>(TI);
+    BB_CUDA(cudaMemcpyAsync(fd, fh.data(), TI * 4, cudaMemcpyHostToDevice, st));
+    ta.forced = fd;
+  }
+  SplitScratch sc;
+  sc.best_gain = A.alloc<double>((size_t)max_nodes * s.d);
+  sc.best_flat = A.alloc<int>((size_t)max_nodes * s.d);
+  sc.forced_gain = A.alloc<double>(max_nodes);
+  sc.done = A.alloc<unsigned int>(max_nodes);
+  BB_CUDA(cudaMemsetAsync(sc.done, 0, (size_t)max_nodes * 4, st));
+
+  // F = f0 (boosting.py:158-160)
+  k_fill_f64<<<grid_for(n, 256, c.sm_count), 256, 0, st>>>(F, n, f0);
+  BB_LAUNCH_CHECK();
+
+  std::vector<HistPlan> plans(s.depth + 1);
+  for (int l = 1; l <= s.depth; ++l) plans[l] = plan_layer(l, s, c.sm_count, kHistSmem);
+  BB_CUDA(cudaFuncSetAttribute(k_layer_hist<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHistSmem));
+
+  // host subsample bits, double-buffered in pinned memory
+  Pcg64 g;
+  g.state = ((unsigned __int128)cfg.pcg_state_hi << 64) | cfg.pcg_state_lo;
+  g.inc = ((unsigned __int128)cfg.pcg_inc_hi << 64) | cfg.pcg_inc_lo;
+  g.has_uint32 = cfg.pcg_has_uint32;
+  g.uinteger = cfg.pcg_uinteger;
+  unsigned int* pinned[2];
+  BB_CUDA(cudaMallocHost(&pinned[0], (size_t)words * 4));
+  BB_CUDA(cudaMallocHost(&pinned[1], (size_t)words * 4));
+  cudaEvent_t copied[2];
+  BB_CUDA(cudaEventCreateWithFlags(&copied[0], cudaEventDisableTiming));
+  BB_CUDA(cudaEventCreateWithFlags(&copied[1], cudaEventDisableTiming));
+  std::vector<uint32_t> perm;
+  std::vector<NodeT> leaf_tmp;
+  const int gridN = grid_for(n, 256, c.sm_count);
+  const int gridA = grid_for(n, 512, c.sm_count, 4);
+  const auto t0 = std::chrono::steady_clock::now();
+  try {
+    for (int t = 0; t < s.T; ++t) {
+      unsigned int* hb = pinned[t & 1];
+      if (t >= 2) BB_CUDA(cudaEventSynchronize(copied[t & 1]));
+      subsample_tree(g, s.n_sig, s.n - s.n_sig, cfg.subsample, hb, perm);
+      BB_CUDA(cudaMemcpyAsync(mask, hb, (size_t)words * 4, cudaMemcpyHostToDevice, st));
+      BB_CUDA(cudaEventRecord(copied[t & 1], st));
+      k_update_refresh<NodeT><<<gridN, 256, 0, st>>>(n, s.n_sig, F, node, w_cb, q, mask,
+                                                      t > 0 ? ta.nw + (size_t)(t - 1) * s.n_nodes : nullptr, two_s);
+      BB_LAUNCH_CHECK();
+      for (int layer = 1; layer <= s.depth; ++layer) {
+        const HistPlan& p = plans[layer];
+        const int items = (p.chunks_sig + p.chunks_bkg) * p.n_fg * p.n_ng;
+        const size_t smem = (size_t)p.ngs * p.fg * s.B * 8;
+        k_layer_hist<CodeT, NodeT><<<items, 512, smem, st>>>(codes, stride, code_off, node, q, n, s.n_sig, s.d, s.B, p,
+                                                               hist);
+        BB_LAUNCH_CHECK();
+        const int nodes = p.nodes;
+        const int n_fc_want = std::max(1, std::min(s.d, (2 * c.sm_count + nodes - 1) / nodes));
+        const int fc_size = (int)ceil_div(s.d, n_fc_want);
+        const int n_fc = (int)ceil_div(s.d, fc_size);
+        k_split<256><<<dim3(nodes, n_fc), 256, 0, st>>>(hist, s.d, s.B, p.start, nodes, fc_size,
+                                                       layer == s.depth ? 1 : 0, scale, t, s.n_internal, ta,
+                                                       bounds_dev, sc);
+        BB_LAUNCH_CHECK();
+        const bool last = layer == s.depth;
+        k_advance<CodeT, NodeT><<<gridA, 512, last ? (size_t)32 * s.n_nodes : 0, st>>>(
+            codes, stride, code_off, node, n, s.n_sig, p.start, t, s.n_internal, ta, last ? 1 : 0, s.n_nodes, q, mask,
+            F, w_cb, two_s, sums);
+        BB_LAUNCH_CHECK();
+      }
+      k_node_weights<<<1, 256, (size_t)2 * s.n_nodes * 2 * 8, st>>>(sums, s.n_nodes, s.depth, scale, cfg.shrinkage, t,
+                                                                    ta);
+      BB_LAUNCH_CHECK();
+      if (out->leaves) {
+        leaf_tmp.resize(n);
+        BB_CUDA(cudaMemcpyAsync(leaf_tmp.data(), node, (size_t)n * sizeof(NodeT), cudaMemcpyDeviceToHost, st));
+        BB_CUDA(cudaStreamSynchronize(st));
+        uint16_t* dst = out->leaves + (size_t)t * n;
+        for (int64_t i = 0; i < n; ++i) dst[i] = (uint16_t)leaf_tmp[i];
+      }
+    }
+    if (out->scores) {
+      k_update_scores<NodeT><<<gridN, 256, 0, st>>>(n, F, node, ta.nw + (size_t)(s.T - 1) * s.n_nodes);
+      BB_LAUNCH_CHECK();
+      BB_CUDA(cudaMemcpyAsync(out->scores, F, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    }
+    BB_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    cudaStreamSynchronize(st);
+    cudaFreeHost(pinned[0]);
+    cudaFreeHost(pinned[1]);
+    cudaEventDestroy(copied[0]);
+    cudaEventDestroy(copied[1]);
+    throw;
+  }
+  *t_trees_ms = elapsed_ms(t0);
+  cudaFreeHost(pinned[0]);
+  cudaFreeHost(pinned[1]);
+  cudaEventDestroy(copied[0]);
+  cudaEventDestroy(copied[1]);
+
+  // outputs
+  std::vector<unsigned char> vtmp(TI);
+  BB_CUDA(cudaMemcpyAsync(out->feature, ta.feature, TI * 4, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaMemcpyAsync(out->cut_bin, ta.cut, TI * 4, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaMemcpyAsync(out->valid, ta.valid, TI, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaMemcpyAsync(out->gain, ta.gain, TI * 8, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaMemcpyAsync(out->threshold, ta.thr, TI * 8, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaMemcpyAsync(out->node_weight, ta.nw, TN * 8, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaMemcpyAsync(out->node_purity, ta.pur, TN * 8, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaStreamSynchronize(st));
+}
+
+template <typename T>
+static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const int8_t* y, bool y_dev,
+                     const double* w, bool w_dev, const bb_fit_config& cfg, const bb_forced_cut* forced,
+                     int n_forced, bb_fit_out* out) {
+  using K = typename KeyOf<T>::K;
+  const auto t_all = std::chrono::steady_clock::now();
+  cudaStream_t st = c.stream;
+  Arena A(st);
+  const int levels = cfg.binning_levels, B = 1 << levels, nt = B - 1;
+  // ---- upload
+  auto t_up = std::chrono::steady_clock::now();
+  const T* Xd = reinterpret_cast<const T*>(Xv);
+  if (!x_dev) {
+    T* p = A.alloc<T>((size_t)n * d);
+    BB_CUDA(cudaMemcpyAsync(p, Xv, (size_t)n * d * sizeof(T), cudaMemcpyHostToDevice, st));
+    Xd = p;
+  }
+  const int8_t* yd = y;
+  if (!y_dev) {
+    int8_t* p = A.alloc<int8_t>(n);
+    BB_CUDA(cudaMemcpyAsync(p, y, (size_t)n, cudaMemcpyHostToDevice, st));
+    yd = p;
+  }
+  const double* wd = w;
+  if (w && !w_dev) {
+    double* p = A.alloc<double>(n);
+    BB_CUDA(cudaMemcpyAsync(p, w, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    wd = p;
+  }
+  BB_CUDA(cudaStreamSynchronize(st));
+  const double ms_up = elapsed_ms(t_up);
+  // ---- binning
+  auto t_bin = std::chrono::steady_clock::now();
+  std::vector<unsigned long long> finite, nans;
+  unsigned long long* finite_dev = nullptr;
+  K* keys = make_keys<T>(c, A, Xd, n, d, finite, nans, &finite_dev);
+  if (!x_dev) A.release(const_cast<T*>(Xd));
+  double* bounds = A.alloc<double>((size_t)d * nt);
+  K* bkeys = A.alloc<K>((size_t)d * nt);
+  run_select<T>(c, A, keys, n, d, levels, finite_dev, bounds, bkeys);
+  // class blocks
+  const int n_tiles = (int)ceil_div(n, CLS_TILE);
+  int* tile_sig = A.alloc<int>(n_tiles + 1);
+  int* pos = A.alloc<int>(n);
+  double* w_cb = w ? A.alloc<double>(n) : nullptr;
+  k_class_tile_counts<<<n_tiles, 256, 0, st>>>(yd, n, tile_sig);
+  BB_LAUNCH_CHECK();
+  k_class_scan<<<1, 1024, 0, st>>>(tile_sig, n_tiles);
+  BB_LAUNCH_CHECK();
+  k_class_positions<<<n_tiles, 256, 0, st>>>(yd, n, tile_sig, pos, wd, w_cb);
+  BB_LAUNCH_CHECK();
+  int n_sig_i = 0;
+  BB_CUDA(cudaMemcpyAsync(&n_sig_i, tile_sig + n_tiles, 4, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaStreamSynchronize(st));
+  const int64_t n_sig = n_sig_i;
+  if (n_sig == 0 || n_sig == n) throw InvalidArg{"training data must contain both classes"};
+  bool any_nan = false;
+  for (int f = 0; f < d; ++f) any_nan |= nans[f] > 0;
+  const int64_t stride = ceil_div(n, 64) * 64;
+  FitShape s{n, n_sig, d, levels, B, cfg.depth, (1 << cfg.depth) - 1, (1 << (cfg.depth + 1)) - 1, cfg.n_trees};
+  // prior (boosting.py:76-83) and the fixed-point shift from the user weights
+  double w_sig, w_bkg, max_abs = 1.0;
+  if (w) {
+    std::vector<double> wh(n);
+    BB_CUDA(cudaMemcpyAsync(wh.data(), w_cb, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaStreamSynchronize(st));
+    w_sig = pairwise(wh.data(), n_sig);
+    w_bkg = pairwise(wh.data() + n_sig, n - n_sig);
+    max_abs = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (!std::isfinite(wh[i])) throw InvalidArg{"user weights must be finite"};
+      max_abs = std::max(max_abs, std::fabs(wh[i]));
+    }
+  } else {
+    w_sig = (double)n_sig;
+    w_bkg = (double)(n - n_sig);
+  }
+  const double f0 = (w_sig <= 0.0 || w_bkg <= 0.0) ? 0.0 : 0.5 * std::log(w_sig / w_bkg);
+  const int shift = fixed_shift_for(max_abs);
+  double ms_trees = 0.0;
+  auto launch_codes = [&](auto* codes, int off) {
+    using CodeT = std::remove_pointer_t<decltype(codes)>;
+    k_codes<K, CodeT><<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256 * 4), 4 * c.sm_count / d + 1)), d),
+                        256, (size_t)nt * sizeof(K), st>>>(keys, n, nt, bkeys, pos, codes, stride, off);
+    BB_LAUNCH_CHECK();
+  };
+  auto after_codes = [&]() {
+    A.release(keys);
+  };
+  double ms_bin = 0.0;
+  auto go = [&](auto* codes, int off) {
+    using CodeT = std::remove_pointer_t<decltype(codes)>;
+    launch_codes(codes, off);
+    after_codes();
+    BB_CUDA(cudaStreamSynchronize(st));
+    ms_bin = elapsed_ms(t_bin);
+    if (s.depth <= 7)
+      run_trees<CodeT, uint8_t>(c, A, s, codes, stride, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees);
+    else
+      run_trees<CodeT, uint16_t>(c, A, s, codes, stride, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees);
+  };
+  if (B <= 255) {
+    go(A.alloc<uint8_t>((size_t)d * stride), 0);
+  } else if (B == 256 && !any_nan) {
+    go(A.alloc<uint8_t>((size_t)d * stride), 1);
+  } else {
+    go(A.alloc<uint16_t>((size_t)d * stride), 0);
+  }
+  auto t_dn = std::chrono::steady_clock::now();
+  BB_CUDA(cudaMemcpyAsync(out->boundaries, bounds, (size_t)d * nt * 8, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaStreamSynchronize(st));
+  *out->f0 = f0;
+  *out->fixed_shift = shift;
+  if (out->n_sig) *out->n_sig = n_sig;
+  if (out->timing_ms) {
+    out->timing_ms[0] = ms_up;
+    out->timing_ms[1] = ms_bin;
+    out->timing_ms[2] = ms_trees;
+    out->timing_ms[3] = elapsed_ms(t_dn);
+    out->timing_ms[4] = elapsed_ms(t_all);
+  }
+}
+
+}  // namespace bb
+
+using namespace bb;
+
+struct bb_ctx {
+  Ctx c;
+};
+
+template <typename Fn>
+static int guarded(Fn&& fn) {
+  try {
+    fn();
+    return BB_OK;
+  } catch (const InvalidArg& e) {
+    set_error(e.msg);
+    return BB_EINVAL;
+  } catch (const CudaError& e) {
+    set_error(e.msg);
+    return BB_ECUDA;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return BB_ESTATE;
+  }
+}
+
+extern "C" {
+
+const char* bb_last_error(void) { return g_err.c_str(); }
+int bb_abi_version(void) { return BB_ABI_VERSION; }
+
+int bb_device_count(int32_t* out) {
+  return guarded([&] {
+    int n = 0;
+    BB_CUDA(cudaGetDeviceCount(&n));
+    *out = n;
+  });
+}
+
+int bb_ctx_create(int32_t device, bb_ctx** out) {
+  return guarded([&] {
+    auto* h = new bb_ctx();
+    h->c.device = device;
+    try {
+      BB_CUDA(cudaSetDevice(device));
+      BB_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
+      BB_CUDA(cudaDeviceGetAttribute(&h->c.sm_count, cudaDevAttrMultiProcessorCount, device));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int bb_ctx_destroy(bb_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->c.device);
+    if (ctx->c.stream) {
+      cudaStreamSynchronize(ctx->c.stream);
+      cudaStreamDestroy(ctx->c.stream);
+    }
+    delete ctx;
+  });
+}
+
+int bb_fit(bb_ctx* ctx, const void* X, int32_t x_dtype, int32_t x_on_device, int64_t n, int32_t d,
+           const int8_t* y01, int32_t y_on_device, const double* w, int32_t w_on_device,
+           const bb_fit_config* cfg, const bb_forced_cut* forced, int32_t n_forced, bb_fit_out* out) {
+  return guarded([&] {
+    if (!ctx || !cfg || !out) throw InvalidArg{"null argument"};
+    if (n < 2 || d < 1) throw InvalidArg{"need at least 2 rows and 1 feature"};
+    if (n >= (int64_t)1 << 31) throw InvalidArg{"at most 2^31-1 rows per device"};
+    if (cfg->n_trees < 1) throw InvalidArg{"n_trees must be >= 1"};
+    if (cfg->depth < 1 || cfg->depth > 15) throw InvalidArg{"depth must be in [1, 15]"};
+    if (cfg->binning_levels < 1 || cfg->binning_levels > 11)
+      throw InvalidArg{"binning_levels must be in [1, 11] on the GPU path"};
+    if (!(cfg->shrinkage > 0.0 && cfg->shrinkage <= 1.0)) throw InvalidArg{"shrinkage must be in (0, 1]"};
+    if (!(cfg->subsample > 0.0 && cfg->subsample <= 1.0)) throw InvalidArg{"subsample must be in (0, 1]"};
+    const int64_t hist_bytes = (int64_t)2 * (1 << (cfg->depth - 1)) * d * (1 << cfg->binning_levels) * 8;
+    if (hist_bytes > ((int64_t)16 << 30)) throw InvalidArg{"layer histogram exceeds 16 GiB (depth/features/levels)"};
+    std::lock_guard<std::mutex> lock(ctx->c.mu);
+    BB_CUDA(cudaSetDevice(ctx->c.device));
+    if (x_dtype == BB_F32)
+      fit_impl<float>(ctx->c, X, x_on_device, n, d, y01, y_on_device, w, w_on_device, *cfg, forced, n_forced, out);
+    else if (x_dtype == BB_F64)
+      fit_impl<double>(ctx->c, X, x_on_device, n, d, y01, y_on_device, w, w_on_device, *cfg, forced, n_forced, out);
+    else
+      throw InvalidArg{"x_dtype must be BB_F32 or BB_F64"};
+  });
+}
+
+int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype, int32_t x_on_device, int64_t n,
+               int32_t d, double* out_prob, double* out_score, int32_t out_on_device) {
+  return guarded([&] {
+    if (!ctx || !fo) throw InvalidArg{"null argument"};
+    if (d != fo->n_features)
+      throw InvalidArg{"model expects " + std::to_string(fo->n_features) + " features, rows have " + std::to_string(d)};
+    if (n == 0) return;
+    std::lock_guard<std::mutex> lock(ctx->c.mu);
+    Ctx& c = ctx->c;
+    BB_CUDA(cudaSetDevice(c.device));
+    cudaStream_t st = c.stream;
+    Arena A(st);
+    const int I = (1 << fo->depth) - 1, N = (1 << (fo->depth + 1)) - 1;
+    const size_t TI = (size_t)fo->n_trees * I, TN = (size_t)fo->n_trees * N;
+    int* feat = A.alloc<int>(TI);
+    unsigned char* vld = A.alloc<unsigned char>(TI);
+    double* thr = A.alloc<double>(TI);
+    double* nw = A.alloc<double>(TN);
+    if (TI) {
+      BB_CUDA(cudaMemcpyAsync(feat, fo->feature, TI * 4, cudaMemcpyHostToDevice, st));
+      BB_CUDA(cudaMemcpyAsync(vld, fo->valid, TI, cudaMemcpyHostToDevice, st));
+      BB_CUDA(cudaMemcpyAsync(thr, fo->threshold, TI * 8, cudaMemcpyHostToDevice, st));
+      BB_CUDA(cudaMemcpyAsync(nw, fo->node_weight, TN * 8, cudaMemcpyHostToDevice, st));
+    }
+    ApplyForest af{fo->n_trees, fo->depth, I, N, feat, vld, thr, nw, fo->f0};
+    const size_t es = x_dtype == BB_F32 ? 4 : 8;
+    const void* Xd = X;
+    if (!x_on_device) {
+      void* p = A.alloc<unsigned char>((size_t)n * d * es);
+      BB_CUDA(cudaMemcpyAsync(p, X, (size_t)n * d * es, cudaMemcpyHostToDevice, st));
+      Xd = p;
+    }
+    double* pd = out_prob;
+    double* fd = out_score;
+    if (!out_on_device) {
+      pd = out_prob ? A.alloc<double>(n) : nullptr;
+      fd = out_score ? A.alloc<double>(n) : nullptr;
+    }
+    const unsigned grid = (unsigned)ceil_div(n, APPLY_ROWS);
+    const size_t smem = (size_t)APPLY_ROWS * (d + 1) * es;
+    if (x_dtype == BB_F32) {
+      BB_CUDA(cudaFuncSetAttribute(k_apply<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      k_apply<float><<<grid, APPLY_ROWS, smem, st>>>((const float*)Xd, n, d, af, pd, fd);
+    } else {
+      BB_CUDA(cudaFuncSetAttribute(k_apply<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      k_apply<double><<<grid, APPLY_ROWS, smem, st>>>((const double*)Xd, n, d, af, pd, fd);
+    }
+    BB_LAUNCH_CHECK();
+    if (!out_on_device) {
+      if (out_prob) BB_CUDA(cudaMemcpyAsync(out_prob, pd, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+      if (out_score) BB_CUDA(cudaMemcpyAsync(out_score, fd, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    }
+    BB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int bb_bin(bb_ctx* ctx, const void* X, int32_t x_dtype, int64_t n, int32_t d, int32_t levels, double* out_boundaries,
+           int16_t* out_codes) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg{"null argument"};
+    if (levels < 1 || levels > 11) throw InvalidArg{"levels must be in [1, 11]"};
+    std::lock_guard<std::mutex> lock(ctx->c.mu);
+    Ctx& c = ctx->c;
+    BB_CUDA(cudaSetDevice(c.device));
+    cudaStream_t st = c.stream;
+    Arena A(st);
+    const int nt = (1 << levels) - 1;
+    auto body = [&](auto tag) {
+      using T = decltype(tag);
+      using K = typename KeyOf<T>::K;
+      T* Xd = A.alloc<T>((size_t)n * d);
+      BB_CUDA(cudaMemcpyAsync(Xd, X, (size_t)n * d * sizeof(T), cudaMemcpyHostToDevice, st));
+      std::vector<unsigned long long> fin, nan_;
+      unsigned long long* fdev = nullptr;
+      K* keys = make_keys<T>(c, A, Xd, n, d, fin, nan_, &fdev);
+      double* bounds = A.alloc<double>((size_t)d * nt);
+      K* bkeys = A.alloc<K>((size_t)d * nt);
+      run_select<T>(c, A, keys, n, d, levels, fdev, bounds, bkeys);
+      int* pos = A.alloc<int>(n);
+      k_iota<<<grid_for(n, 256, c.sm_count), 256, 0, st>>>(pos, n);
+      BB_LAUNCH_CHECK();
+      uint16_t* codes = A.alloc<uint16_t>((size_t)d * n);
+      k_codes<K, uint16_t><<<dim3((unsigned)std::max<int64_t>(1, ceil_div(n, 1024)), d), 256, (size_t)nt * sizeof(K), st>>>(
+          keys, n, nt, bkeys, pos, codes, n, 0);
+      BB_LAUNCH_CHECK();
+      BB_CUDA(cudaMemcpyAsync(out_boundaries, bounds, (size_t)d * nt * 8, cudaMemcpyDeviceToHost, st));
+      BB_CUDA(cudaMemcpyAsync(out_codes, codes, (size_t)d * n * 2, cudaMemcpyDeviceToHost, st));
+      BB_CUDA(cudaStreamSynchronize(st));
+    };
+    if (x_dtype == BB_F32) body(float{});
+    else if (x_dtype == BB_F64) body(double{});
+    else throw InvalidArg{"x_dtype must be BB_F32 or BB_F64"};
+  });
+}
+
+int bb_layer_hist(bb_ctx* ctx, const uint16_t* codes, const uint16_t* node, const int64_t* q, int64_t n, int64_t n_sig,
+                  int32_t d, int32_t levels, int32_t layer, int64_t* out_hist) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg{"null argument"};
+    if (layer < 1 || layer > 15 || levels < 1 || levels > 11) throw InvalidArg{"bad layer/levels"};
+    std::lock_guard<std::mutex> lock(ctx->c.mu);
+    Ctx& c = ctx->c;
+    BB_CUDA(cudaSetDevice(c.device));
+    cudaStream_t st = c.stream;
+    Arena A(st);
+    const int B = 1 << levels;
+    uint16_t* cd = A.alloc<uint16_t>((size_t)d * n);
+    uint16_t* nd = A.alloc<uint16_t>(n);
+    long long* qd = A.alloc<long long>(n);
+    BB_CUDA(cudaMemcpyAsync(cd, codes, (size_t)d * n * 2, cudaMemcpyHostToDevice, st));
+    BB_CUDA(cudaMemcpyAsync(nd, node, (size_t)n * 2, cudaMemcpyHostToDevice, st));
+    BB_CUDA(cudaMemcpyAsync(qd, q, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    FitShape s{n, n_sig, d, levels, B, layer, 0, 0, 1};
+    const HistPlan p = plan_layer(layer, s, c.sm_count, kHistSmem);
+    const size_t hsz = (size_t)2 * p.nodes * d * B;
+    unsigned long long* hist = A.alloc<unsigned long long>(hsz);
+    BB_CUDA(cudaMemsetAsync(hist, 0, hsz * 8, st));
+    BB_CUDA(cudaFuncSetAttribute(k_layer_hist<uint16_t, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kHistSmem));
+    const int items = (p.chunks_sig + p.chunks_bkg) * p.n_fg * p.n_ng;
+    if (items > 0)
+      k_layer_hist<uint16_t, uint16_t><<<items, 512, (size_t)p.ngs * p.fg * B * 8, st>>>(cd, n, 0, nd, qd, n, n_sig, d, B,
+                                                                                         p, hist);
+    BB_LAUNCH_CHECK();
+    BB_CUDA(cudaMemcpyAsync(out_hist, hist, hsz * 8, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int bb_split(bb_ctx* ctx, const int64_t* hist, int32_t d, int32_t levels, int32_t layer, int32_t final_layer,
+             int32_t shift, const double* boundaries, uint8_t* out_valid, int32_t* out_feature, int32_t* out_cut,
+             double* out_gain, double* out_threshold) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArg{"null argument"};
+    if (layer < 1 || layer > 15 || levels < 1 || levels > 11) throw InvalidArg{"bad layer/levels"};
+    std::lock_guard<std::mutex> lock(ctx->c.mu);
+    Ctx& c = ctx->c;
+    BB_CUDA(cudaSetDevice(c.device));
+    cudaStream_t st = c.stream;
+    Arena A(st);
+    const int B = 1 << levels, nodes = 1 << (layer - 1), start = nodes - 1;
+    const int n_internal = 2 * nodes - 1;  // heap ids 0 .. start+nodes-1
+    const size_t hsz = (size_t)2 * nodes * d * B;
+    unsigned long long* hd = A.alloc<unsigned long long>(hsz);
+    BB_CUDA(cudaMemcpyAsync(hd, hist, hsz * 8, cudaMemcpyHostToDevice, st));
+    double* bd = A.alloc<double>((size_t)d * (B - 1));
+    BB_CUDA(cudaMemcpyAsync(bd, boundaries, (size_t)d * (B - 1) * 8, cudaMemcpyHostToDevice, st));
+    TreeArrays ta;
+    ta.feature = A.alloc<int>(n_internal);
+    ta.cut = A.alloc<int>(n_internal);
+    ta.valid = A.alloc<unsigned char>(n_internal);
+    ta.gain = A.alloc<double>(n_internal);
+    ta.thr = A.alloc<double>(n_internal);
+    ta.nw = nullptr;
+    ta.pur = nullptr;
+    ta.forced = nullptr;
+    SplitScratch sc;
+    sc.best_gain = A.alloc<double>((size_t)nodes * d);
+    sc.best_flat = A.alloc<int>((size_t)nodes * d);
+    sc.forced_gain = A.alloc<double>(nodes);
+    sc.done = A.alloc<unsigned int>(nodes);
+    BB_CUDA(cudaMemsetAsync(sc.done, 0, (size_t)nodes * 4, st));
+    const int n_fc_want = std::max(1, std::min<int>(d, (2 * c.sm_count + nodes - 1) / nodes));
+    const int fc_size = (int)ceil_div(d, n_fc_want);
+    const int n_fc = (int)ceil_div(d, fc_size);
+    k_split<256><<<dim3(nodes, n_fc), 256, 0, st>>>(hd, d, B, start, nodes, fc_size, final_layer, std::ldexp(1.0, -shift),
+                                                   0, n_internal, ta, bd, sc);
+    BB_LAUNCH_CHECK();
+    BB_CUDA(cudaMemcpyAsync(out_valid, ta.valid + start, nodes, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaMemcpyAsync(out_feature, ta.feature + start, (size_t)nodes * 4, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaMemcpyAsync(out_cut, ta.cut + start, (size_t)nodes * 4, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaMemcpyAsync(out_gain, ta.gain + start, (size_t)nodes * 8, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaMemcpyAsync(out_threshold, ta.thr + start, (size_t)nodes * 8, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int bb_subsample_masks(int64_t n_sig, int64_t n_bkg, double rate, int32_t n_trees, const bb_fit_config* rng,
+                       uint32_t* out_bits) {
+  return guarded([&] {
+    if (!rng || !out_bits) throw InvalidArg{"null argument"};
+    if (!(rate > 0.0 && rate <= 1.0)) throw InvalidArg{"subsample rate must be in (0, 1]"};
+    Pcg64 g;
+    g.state = ((unsigned __int128)rng->pcg_state_hi << 64) | rng->pcg_state_lo;
+    g.inc = ((unsigned __int128)rng->pcg_inc_hi << 64) | rng->pcg_inc_lo;
+    g.has_uint32 = rng->pcg_has_uint32;
+    g.uinteger = rng->pcg_uinteger;
+    const int64_t words = ceil_div(n_sig + n_bkg, 32);
+    std::vector<uint32_t> perm;
+    for (int t = 0; t < n_trees; ++t) subsample_tree(g, n_sig, n_bkg, rate, out_bits + (size_t)t * words, perm);
+  });
+}
+
+double bb_pairwise_sum(const double* a, int64_t n) { return pairwise(a, n); }
+
+}  // extern "C"

@@ -1,0 +1,382 @@
+// Per-tree kernels of the boosting loop (reference trees.py:139-315,
+// boosting.py:109-114,165-171).  Data layout in HBM:
+//   codes  [d][stride]   u8|u16 bin codes, column-major, class-block row order
+//   node   [n]           u8|u16 heap node id of every row
+//   q      [n]           int64 fixed-point effective weight, 0 when inactive
+//   F, w   [n]           float64 score, user weight (w may be absent = 1.0)
+//   mask   [n/32]        u32 active bits of the current tree
+//   hist   [2][nodes][d][B]  int64 per-layer (class, node, feature, code-1)
+#pragma once
+#include "common.cuh"
+
+namespace bb {
+
+struct TreeArrays {  // device, all trees
+  int* feature;      // [T][I]
+  int* cut;          // [T][I]
+  unsigned char* valid;
+  double* gain;
+  double* thr;
+  double* nw;        // [T][N] shrunk node weights
+  double* pur;       // [T][N]
+  const int* forced; // [T][I] -2: free, -1: forced invalid, else f*65536+cut
+};
+
+__device__ __forceinline__ int row_label(int64_t i, int64_t n_sig) { return i < n_sig ? 1 : -1; }
+
+// r = 2y*expit(-2yF) = (2y) * (1/(1+exp(2yF)))  (boosting.py:109-114; expit
+// is 1/(1+exp(-x)) bit-for-bit).  Explicit _rn intrinsics keep
+// the compiler from contracting into FMAs.
+__device__ __forceinline__ double residual_of(double F, int lab) {
+  const double two_y = 2.0 * (double)lab;
+  const double e = exp(__dmul_rn(two_y, F));
+  const double s = __ddiv_rn(1.0, __dadd_rn(1.0, e));
+  return __dmul_rn(two_y, s);
+}
+__device__ __forceinline__ double boost_weight_of(double r) {
+  const double a = fabs(r);
+  return __dmul_rn(a, __dsub_rn(2.0, a));
+}
+
+__global__ void k_fill_f64(double* __restrict__ a, int64_t n, double v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) a[i] = v;
+}
+__global__ void k_iota(int* __restrict__ a, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) a[i] = (int)i;
+}
+
+// ---------------------------------------------------------------- refresh
+// F += gamma_prev[node] (score update of the previous tree, all rows), then
+// responses, boost weights and the quantised effective weight of tree t.
+template <typename NodeT>
+__global__ void k_update_refresh(int64_t n, int64_t n_sig, double* __restrict__ F, NodeT* __restrict__ node,
+                                 const double* __restrict__ w, long long* __restrict__ q,
+                                 const unsigned int* __restrict__ mask, const double* __restrict__ nw_prev,
+                                 double two_s) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double f = F[i];
+    if (nw_prev) {
+      f = __dadd_rn(f, nw_prev[node[i]]);
+      F[i] = f;
+    }
+    const int lab = row_label(i, n_sig);
+    const double r = residual_of(f, lab);
+    const double bw = boost_weight_of(r);
+    const bool act = (mask[i >> 5] >> (i & 31)) & 1u;
+    const double wi = w ? w[i] : 1.0;
+    q[i] = act ? __double2ll_rn(__dmul_rn(__dmul_rn(wi, bw), two_s)) : 0ll;
+    node[i] = 0;
+  }
+}
+
+// final score update only (after the last tree, optional)
+template <typename NodeT>
+__global__ void k_update_scores(int64_t n, double* __restrict__ F, const NodeT* __restrict__ node,
+                                const double* __restrict__ nw) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    F[i] = __dadd_rn(F[i], nw[node[i]]);
+}
+
+// ---------------------------------------------------------------- histogram
+// One launch per layer builds signal and background histograms for every
+// node x feature (trees.py:139-167).  CTA work item = (row chunk of one class
+// block, feature group, node group); its (node, feature, code) slots live in
+// shared memory as 2-limb int64 (slot_add), then merge into the global
+// histogram with native 64-bit global reductions.  Rows parked above the
+// layer, inactive rows (q == 0) and missing codes (slot 0 is never read by
+// the split search, trees.py:181-186) are skipped.
+struct HistPlan {
+  int start, nodes;        // layer_start, nodes in layer
+  int fg, n_fg;            // features per group, groups
+  int ngs, n_ng;           // nodes per node group, node groups
+  int chunks_sig, chunks_bkg;
+  int64_t chunk_rows;
+};
+
+template <typename CodeT, typename NodeT>
+__global__ void __launch_bounds__(512) k_layer_hist(const CodeT* __restrict__ codes, int64_t stride, int code_off,
+                                                    const NodeT* __restrict__ node, const long long* __restrict__ q,
+                                                    int64_t n, int64_t n_sig, int d, int B, HistPlan p,
+                                                    unsigned long long* __restrict__ hist) {
+  extern __shared__ uint32_t s_slots[];
+  int item = blockIdx.x;
+  const int fgi = item % p.n_fg;
+  item /= p.n_fg;
+  const int ngi = item % p.n_ng;
+  const int chunk = item / p.n_ng;
+  int cls;
+  int64_t lo, hi;
+  if (chunk < p.chunks_sig) {
+    cls = 0;
+    lo = (int64_t)chunk * p.chunk_rows;
+    hi = min(n_sig, lo + p.chunk_rows);
+  } else {
+    cls = 1;
+    lo = n_sig + (int64_t)(chunk - p.chunks_sig) * p.chunk_rows;
+    hi = min(n, lo + p.chunk_rows);
+  }
+  const int f0 = fgi * p.fg;
+  const int fcount = min(p.fg, d - f0);
+  const int n0 = ngi * p.ngs;
+  const int ncount = min(p.ngs, p.nodes - n0);
+  const int nslots = ncount * fcount * B;
+  for (int i = threadIdx.x; i < 2 * nslots; i += blockDim.x) s_slots[i] = 0u;
+  __syncthreads();
+  const int start = p.start + n0;
+  for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
+    const int nd = (int)node[r] - start;
+    if (nd < 0 || nd >= ncount) continue;  // parked above this layer / other node group
+    const long long qq = q[r];
+    if (qq == 0) continue;                 // inactive row or zero weight
+    uint32_t* base = s_slots + 2 * (nd * fcount) * B;
+    const CodeT* cp = codes + (int64_t)f0 * stride + r;
+    for (int j = 0; j < fcount; ++j) {
+      const int c = (int)cp[(int64_t)j * stride] + code_off;
+      if (c != 0) slot_add(base + 2 * (j * B + c - 1), qq);
+    }
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < nslots; s += blockDim.x) {
+    const long long v = slot_value(s_slots + 2 * s);
+    if (v != 0) {
+      const int b = s % B;
+      const int j = (s / B) % fcount;
+      const int nd = s / (B * fcount);
+      const int64_t g = (((int64_t)cls * p.nodes + (n0 + nd)) * d + (f0 + j)) * B + b;
+      atomicAdd(&hist[g], as_ull(v));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- split
+// CPH prefix scan + separation gain + argmax (trees.py:117-136,170-204),
+// fixed-point definition shared with oracle/binboost_np.py:_gains_fixed.
+// Grid (nodes, feature chunks); each CTA scans its features' signal and
+// background histograms, keeps the first maximum over flat (f, c-1), and the
+// last CTA of a node reduces the chunks and writes the cut.
+struct SplitScratch {
+  double* best_gain;       // [nodes][n_fc]
+  int* best_flat;          // [nodes][n_fc]
+  double* forced_gain;     // [nodes]
+  unsigned int* done;      // [nodes]
+};
+
+__device__ __forceinline__ double g_term(long long s_q, long long b_q, double scale) {
+  const long long den_q = s_q + b_q;
+  if (den_q <= 0) return 0.0;
+  const double s = __dmul_rn((double)s_q, scale);
+  const double den = __dmul_rn((double)den_q, scale);
+  return __ddiv_rn(__dmul_rn(s, s), den);
+}
+
+__device__ __forceinline__ bool better(double g, int flat, double bg, int bflat) {
+  return (g > bg) || (g == bg && flat < bflat);
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restrict__ hist_u, int d, int B, int start,
+                                                   int nodes, int fc_size, int final_layer, double scale, int tree,
+                                                   int n_internal, TreeArrays ta, const double* __restrict__ bounds,
+                                                   SplitScratch sc) {
+  long long* hist = reinterpret_cast<long long*>(hist_u);
+  const int node = blockIdx.x;
+  const int fci = blockIdx.y;
+  const int n_fc = gridDim.y;
+  const int heap = start + node;
+  const int fc = ta.forced ? ta.forced[(int64_t)tree * n_internal + heap] : -2;
+  const int per = (B + THREADS - 1) / THREADS;  // consecutive codes per thread (<= 8)
+  __shared__ long long s_ws[THREADS / 32], s_wb[THREADS / 32];
+  __shared__ double s_bg[THREADS / 32];
+  __shared__ int s_bf[THREADS / 32];
+  double best_g = -INFINITY;
+  int best_flat = 0x7fffffff;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int fbeg = fci * fc_size, fend = min(d, fbeg + fc_size);
+  for (int f = fbeg; f < fend; ++f) {
+    long long* hs = hist + ((int64_t)node * d + f) * B;
+    long long* hb = hist + (((int64_t)nodes + node) * d + f) * B;
+    long long vs[8], vb[8];
+    long long ts = 0, tb = 0;
+    const int c0 = threadIdx.x * per;
+    for (int j = 0; j < per; ++j) {
+      const int c = c0 + j;
+      vs[j] = (c < B) ? hs[c] : 0;
+      vb[j] = (c < B) ? hb[c] : 0;
+      ts += vs[j];
+      tb += vb[j];
+    }
+    // block-wide exclusive scan of (ts, tb)
+    long long is = ts, ib = tb;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long us = __shfl_up_sync(0xffffffffu, is, o);
+      const long long ub = __shfl_up_sync(0xffffffffu, ib, o);
+      if (lane >= o) { is += us; ib += ub; }
+    }
+    if (lane == 31) { s_ws[warp] = is; s_wb[warp] = ib; }
+    __syncthreads();
+    long long off_s = 0, off_b = 0, tot_s = 0, tot_b = 0;
+    for (int w = 0; w < THREADS / 32; ++w) {
+      if (w < warp) { off_s += s_ws[w]; off_b += s_wb[w]; }
+      tot_s += s_ws[w];
+      tot_b += s_wb[w];
+    }
+    __syncthreads();
+    long long cs = off_s + is - ts, cb = off_b + ib - tb;
+    for (int j = 0; j < per; ++j) {
+      const int c = c0 + j;  // 0-based code index: cut bin c+1 keeps codes 1..c+1 left
+      cs += vs[j];
+      cb += vb[j];
+      if (c >= B - 1) break;
+      const long long rs = tot_s - cs, rb = tot_b - cb;
+      double g = -INFINITY;
+      if (cs + cb > 0 && rs + rb > 0)
+        g = __dsub_rn(__dadd_rn(g_term(cs, cb, scale), g_term(rs, rb, scale)), g_term(tot_s, tot_b, scale));
+      const int flat = f * (B - 1) + c;
+      if (better(g, flat, best_g, best_flat)) { best_g = g; best_flat = flat; }
+      if (fc >= 0 && (fc >> 16) == f && (fc & 0xffff) == c + 1) sc.forced_gain[node] = g;
+    }
+    // consume then zero the histogram for the next layer
+    for (int j = 0; j < per; ++j) {
+      const int c = c0 + j;
+      if (c < B) { hs[c] = 0; hb[c] = 0; }
+    }
+  }
+  // block argmax
+  for (int o = 16; o > 0; o >>= 1) {
+    const double og = __shfl_down_sync(0xffffffffu, best_g, o);
+    const int of = __shfl_down_sync(0xffffffffu, best_flat, o);
+    if (better(og, of, best_g, best_flat)) { best_g = og; best_flat = of; }
+  }
+  if (lane == 0) { s_bg[warp] = best_g; s_bf[warp] = best_flat; }
+  __syncthreads();
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < THREADS / 32; ++w)
+      if (better(s_bg[w], s_bf[w], best_g, best_flat)) { best_g = s_bg[w]; best_flat = s_bf[w]; }
+    sc.best_gain[node * n_fc + fci] = best_g;
+    sc.best_flat[node * n_fc + fci] = best_flat;
+    __threadfence();
+    const unsigned prev = atomicAdd(&sc.done[node], 1u);
+    s_last = (prev == (unsigned)n_fc - 1);
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  double g = -INFINITY;
+  int flat = 0x7fffffff;
+  for (int k = 0; k < n_fc; ++k) {
+    const double kg = ((volatile double*)sc.best_gain)[node * n_fc + k];
+    const int kf = ((volatile int*)sc.best_flat)[node * n_fc + k];
+    if (better(kg, kf, g, flat)) { g = kg; flat = kf; }
+  }
+  sc.done[node] = 0u;
+  const int64_t o = (int64_t)tree * n_internal + heap;
+  bool ok;
+  int f = -1, cut = 0;
+  if (fc == -1) {
+    ok = false;
+  } else if (fc >= 0) {
+    ok = true;
+    f = fc >> 16;
+    cut = fc & 0xffff;
+    g = ((volatile double*)sc.forced_gain)[node];
+  } else {
+    ok = isfinite(g) && (g > 0.0 || (g == 0.0 && !final_layer));
+    if (ok) { f = flat / (B - 1); cut = flat % (B - 1) + 1; }
+  }
+  ta.valid[o] = ok ? 1 : 0;
+  ta.feature[o] = ok ? f : -1;
+  ta.cut[o] = ok ? cut : 0;
+  ta.gain[o] = ok ? g : 0.0;
+  ta.thr[o] = ok ? bounds[(int64_t)f * (B - 1) + cut - 1] : __longlong_as_double(0x7ff8000000000000ll);
+}
+
+// ---------------------------------------------------------------- advance
+// Move every row at the layer to its child (trees.py:207-228 for active rows,
+// which traverse_bins, trees.py:318-330, repeats for all rows): left iff
+// code <= cut; invalid cut or missing code parks the row.  Advancing ALL rows
+// makes the final node the leaf traverse_bins would find.  On the last layer
+// the active rows' (eff, resp) fixed-point sums are accumulated per final
+// node, from which k_node_weights derives every node's sums (trees.py:231-244).
+template <typename CodeT, typename NodeT>
+__global__ void __launch_bounds__(512) k_advance(const CodeT* __restrict__ codes, int64_t stride, int code_off,
+                                                 NodeT* __restrict__ node, int64_t n, int64_t n_sig, int start,
+                                                 int tree, int n_internal, TreeArrays ta, int last_layer, int n_nodes,
+                                                 const long long* __restrict__ q, const unsigned int* __restrict__ mask,
+                                                 const double* __restrict__ F, const double* __restrict__ w,
+                                                 double two_s, unsigned long long* __restrict__ sums) {
+  extern __shared__ uint32_t s_sums[];  // [2 cls][n_nodes][2 kinds] 2-limb
+  const int* feat = ta.feature + (int64_t)tree * n_internal;
+  const int* cutp = ta.cut + (int64_t)tree * n_internal;
+  const unsigned char* vld = ta.valid + (int64_t)tree * n_internal;
+  if (last_layer) {
+    for (int i = threadIdx.x; i < 2 * n_nodes * 2 * 2; i += blockDim.x) s_sums[i] = 0u;
+    __syncthreads();
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int nd = node[i];
+    if (nd >= start && vld[nd]) {
+      const int c = (int)codes[(int64_t)feat[nd] * stride + i] + code_off;
+      if (c != 0) {
+        nd = 2 * nd + 1 + (c > cutp[nd] ? 1 : 0);
+        node[i] = (NodeT)nd;
+      }
+    }
+    if (last_layer && ((mask[i >> 5] >> (i & 31)) & 1u)) {
+      const int lab = row_label(i, n_sig);
+      const int cls = lab > 0 ? 0 : 1;
+      const double r = residual_of(F[i], lab);
+      const double wi = w ? w[i] : 1.0;
+      const long long qr = __double2ll_rn(__dmul_rn(__dmul_rn(wi, r), two_s));
+      uint32_t* s = s_sums + 4 * (cls * n_nodes + nd);
+      slot_add(s, q[i]);
+      slot_add(s + 2, qr);
+    }
+  }
+  if (last_layer) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < 2 * n_nodes * 2; k += blockDim.x) {
+      const long long v = slot_value(s_sums + 2 * k);
+      if (v != 0) atomicAdd(&sums[k], as_ull(v));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- weights
+// Node sums of every node from the final-node sums (subtree totals, exact
+// integers), node weight sum(w r)/sum(w bw) with the 1e-12 guard, purity,
+// shrinkage (trees.py:297-304, boosting.py:168).  One CTA; zeroes sums.
+__global__ void k_node_weights(unsigned long long* __restrict__ sums_u, int n_nodes, int depth, double scale,
+                               double shrinkage, int tree, TreeArrays ta) {
+  extern __shared__ long long s_tot[];  // [2 cls][n_nodes][2]
+  long long* sums = reinterpret_cast<long long*>(sums_u);
+  const int m = 2 * n_nodes * 2;
+  for (int k = threadIdx.x; k < m; k += blockDim.x) {
+    s_tot[k] = sums[k];
+    sums[k] = 0;
+  }
+  __syncthreads();
+  // bottom-up: internal node p (layers depth .. 1) adds its children
+  for (int layer = depth; layer >= 1; --layer) {
+    const int first = (1 << (layer - 1)) - 1, cnt = 1 << (layer - 1);
+    for (int k = threadIdx.x; k < cnt * 4; k += blockDim.x) {
+      const int p = first + (k >> 2), cls = (k >> 1) & 1, kind = k & 1;
+      const int a = 2 * p + 1, b = 2 * p + 2;
+      s_tot[(cls * n_nodes + p) * 2 + kind] += s_tot[(cls * n_nodes + a) * 2 + kind] + s_tot[(cls * n_nodes + b) * 2 + kind];
+    }
+    __syncthreads();
+  }
+  for (int p = threadIdx.x; p < n_nodes; p += blockDim.x) {
+    const long long es = s_tot[(0 * n_nodes + p) * 2 + 0], eb = s_tot[(1 * n_nodes + p) * 2 + 0];
+    const long long rs = s_tot[(0 * n_nodes + p) * 2 + 1], rb = s_tot[(1 * n_nodes + p) * 2 + 1];
+    const double den = __dmul_rn((double)(es + eb), scale);
+    const double num = __dmul_rn((double)(rs + rb), scale);
+    const double esd = __dmul_rn((double)es, scale);
+    const double gam = (fabs(den) >= 1e-12) ? __ddiv_rn(num, den) : 0.0;
+    const double pur = (den >= 1e-12) ? __ddiv_rn(esd, den) : 0.0;
+    ta.nw[(int64_t)tree * n_nodes + p] = __dmul_rn(gam, shrinkage);
+    ta.pur[(int64_t)tree * n_nodes + p] = pur;
+  }
+}
+
+}  // namespace bb

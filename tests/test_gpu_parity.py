@@ -1,0 +1,285 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the
+golden vectors the unmodified reference produced (tests/golden/gen_golden.py).
+
+Bars: boundaries, codes, cut feature/bin/validity,
+thresholds and per-row leaf ids bit-exact; probabilities within 1e-5
+absolute; integer histograms exact vs the fixed-point oracle.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import json
+import math
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.binboost_np import _gains_fixed, _pick_cuts
+from paper_1609_06119_b200 import FitConfig, _lib, bridge, fit_forest, predict_batch
+from paper_1609_06119_b200.datagen import make_config
+
+pytestmark = pytest.mark.gpu
+
+PROB_TOL = 1e-5
+
+
+def sha(a) -> str:
+    return hashlib.sha1(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def gpu_bin(X, levels):
+    X = np.ascontiguousarray(X)
+    dt = _lib.BB_F32 if X.dtype == np.float32 else _lib.BB_F64
+    n, d = X.shape
+    bounds = np.zeros((d, (1 << levels) - 1))
+    codes = np.zeros((d, n), np.int16)
+    _lib.check(_lib.lib().bb_bin(_lib.context(), _lib.ptr(X), dt, n, d, levels, _lib.ptr(bounds), _lib.ptr(codes)))
+    return bounds, codes
+
+
+# ------------------------------------------------------------------ binning
+def test_binning_golden_columns(golden_dir):
+    g = np.load(f"{golden_dir}/binning_random.npz")
+    vals = np.split(g["values"], np.cumsum(g["lengths"])[:-1])
+    bnds = np.split(g["boundaries"], np.cumsum(g["bound_lengths"])[:-1])
+    codes = np.split(g["codes"], np.cumsum(g["lengths"])[:-1])
+    for col, L, b_ref, c_ref in zip(vals, g["levels"], bnds, codes):
+        b, c = gpu_bin(col.reshape(-1, 1), int(L))
+        np.testing.assert_array_equal(b[0], b_ref)
+        np.testing.assert_array_equal(c[0], c_ref)
+
+
+def test_binning_kats(golden_dir):
+    k = json.load(open(f"{golden_dir}/kats.json"))
+    b, _ = gpu_bin(np.arange(1.0, 9.0).reshape(-1, 1), 2)
+    assert b[0].tolist() == k["bounds_1to8_L2"]
+    b, _ = gpu_bin(np.array([[5.0], [5], [5], [5]]), 1)
+    assert b[0].tolist() == k["bounds_5555_L1"]
+    b, _ = gpu_bin(np.array([1.0, 2, np.nan, np.inf, 3, 4]).reshape(-1, 1), 1)
+    assert b[0].tolist() == k["bounds_mixed_L1"]
+
+
+@pytest.mark.parametrize("name,n", [("cfg1", 100_000), ("cfg2", 200_000), ("cfg5", 50_000)])
+def test_binning_configs_vs_oracle(name, n):
+    X, _, _, kw = make_config(name, n=n)
+    L = kw["binning_levels"]
+    for arr in (X, X.astype(np.float64)):
+        b, c = gpu_bin(arr, L)
+        for j in range(X.shape[1]):
+            ref_b = oracle.fit_boundaries(X[:, j], L)
+            np.testing.assert_array_equal(b[j], ref_b)
+            np.testing.assert_array_equal(c[j], oracle.bin_codes(ref_b, X[:, j]))
+
+
+# ------------------------------------------------------------------ histogram
+def _random_layer(rng, n, n_sig, d, levels, layer, nan_rate=0.05, neg=True):
+    B = 1 << levels
+    codes = rng.integers(1, B + 1, (d, n)).astype(np.uint16)
+    codes[rng.random((d, n)) < nan_rate] = 0
+    start = (1 << (layer - 1)) - 1
+    node = rng.integers(start, 2 * start + 1, n).astype(np.uint16)
+    parked = rng.random(n) < 0.05
+    node[parked] = rng.integers(0, max(start, 1), parked.sum()) if start > 0 else 0
+    q = rng.integers(0, 1 << 32, n).astype(np.int64)
+    q[rng.random(n) < 0.4] = 0
+    if neg:
+        m = rng.random(n) < 0.05
+        q[m] = -q[m]
+    return codes, node, q
+
+
+def _oracle_hist(codes, node, q, n_sig, d, levels, layer):
+    B = 1 << levels
+    start = (1 << (layer - 1)) - 1
+    nodes = 1 << (layer - 1)
+    out = np.zeros((2, nodes, d, B), np.int64)
+    for cls, sl in ((0, slice(0, n_sig)), (1, slice(n_sig, None))):
+        nd = node[sl].astype(np.int64) - start
+        ok = (nd >= 0) & (nd < nodes)
+        for j in range(d):
+            c = codes[j, sl].astype(np.int64)
+            m = ok & (c > 0)
+            flat = nd[m] * B + (c[m] - 1)
+            out[cls, :, j, :] = oracle.binboost_np._exact_int_bincount(flat, q[sl][m], nodes * B).reshape(nodes, B)
+    return out
+
+
+@pytest.mark.parametrize("levels,layer,d", [(8, 1, 10), (8, 3, 40), (8, 5, 7), (10, 6, 3), (3, 2, 5), (1, 1, 2)])
+def test_layer_hist_exact(levels, layer, d):
+    rng = np.random.default_rng(levels * 100 + layer)
+    n, n_sig = 60_000, 23_456
+    codes, node, q = _random_layer(rng, n, n_sig, d, levels, layer)
+    B = 1 << levels
+    nodes = 1 << (layer - 1)
+    out = np.zeros((2, nodes, d, B), np.int64)
+    _lib.check(_lib.lib().bb_layer_hist(_lib.context(), _lib.ptr(codes), _lib.ptr(node), _lib.ptr(q), n, n_sig, d,
+                                        levels, layer, _lib.ptr(out)))
+    np.testing.assert_array_equal(out, _oracle_hist(codes, node, q, n_sig, d, levels, layer))
+
+
+@pytest.mark.parametrize("levels,layer,d,final", [(8, 1, 10, 0), (8, 3, 40, 1), (4, 4, 3, 0), (2, 2, 2, 1)])
+def test_split_exact(levels, layer, d, final):
+    rng = np.random.default_rng(7 + levels + layer)
+    n, n_sig = 30_000, 12_000
+    codes, node, q = _random_layer(rng, n, n_sig, d, levels, layer, neg=False)
+    q = (q >> 1)
+    B = 1 << levels
+    nodes = 1 << (layer - 1)
+    hist = _oracle_hist(codes, node, q, n_sig, d, levels, layer)
+    # discrete-like ties: duplicate a feature so equal gains occur
+    if d >= 2:
+        hist[:, :, 1, :] = hist[:, :, 0, :]
+    bounds = np.sort(rng.normal(size=(d, B - 1)), axis=1)
+    shift = 32
+    v = np.zeros(nodes, np.uint8)
+    f = np.zeros(nodes, np.int32)
+    c = np.zeros(nodes, np.int32)
+    g = np.zeros(nodes)
+    t = np.zeros(nodes)
+    _lib.check(_lib.lib().bb_split(_lib.context(), _lib.ptr(hist), d, levels, layer, final, shift, _lib.ptr(bounds),
+                                   _lib.ptr(v), _lib.ptr(f), _lib.ptr(c), _lib.ptr(g), _lib.ptr(t)))
+    # oracle: cumulative layout (nodes, d, B+1) with slot 0 = NaN (unused)
+    cum = [np.concatenate([np.zeros((nodes, d, 1), np.int64), np.cumsum(hist[k], axis=2)], axis=2) for k in (0, 1)]
+    scored = _gains_fixed(cum[0], cum[1], B, 2.0 ** -shift)
+    ref = _pick_cuts(scored, B, bool(final), {})
+    for k, (ok, rf, rc, rg) in enumerate(ref):
+        assert bool(v[k]) == ok, k
+        if ok:
+            assert (f[k], c[k]) == (rf, rc), k
+            assert g[k] == rg, k
+            assert t[k] == bounds[rf][rc - 1]
+
+
+# ------------------------------------------------------------------ full fit
+def _forced_from_golden(g, gap_tol=1e-9):
+    """Teacher-forced protocol: nodes whose reference
+    argmax is within rounding noise take the reference's decision."""
+    forced = {}
+    for t, node, gap, pure in g["audit"]:
+        t, node = int(t), int(node)
+        if gap < gap_tol or pure:
+            forced[(t, node)] = (bool(g["valid"][t, node]), int(g["feature"][t, node]), int(g["cut_bin"][t, node]))
+    return forced
+
+
+def _check_fit_vs_golden(forest, g, rows_X, forced_ok=True):
+    T = int(g["n_trees"])
+    np.testing.assert_array_equal(np.stack([b.boundaries for b in forest.binnings]), g["boundaries"])
+    for t in range(T):
+        tr = forest.trees[t]
+        np.testing.assert_array_equal(tr.valid, g["valid"][t], err_msg=f"tree {t}")
+        np.testing.assert_array_equal(tr.feature, g["feature"][t], err_msg=f"tree {t}")
+        np.testing.assert_array_equal(tr.cut_bin, g["cut_bin"][t], err_msg=f"tree {t}")
+        np.testing.assert_array_equal(tr.threshold, g["threshold"][t], err_msg=f"tree {t}")
+        lv = forest.fit_info["leaves"][t].astype(np.int16)
+        assert sha(lv) == g["leaf_hashes"][t], f"leaf ids differ at tree {t}"
+        # node weights come from fixed-point sums: not a bit-exact quantity;
+        # the contract on them is the probability bar below
+        np.testing.assert_allclose(tr.node_weight, g["node_weight"][t], rtol=1e-4, atol=1e-6)
+    p = predict_batch(forest, rows_X)
+    assert np.max(np.abs(p - g["pred"])) <= PROB_TOL
+
+
+def test_fit_cfg1_vs_reference_golden(golden_dir):
+    g = np.load(f"{golden_dir}/cfg1_fit.npz")
+    X, y, w, kw = make_config("cfg1")
+    cfg = FitConfig(n_trees=kw["trees"], depth=kw["depth"], shrinkage=kw["shrinkage"], subsample=kw["subsample"],
+                    binning_levels=kw["binning_levels"], seed=kw["seed"])
+    forced = _forced_from_golden(g)
+    assert not forced, "cfg1 has no tie-ambiguous nodes (SURVEY.md A4): free-running parity"
+    forest = fit_forest(X, y, w, cfg, return_leaves=True)
+    assert forest.f0 == float(g["f0"])
+    _check_fit_vs_golden(forest, g, X[g["pred_rows"]])
+
+
+def test_fit_vs_fixed_point_oracle():
+    X, y, w, _ = make_config("cfg2", n=60_000)
+    cfg = FitConfig(n_trees=12, depth=4, shrinkage=0.2, subsample=0.6, binning_levels=6, seed=11)
+    forest = fit_forest(X, y, w, cfg, return_leaves=True, return_scores=True)
+    ref = oracle.fit_forest(X, y, w, n_trees=12, depth=4, shrinkage=0.2, subsample=0.6, levels=6, seed=11,
+                            fixed_point=True, record_leaves=True)
+    assert forest.fit_info["fixed_shift"] == ref.fixed_shift
+    for t in range(12):
+        tr = forest.trees[t]
+        np.testing.assert_array_equal(tr.feature, ref.feature[t])
+        np.testing.assert_array_equal(tr.cut_bin, ref.cut_bin[t])
+        np.testing.assert_array_equal(tr.valid, ref.valid[t])
+        np.testing.assert_array_equal(forest.fit_info["leaves"][t], ref.leaves[t].astype(np.uint16))
+        np.testing.assert_allclose(tr.node_weight, ref.node_weight[t], rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(tr.gain, ref.gain[t], rtol=1e-9, atol=1e-12)
+
+
+def test_small_fits_vs_reference_golden(golden_dir):
+    z = np.load(f"{golden_dir}/small_fits.npz")
+    n_cases = len({k.split("__")[0] for k in z.files})
+    forced_total = 0
+    for i in range(n_cases):
+        g = {k.split("__", 1)[1]: z[k] for k in z.files if k.startswith(f"c{i}__")}
+        T, D, eta, alpha, L, seed = g["config"]
+        cfg = FitConfig(n_trees=int(T), depth=int(D), shrinkage=float(eta), subsample=float(alpha),
+                        binning_levels=int(L), seed=int(seed))
+        forced = _forced_from_golden(g)
+        forced_total += len(forced)
+        forest = fit_forest(g["X"], g["y"], g.get("w"), cfg, forced_cuts=forced, return_leaves=True)
+        assert forest.f0 == float(g["f0"]), i
+        try:
+            _check_fit_vs_golden(forest, g, g["X"][g["pred_rows"]])
+        except AssertionError as e:
+            raise AssertionError(f"case {i}: {e}") from None
+    print("forced nodes across small cases:", forced_total)
+
+
+# ------------------------------------------------------------------ apply
+def test_apply_cfg4_slice_vs_golden(golden_dir):
+    g = np.load(f"{golden_dir}/apply_cfg4_slice.npz")
+    X, _, _, _ = make_config("cfg4", n=20_000)
+    from paper_1609_06119_b200.engine import FeatureBinning, Forest, Tree
+
+    T = g["feature"].shape[0]
+    trees = [Tree(depth=3, feature=g["feature"][t], cut_bin=g["cut_bin"][t], threshold=g["threshold"][t],
+                  gain=np.zeros(7), valid=np.ones(7, bool), node_weight=g["node_weight"][t],
+                  node_purity=np.zeros(15)) for t in range(T)]
+    forest = Forest(f0=0.0, trees=trees, binnings=[FeatureBinning(b, 8) for b in g["boundaries"]])
+    for arr in (X, X.astype(np.float64)):
+        p = predict_batch(forest, arr)
+        assert np.max(np.abs(p - g["pred"])) <= 1e-15
+
+
+def test_apply_nan_and_invalid_nodes():
+    rng = np.random.default_rng(3)
+    X = rng.normal(size=(5000, 4))
+    X[rng.random(X.shape) < 0.2] = np.nan
+    y = (rng.random(5000) < 0.5).astype(int)
+    forest = fit_forest(X, y, None, FitConfig(n_trees=15, depth=4, binning_levels=3, seed=5))
+    ref = oracle.predict_scores(forest.f0, np.stack([t.valid for t in forest.trees]),
+                                np.stack([t.feature for t in forest.trees]),
+                                np.stack([t.threshold for t in forest.trees]),
+                                np.stack([t.node_weight for t in forest.trees]), 4, X)
+    p, F = predict_batch(forest, X, return_scores=True)
+    np.testing.assert_array_equal(F, ref)
+
+
+# ------------------------------------------------------------------ bridge
+def test_bridge_fit_predict_and_concurrency():
+    X, y, w, _ = make_config("cfg1", n=20_000)
+    m = bridge.fit(X, y, w, trees=20, depth=3, seed=3)
+    p = m.predict(X[:1000])
+    assert p.shape == (1000,) and np.all((p > 0) & (p < 1))
+    assert m.predict(np.empty(0)).shape == (0,)
+    results = [None] * 4
+
+    def work(k):
+        results[k] = m.predict(X[:1000])
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    for r in results:
+        np.testing.assert_array_equal(r, p)
+    m.close()
+    with pytest.raises(RuntimeError, match="model handle is closed"):
+        m.predict(X[:3])

@@ -62,7 +62,7 @@ typedef struct {
   int32_t n_trees;
   int32_t depth;
   int32_t binning_levels;
-  int32_t reserved0;
+  int32_t flags;        /* bit 0: time every histogram launch with CUDA events */
   double shrinkage;
   double subsample;
   uint64_t pcg_state_hi, pcg_state_lo;
@@ -93,7 +93,10 @@ typedef struct {
   int64_t* n_sig;       /* [1]  rows in the signal block                */
   uint16_t* leaves;     /* optional [T][n] final node per row, class-block order */
   double* scores;       /* optional [n] final F per row, class-block order */
-  double* timing_ms;    /* optional [8]: upload, binning, trees, download, total */
+  double* timing_ms;    /* optional [16]: [0] upload [1] binning [2] trees [3] download
+                         * [4] host total (ms); [5] device total (CUDA events, ms);
+                         * [6] histogram kernels (ms, flags bit 0); [7] histogram
+                         * launches; [8] all kernel launches; [9] mask generation (host ms) */
 } bb_fit_out;
 
 /* X: row-major (n, d) float32 (BB_F32) or float64 (BB_F64); y01: int8, > 0

@@ -173,16 +173,19 @@ def _pick_cuts(scored, n_bins, final_layer, forced_layer):
     return out
 
 
-def _audit_layer(scored, cum_b_total, cum_s_total, tree_i, start):
+def _audit_layer(scored, mass, cum_s_total, tree_i, start, mass_b_total):
     """Per node: best gain, runner-up DISTINCT gain, relative gap, pure-signal
-    flag (SURVEY.md §7 hard part 2, §8(c) teacher-forced protocol)."""
+    flag, node absolute-mass scale (SURVEY.md §7 hard part 2, §8(c)
+    teacher-forced protocol)."""
     recs = []
     flat = scored.reshape(scored.shape[0], -1)
     for node in range(flat.shape[0]):
         row = flat[node]
         fin = row[np.isfinite(row)]
+        scale = float(np.max(mass[node])) if mass.shape[1] else 0.0
         if fin.size == 0:
-            recs.append(dict(tree=tree_i, node=start + node, best=None, second=None, gap=math.inf, pure_signal=False))
+            recs.append(dict(tree=tree_i, node=start + node, best=None, second=None, gap=math.inf, pure_signal=False,
+                             scale=scale))
             continue
         best = float(fin.max())
         below = fin[fin < best]
@@ -191,8 +194,9 @@ def _audit_layer(scored, cum_b_total, cum_s_total, tree_i, start):
             gap = math.inf
         else:
             gap = (best - second) / max(abs(best), 1e-300)
-        pure = bool(np.all(cum_b_total[node] == 0.0) and np.any(cum_s_total[node] != 0.0))
-        recs.append(dict(tree=tree_i, node=start + node, best=best, second=second, gap=gap, pure_signal=pure))
+        pure = bool(np.all(mass_b_total[node] == 0.0) and np.any(cum_s_total[node] != 0.0))
+        recs.append(dict(tree=tree_i, node=start + node, best=best, second=second, gap=gap, pure_signal=pure,
+                         scale=scale))
     return recs
 
 
@@ -368,7 +372,9 @@ def fit_forest(
             else:
                 scored = _gains_float(hists[0], hists[1], B)
             if audit and not fixed_point:
-                out.audit.extend(_audit_layer(scored, hists[1][:, :, B], hists[0][:, :, B], t, start))
+                mass = np.abs(np.diff(hists[0][:, :, 1:], axis=2, prepend=0.0)).sum(axis=2) + \
+                    np.abs(np.diff(hists[1][:, :, 1:], axis=2, prepend=0.0)).sum(axis=2)
+                out.audit.extend(_audit_layer(scored, mass, hists[0][:, :, B], t, start, hists[1][:, :, B]))
             forced_layer = {node - start: v for (tt, node), v in forced.items() if tt == t and start <= node < start + count}
             cuts = _pick_cuts(scored, B, final, forced_layer)
             for local_i, (ok, f, c, g) in enumerate(cuts):

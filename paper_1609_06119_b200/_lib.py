@@ -27,7 +27,7 @@ class FitConfigC(C.Structure):
         ("n_trees", C.c_int32),
         ("depth", C.c_int32),
         ("binning_levels", C.c_int32),
-        ("reserved0", C.c_int32),
+        ("flags", C.c_int32),
         ("shrinkage", C.c_double),
         ("subsample", C.c_double),
         ("pcg_state_hi", C.c_uint64),

@@ -170,20 +170,28 @@ static typename KeyOf<T>::K* make_keys(Ctx& c, Arena& A, const T* Xd, int64_t n,
 }
 
 // ------------------------------------------------------------- tree loop
+struct FitStats {
+  double mask_ms = 0.0, hist_ms = 0.0;
+  int64_t launches = 0, hist_launches = 0;
+};
+
 struct FitShape {
   int64_t n, n_sig;
   int d, levels, B, depth, n_internal, n_nodes, T;
 };
 
-static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, int64_t smem_budget) {
+template <typename CodeT, typename NodeT>
+static HistPlan plan_layer(int layer, const FitShape& s, int sm_count) {
   HistPlan p{};
   p.nodes = 1 << (layer - 1);
   p.start = p.nodes - 1;
-  const int64_t fn_budget = std::max<int64_t>(1, smem_budget / ((int64_t)s.B * 8));
+  constexpr int64_t kSmemMax = 227 * 1024 - 1024;
+  const int64_t hist_budget = 96 * 1024;
+  const int64_t fn_budget = std::max<int64_t>(1, hist_budget / ((int64_t)s.B * 8));
   if (p.nodes <= fn_budget) {
     p.ngs = p.nodes;
     p.n_ng = 1;
-    int fg = (int)std::min<int64_t>(s.d, fn_budget / p.nodes);
+    const int fg = (int)std::min<int64_t>(s.d, fn_budget / p.nodes);
     p.n_fg = (int)ceil_div(s.d, fg);
     p.fg = (int)ceil_div(s.d, p.n_fg);
   } else {
@@ -192,30 +200,46 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, int64_t s
     p.ngs = (int)fn_budget;
     p.n_ng = (int)ceil_div(p.nodes, p.ngs);
   }
-  const int64_t items = (int64_t)p.n_fg * p.n_ng;
-  const int64_t target = (int64_t)sm_count * 2 * 2;
-  const int64_t chunks = std::max<int64_t>(2, ceil_div(target, items));
-  int64_t cr = std::max<int64_t>(8192, ceil_div(s.n, chunks));
-  cr = ceil_div(cr, 512) * 512;
-  p.chunk_rows = cr;
-  p.chunks_sig = (int)ceil_div(s.n_sig, cr);
-  p.chunks_bkg = (int)ceil_div(s.n - s.n_sig, cr);
+  const int tile = kTile;
+  auto need = [&](int fg) {
+    return (int64_t)align16(p.ngs * fg * s.B * 8) + 2 * (int64_t)hist_buf_bytes<CodeT, NodeT>(tile, fg) + 4 * tile + 64;
+  };
+  while (p.fg > 1 && need(p.fg) > kSmemMax) {
+    p.n_fg += 1;
+    p.fg = (int)ceil_div(s.d, p.n_fg);
+    p.n_fg = (int)ceil_div(s.d, p.fg);
+  }
+  if (need(p.fg) > kSmemMax) throw InvalidArg{"histogram stage does not fit in shared memory"};
+  p.tile = tile;
+  p.smem = (int)need(p.fg);
+  p.tiles_sig0 = 0;
+  p.tiles_sig1 = (int)ceil_div(s.n_sig, tile);
+  p.tiles_bkg0 = (int)(s.n_sig / tile);
+  p.tiles_bkg1 = (int)ceil_div(s.n, tile);
+  const int groups = p.n_fg * p.n_ng;
+  const int total = std::max(2, (int)ceil_div(sm_count, groups));
+  const int ts = p.tiles_sig1 - p.tiles_sig0, tb = p.tiles_bkg1 - p.tiles_bkg0;
+  p.split_sig = std::max(1, std::min(ts, (int)std::llround((double)total * ts / (ts + tb))));
+  p.split_bkg = std::max(1, std::min(tb, total - p.split_sig));
   return p;
 }
 
-constexpr int64_t kHistSmem = 96 * 1024;
+static inline int hist_grid(const HistPlan& p) { return p.n_fg * p.n_ng * (p.split_sig + p.split_bkg); }
 
 template <typename CodeT, typename NodeT>
-static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, int64_t stride, int code_off,
+static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, int code_off,
                       const double* w_cb, double f0, int shift, const bb_fit_config& cfg,
                       const bb_forced_cut* forced, int n_forced, const double* bounds_dev, bb_fit_out* out,
-                      double* t_trees_ms) {
+                      double* t_trees_ms, FitStats& stats) {
   const int64_t n = s.n;
   cudaStream_t st = c.stream;
   const double two_s = std::ldexp(1.0, shift), scale = std::ldexp(1.0, -shift);
+  const int64_t npad = ceil_div(n, kRowPad) * kRowPad;
   double* F = A.alloc<double>(n);
-  NodeT* node = A.alloc<NodeT>(n);
-  long long* q = A.alloc<long long>(n);
+  NodeT* node = A.alloc<NodeT>(npad);
+  long long* q = A.alloc<long long>(npad);
+  BB_CUDA(cudaMemsetAsync(node, 0, (size_t)npad * sizeof(NodeT), st));
+  BB_CUDA(cudaMemsetAsync(q, 0, (size_t)npad * 8, st));
   const int64_t words = ceil_div(n, 32);
   unsigned int* mask = A.alloc<unsigned int>(words);
   const int max_nodes = 1 << (s.depth - 1);
@@ -259,8 +283,8 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   BB_LAUNCH_CHECK();
 
   std::vector<HistPlan> plans(s.depth + 1);
-  for (int l = 1; l <= s.depth; ++l) plans[l] = plan_layer(l, s, c.sm_count, kHistSmem);
-  BB_CUDA(cudaFuncSetAttribute(k_layer_hist<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHistSmem));
+  for (int l = 1; l <= s.depth; ++l) plans[l] = plan_layer<CodeT, NodeT>(l, s, c.sm_count);
+  BB_CUDA(cudaFuncSetAttribute(k_layer_hist<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
 
   // host subsample bits, double-buffered in pinned memory
   Pcg64 g;
@@ -276,6 +300,14 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   BB_CUDA(cudaEventCreateWithFlags(&copied[1], cudaEventDisableTiming));
   std::vector<uint32_t> perm;
   std::vector<NodeT> leaf_tmp;
+  const bool prof = (cfg.flags & 1) != 0;
+  std::vector<cudaEvent_t> hev;
+  auto hist_event = [&]() {
+    cudaEvent_t e;
+    BB_CUDA(cudaEventCreate(&e));
+    BB_CUDA(cudaEventRecord(e, st));
+    hev.push_back(e);
+  };
   const int gridN = grid_for(n, 256, c.sm_count);
   const int gridA = grid_for(n, 512, c.sm_count, 4);
   const auto t0 = std::chrono::steady_clock::now();
@@ -283,19 +315,24 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
     for (int t = 0; t < s.T; ++t) {
       unsigned int* hb = pinned[t & 1];
       if (t >= 2) BB_CUDA(cudaEventSynchronize(copied[t & 1]));
+      const auto tm = std::chrono::steady_clock::now();
       subsample_tree(g, s.n_sig, s.n - s.n_sig, cfg.subsample, hb, perm);
+      stats.mask_ms += elapsed_ms(tm);
       BB_CUDA(cudaMemcpyAsync(mask, hb, (size_t)words * 4, cudaMemcpyHostToDevice, st));
       BB_CUDA(cudaEventRecord(copied[t & 1], st));
       k_update_refresh<NodeT><<<gridN, 256, 0, st>>>(n, s.n_sig, F, node, w_cb, q, mask,
                                                       t > 0 ? ta.nw + (size_t)(t - 1) * s.n_nodes : nullptr, two_s);
       BB_LAUNCH_CHECK();
+      stats.launches += 1;
       for (int layer = 1; layer <= s.depth; ++layer) {
         const HistPlan& p = plans[layer];
-        const int items = (p.chunks_sig + p.chunks_bkg) * p.n_fg * p.n_ng;
-        const size_t smem = (size_t)p.ngs * p.fg * s.B * 8;
-        k_layer_hist<CodeT, NodeT><<<items, 512, smem, st>>>(codes, stride, code_off, node, q, n, s.n_sig, s.d, s.B, p,
-                                                               hist);
+        if (prof) hist_event();
+        k_layer_hist<CodeT, NodeT><<<hist_grid(p), kHistThreads, p.smem, st>>>(codes, code_off, node, q, n, s.n_sig,
+                                                                               s.d, s.B, p, hist);
         BB_LAUNCH_CHECK();
+        if (prof) hist_event();
+        stats.launches += 3;
+        stats.hist_launches += 1;
         const int nodes = p.nodes;
         const int n_fc_want = std::max(1, std::min(s.d, (2 * c.sm_count + nodes - 1) / nodes));
         const int fc_size = (int)ceil_div(s.d, n_fc_want);
@@ -306,13 +343,14 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         BB_LAUNCH_CHECK();
         const bool last = layer == s.depth;
         k_advance<CodeT, NodeT><<<gridA, 512, last ? (size_t)32 * s.n_nodes : 0, st>>>(
-            codes, stride, code_off, node, n, s.n_sig, p.start, t, s.n_internal, ta, last ? 1 : 0, s.n_nodes, q, mask,
+            codes, s.d, code_off, node, n, s.n_sig, p.start, t, s.n_internal, ta, last ? 1 : 0, s.n_nodes, q, mask,
             F, w_cb, two_s, sums);
         BB_LAUNCH_CHECK();
       }
       k_node_weights<<<1, 256, (size_t)2 * s.n_nodes * 2 * 8, st>>>(sums, s.n_nodes, s.depth, scale, cfg.shrinkage, t,
                                                                     ta);
       BB_LAUNCH_CHECK();
+      stats.launches += 1;
       if (out->leaves) {
         leaf_tmp.resize(n);
         BB_CUDA(cudaMemcpyAsync(leaf_tmp.data(), node, (size_t)n * sizeof(NodeT), cudaMemcpyDeviceToHost, st));
@@ -327,8 +365,15 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
       BB_CUDA(cudaMemcpyAsync(out->scores, F, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
     }
     BB_CUDA(cudaStreamSynchronize(st));
+    for (size_t k = 0; k + 1 < hev.size(); k += 2) {
+      float ms = 0.f;
+      BB_CUDA(cudaEventElapsedTime(&ms, hev[k], hev[k + 1]));
+      stats.hist_ms += ms;
+    }
+    for (auto e : hev) cudaEventDestroy(e);
   } catch (...) {
     cudaStreamSynchronize(st);
+    for (auto e : hev) cudaEventDestroy(e);
     cudaFreeHost(pinned[0]);
     cudaFreeHost(pinned[1]);
     cudaEventDestroy(copied[0]);
@@ -360,6 +405,15 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   using K = typename KeyOf<T>::K;
   const auto t_all = std::chrono::steady_clock::now();
   cudaStream_t st = c.stream;
+  cudaEvent_t ev0, ev1;
+  BB_CUDA(cudaEventCreate(&ev0));
+  BB_CUDA(cudaEventCreate(&ev1));
+  BB_CUDA(cudaEventRecord(ev0, st));
+  FitStats stats;
+  struct EvGuard {
+    cudaEvent_t a, b;
+    ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
+  } evg{ev0, ev1};
   Arena A(st);
   const int levels = cfg.binning_levels, B = 1 << levels, nt = B - 1;
   // ---- upload
@@ -411,7 +465,7 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   if (n_sig == 0 || n_sig == n) throw InvalidArg{"training data must contain both classes"};
   bool any_nan = false;
   for (int f = 0; f < d; ++f) any_nan |= nans[f] > 0;
-  const int64_t stride = ceil_div(n, 64) * 64;
+  const int64_t stride = ceil_div(n, kTile) * kTile;  // rows incl. tile padding
   FitShape s{n, n_sig, d, levels, B, cfg.depth, (1 << cfg.depth) - 1, (1 << (cfg.depth + 1)) - 1, cfg.n_trees};
   // prior (boosting.py:76-83) and the fixed-point shift from the user weights
   double w_sig, w_bkg, max_abs = 1.0;
@@ -436,7 +490,7 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   auto launch_codes = [&](auto* codes, int off) {
     using CodeT = std::remove_pointer_t<decltype(codes)>;
     k_codes<K, CodeT><<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256 * 4), 4 * c.sm_count / d + 1)), d),
-                        256, (size_t)nt * sizeof(K), st>>>(keys, n, nt, bkeys, pos, codes, stride, off);
+                        256, (size_t)nt * sizeof(K), st>>>(keys, n, nt, bkeys, pos, codes, stride, off, d, 1);
     BB_LAUNCH_CHECK();
   };
   auto after_codes = [&]() {
@@ -450,9 +504,9 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
     BB_CUDA(cudaStreamSynchronize(st));
     ms_bin = elapsed_ms(t_bin);
     if (s.depth <= 7)
-      run_trees<CodeT, uint8_t>(c, A, s, codes, stride, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees);
+      run_trees<CodeT, uint8_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees, stats);
     else
-      run_trees<CodeT, uint16_t>(c, A, s, codes, stride, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees);
+      run_trees<CodeT, uint16_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees, stats);
   };
   if (B <= 255) {
     go(A.alloc<uint8_t>((size_t)d * stride), 0);
@@ -463,7 +517,10 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   }
   auto t_dn = std::chrono::steady_clock::now();
   BB_CUDA(cudaMemcpyAsync(out->boundaries, bounds, (size_t)d * nt * 8, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaEventRecord(ev1, st));
   BB_CUDA(cudaStreamSynchronize(st));
+  float dev_ms = 0.f;
+  BB_CUDA(cudaEventElapsedTime(&dev_ms, ev0, ev1));
   *out->f0 = f0;
   *out->fixed_shift = shift;
   if (out->n_sig) *out->n_sig = n_sig;
@@ -473,6 +530,11 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
     out->timing_ms[2] = ms_trees;
     out->timing_ms[3] = elapsed_ms(t_dn);
     out->timing_ms[4] = elapsed_ms(t_all);
+    out->timing_ms[5] = dev_ms;
+    out->timing_ms[6] = stats.hist_ms;
+    out->timing_ms[7] = (double)stats.hist_launches;
+    out->timing_ms[8] = (double)(stats.launches + 9 + 2 * (KeyOf<T>::BITS == 32 ? 4 : 8));
+    out->timing_ms[9] = stats.mask_ms;
   }
 }
 
@@ -651,7 +713,7 @@ int bb_bin(bb_ctx* ctx, const void* X, int32_t x_dtype, int64_t n, int32_t d, in
       BB_LAUNCH_CHECK();
       uint16_t* codes = A.alloc<uint16_t>((size_t)d * n);
       k_codes<K, uint16_t><<<dim3((unsigned)std::max<int64_t>(1, ceil_div(n, 1024)), d), 256, (size_t)nt * sizeof(K), st>>>(
-          keys, n, nt, bkeys, pos, codes, n, 0);
+          keys, n, nt, bkeys, pos, codes, n, 0, d, 0);
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaMemcpyAsync(out_boundaries, bounds, (size_t)d * nt * 8, cudaMemcpyDeviceToHost, st));
       BB_CUDA(cudaMemcpyAsync(out_codes, codes, (size_t)d * n * 2, cudaMemcpyDeviceToHost, st));
@@ -674,23 +736,28 @@ int bb_layer_hist(bb_ctx* ctx, const uint16_t* codes, const uint16_t* node, cons
     cudaStream_t st = c.stream;
     Arena A(st);
     const int B = 1 << levels;
-    uint16_t* cd = A.alloc<uint16_t>((size_t)d * n);
-    uint16_t* nd = A.alloc<uint16_t>(n);
-    long long* qd = A.alloc<long long>(n);
-    BB_CUDA(cudaMemcpyAsync(cd, codes, (size_t)d * n * 2, cudaMemcpyHostToDevice, st));
+    const int64_t npad = ceil_div(n, kRowPad) * kRowPad;
+    std::vector<uint16_t> tiled((size_t)d * npad, 0);
+    for (int f = 0; f < d; ++f)
+      for (int64_t i = 0; i < n; ++i) tiled[(size_t)code_index(i, f, d)] = codes[(size_t)f * n + i];
+    uint16_t* cd = A.alloc<uint16_t>((size_t)d * npad);
+    uint16_t* nd = A.alloc<uint16_t>(npad);
+    long long* qd = A.alloc<long long>(npad);
+    BB_CUDA(cudaMemsetAsync(nd, 0, (size_t)npad * 2, st));
+    BB_CUDA(cudaMemsetAsync(qd, 0, (size_t)npad * 8, st));
+    BB_CUDA(cudaMemcpyAsync(cd, tiled.data(), (size_t)d * npad * 2, cudaMemcpyHostToDevice, st));
     BB_CUDA(cudaMemcpyAsync(nd, node, (size_t)n * 2, cudaMemcpyHostToDevice, st));
     BB_CUDA(cudaMemcpyAsync(qd, q, (size_t)n * 8, cudaMemcpyHostToDevice, st));
     FitShape s{n, n_sig, d, levels, B, layer, 0, 0, 1};
-    const HistPlan p = plan_layer(layer, s, c.sm_count, kHistSmem);
+    const HistPlan p = plan_layer<uint16_t, uint16_t>(layer, s, c.sm_count);
     const size_t hsz = (size_t)2 * p.nodes * d * B;
     unsigned long long* hist = A.alloc<unsigned long long>(hsz);
     BB_CUDA(cudaMemsetAsync(hist, 0, hsz * 8, st));
     BB_CUDA(cudaFuncSetAttribute(k_layer_hist<uint16_t, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kHistSmem));
-    const int items = (p.chunks_sig + p.chunks_bkg) * p.n_fg * p.n_ng;
-    if (items > 0)
-      k_layer_hist<uint16_t, uint16_t><<<items, 512, (size_t)p.ngs * p.fg * B * 8, st>>>(cd, n, 0, nd, qd, n, n_sig, d, B,
-                                                                                         p, hist);
+                                 227 * 1024));
+    k_layer_hist<uint16_t, uint16_t><<<hist_grid(p), kHistThreads, p.smem, st>>>(cd, 0, nd, qd, n, n_sig, d, B, p,
+                                                                                  hist);
+    BB_CUDA(cudaStreamSynchronize(st));  // host staging vector lives until here
     BB_LAUNCH_CHECK();
     BB_CUDA(cudaMemcpyAsync(out_hist, hist, hsz * 8, cudaMemcpyDeviceToHost, st));
     BB_CUDA(cudaStreamSynchronize(st));

@@ -113,6 +113,59 @@ __device__ __forceinline__ long long slot_value(const uint32_t* slot) {
 
 __device__ __forceinline__ unsigned long long as_ull(long long v) { return (unsigned long long)v; }
 
+// ------------------------------------------------------ TMA (bulk copy)
+// 1-D cp.async.bulk global->shared completing on an mbarrier (sm_90+; SASS
+// UBLKCP).  All addresses and sizes must be 16-byte multiples.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+// 2-limb slot with the limbs in separate arrays (lo[], hi[]): consecutive
+// slots fall in consecutive banks.
+__device__ __forceinline__ void slot_add2(uint32_t* lo, uint32_t* hi, int s, long long q) {
+  const uint32_t l = (uint32_t)(unsigned long long)q;
+  uint32_t h = (uint32_t)((unsigned long long)q >> 32);
+  const uint32_t old = atomicAdd(lo + s, l);
+  h += (old + l < old) ? 1u : 0u;
+  if (h) atomicAdd(hi + s, h);
+}
+
+// Rows of every per-row device array are padded to this multiple so that
+// whole tiles can be bulk-copied.
+constexpr int64_t kRowPad = 1024;
+
+// Bin codes are stored column-major inside 1024-row tiles:
+// codes[(tile * d + feature) * kTile + row % kTile].  One tile's feature group
+// is one contiguous block (a single bulk copy); one feature of a tile is a
+// contiguous 1024-code column (coalesced, vectorisable).
+constexpr int kTileLog = 10;
+constexpr int kTile = 1 << kTileLog;
+__host__ __device__ __forceinline__ int64_t code_index(int64_t row, int f, int d) {
+  return ((row >> kTileLog) * d + f) * (int64_t)kTile + (row & (kTile - 1));
+}
+
 // --------------------------------------------------------------- misc
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

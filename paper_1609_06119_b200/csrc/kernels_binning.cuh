@@ -358,12 +358,14 @@ __global__ void k_class_positions(const int8_t* __restrict__ y, int64_t n, const
 }
 
 // ---------------------------------------------------------------- 4
-// codes[f][pos[i]] = stored code.  stored = code - code_off (code_off = 1 only
-// for NaN-free data at B = 256 with u8 storage).
+// codes[code_index(pos[i], f)] = stored code; stored = code - code_off
+// (code_off = 1 only for NaN-free data at B = 256 with u8 storage).
+// tiled = 0 writes plain column-major [f][code_stride] (bb_bin parity entry).
 template <typename K, typename CodeT>
 __global__ void __launch_bounds__(256) k_codes(const K* __restrict__ keys, int64_t n, int nt,
                                                const K* __restrict__ bkeys, const int* __restrict__ pos,
-                                               CodeT* __restrict__ codes, int64_t code_stride, int code_off) {
+                                               CodeT* __restrict__ codes, int64_t code_stride, int code_off,
+                                               int d, int tiled) {
   extern __shared__ unsigned char s_raw[];
   K* sb = reinterpret_cast<K*>(s_raw);
   const int f = blockIdx.y;
@@ -371,7 +373,6 @@ __global__ void __launch_bounds__(256) k_codes(const K* __restrict__ keys, int64
   for (int t = threadIdx.x; t < nt; t += blockDim.x) sb[t] = bk[t];
   __syncthreads();
   const K* col = keys + (int64_t)f * n;
-  CodeT* out = codes + (int64_t)f * code_stride;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const K k = col[i];
     int code;
@@ -386,7 +387,8 @@ __global__ void __launch_bounds__(256) k_codes(const K* __restrict__ keys, int64
       }
       code = lo + 1;
     }
-    out[pos[i]] = (CodeT)(code - code_off);
+    const int64_t p = pos[i];
+    codes[tiled ? code_index(p, f, d) : (int64_t)f * code_stride + p] = (CodeT)(code - code_off);
   }
 }
 

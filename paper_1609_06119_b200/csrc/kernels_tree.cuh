@@ -79,70 +79,176 @@ __global__ void k_update_scores(int64_t n, double* __restrict__ F, const NodeT* 
 
 // ---------------------------------------------------------------- histogram
 // One launch per layer builds signal and background histograms for every
-// node x feature (trees.py:139-167).  CTA work item = (row chunk of one class
-// block, feature group, node group); its (node, feature, code) slots live in
-// shared memory as 2-limb int64 (slot_add), then merge into the global
-// histogram with native 64-bit global reductions.  Rows parked above the
-// layer, inactive rows (q == 0) and missing codes (slot 0 is never read by
-// the split search, trees.py:181-186) are skipped.
+// node x feature (trees.py:139-167).  Work item = (class block, feature
+// group, node group, contiguous run of row tiles).  Per tile, one thread
+// bulk-copies (TMA, cp.async.bulk) the node ids, fixed-point weights and the
+// group's code columns into a double-buffered shared-memory stage; the CTA
+// compacts the rows that contribute (in class range, at this layer, in the
+// node group, q != 0 — inactive rows carry q == 0) and every thread then
+// adds its rows' weights into (node, feature, code) slots held in shared
+// memory as 2-limb int64 (slot_add2: one returning 32-bit ATOMS per update).
+// Missing codes (bin 0) are skipped: the split search never reads slot 0
+// (trees.py:181-186).  At the end each CTA merges its slots into the global
+// histogram with native 64-bit global reductions.
 struct HistPlan {
-  int start, nodes;        // layer_start, nodes in layer
-  int fg, n_fg;            // features per group, groups
-  int ngs, n_ng;           // nodes per node group, node groups
-  int chunks_sig, chunks_bkg;
-  int64_t chunk_rows;
+  int start, nodes;          // layer_start, nodes in layer
+  int fg, n_fg;              // features per group, groups
+  int ngs, n_ng;             // nodes per node group, node groups
+  int tile;                  // rows per tile (= kTile)
+  int tiles_sig0, tiles_sig1, tiles_bkg0, tiles_bkg1;  // tile ranges per class
+  int split_sig, split_bkg;  // CTAs per group per class
+  int smem;                  // dynamic shared memory bytes
 };
 
+constexpr int kHistThreads = 512;
+
+__host__ __device__ __forceinline__ int align16(int x) { return (x + 15) & ~15; }
+
 template <typename CodeT, typename NodeT>
-__global__ void __launch_bounds__(512) k_layer_hist(const CodeT* __restrict__ codes, int64_t stride, int code_off,
-                                                    const NodeT* __restrict__ node, const long long* __restrict__ q,
-                                                    int64_t n, int64_t n_sig, int d, int B, HistPlan p,
-                                                    unsigned long long* __restrict__ hist) {
-  extern __shared__ uint32_t s_slots[];
-  int item = blockIdx.x;
-  const int fgi = item % p.n_fg;
-  item /= p.n_fg;
-  const int ngi = item % p.n_ng;
-  const int chunk = item / p.n_ng;
-  int cls;
-  int64_t lo, hi;
-  if (chunk < p.chunks_sig) {
+__host__ __device__ __forceinline__ int hist_buf_bytes(int tile, int fcount) {
+  return align16(tile * (int)sizeof(NodeT)) + tile * 8 + fcount * tile * (int)sizeof(CodeT);
+}
+
+template <typename CodeT, typename NodeT>
+__global__ void __launch_bounds__(kHistThreads, 1)
+    k_layer_hist(const CodeT* __restrict__ codes, int code_off, const NodeT* __restrict__ node,
+                 const long long* __restrict__ q, int64_t n, int64_t n_sig, int d, int B, HistPlan p,
+                 unsigned long long* __restrict__ hist) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int groups = p.n_fg * p.n_ng;
+  const int group = blockIdx.x % groups;
+  const int part = blockIdx.x / groups;
+  const int fgi = group % p.n_fg, ngi = group / p.n_fg;
+  int cls, ta, tb;
+  int64_t clo, chi;
+  if (part < p.split_sig) {
     cls = 0;
-    lo = (int64_t)chunk * p.chunk_rows;
-    hi = min(n_sig, lo + p.chunk_rows);
+    clo = 0;
+    chi = n_sig;
+    const int nt = p.tiles_sig1 - p.tiles_sig0;
+    ta = p.tiles_sig0 + (int)((int64_t)nt * part / p.split_sig);
+    tb = p.tiles_sig0 + (int)((int64_t)nt * (part + 1) / p.split_sig);
   } else {
     cls = 1;
-    lo = n_sig + (int64_t)(chunk - p.chunks_sig) * p.chunk_rows;
-    hi = min(n, lo + p.chunk_rows);
+    clo = n_sig;
+    chi = n;
+    const int k = part - p.split_sig;
+    const int nt = p.tiles_bkg1 - p.tiles_bkg0;
+    ta = p.tiles_bkg0 + (int)((int64_t)nt * k / p.split_bkg);
+    tb = p.tiles_bkg0 + (int)((int64_t)nt * (k + 1) / p.split_bkg);
   }
   const int f0 = fgi * p.fg;
   const int fcount = min(p.fg, d - f0);
   const int n0 = ngi * p.ngs;
   const int ncount = min(p.ngs, p.nodes - n0);
   const int nslots = ncount * fcount * B;
-  for (int i = threadIdx.x; i < 2 * nslots; i += blockDim.x) s_slots[i] = 0u;
-  __syncthreads();
-  const int start = p.start + n0;
-  for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
-    const int nd = (int)node[r] - start;
-    if (nd < 0 || nd >= ncount) continue;  // parked above this layer / other node group
-    const long long qq = q[r];
-    if (qq == 0) continue;                 // inactive row or zero weight
-    uint32_t* base = s_slots + 2 * (nd * fcount) * B;
-    const CodeT* cp = codes + (int64_t)f0 * stride + r;
-    for (int j = 0; j < fcount; ++j) {
-      const int c = (int)cp[(int64_t)j * stride] + code_off;
-      if (c != 0) slot_add(base + 2 * (j * B + c - 1), qq);
-    }
+  const int tile = p.tile;
+  uint32_t* lo = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* hi = lo + nslots;
+  unsigned char* stage = smem + align16(nslots * 8);
+  const int bufb = hist_buf_bytes<CodeT, NodeT>(tile, fcount);
+  uint32_t* list = reinterpret_cast<uint32_t*>(stage + 2 * bufb);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(list + tile);
+  int* counter = reinterpret_cast<int*>(bar + 2);
+
+  for (int i = threadIdx.x; i < 2 * nslots; i += kHistThreads) lo[i] = 0u;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    counter[0] = 0;
+    counter[1] = 0;
   }
   __syncthreads();
-  for (int s = threadIdx.x; s < nslots; s += blockDim.x) {
-    const long long v = slot_value(s_slots + 2 * s);
+
+  auto issue = [&](int k, int buf) {
+    unsigned char* b = stage + buf * bufb;
+    const int64_t row0 = (int64_t)k * tile;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bar[buf], (unsigned)(tile * (int)sizeof(NodeT) + tile * 8 + fcount * tile * (int)sizeof(CodeT)));
+    tma_load_1d(b, node + row0, tile * sizeof(NodeT), &bar[buf]);
+    tma_load_1d(b + align16(tile * (int)sizeof(NodeT)), q + row0, tile * 8, &bar[buf]);
+    unsigned char* cb = b + align16(tile * (int)sizeof(NodeT)) + tile * 8;
+    tma_load_1d(cb, codes + ((int64_t)k * d + f0) * kTile, fcount * kTile * sizeof(CodeT), &bar[buf]);
+  };
+
+  if (threadIdx.x == 0 && ta < tb) issue(ta, 0);
+  const int start = p.start + n0;
+  for (int k = ta; k < tb; ++k) {
+    const int it = k - ta, buf = it & 1;
+    if (threadIdx.x == 0) {
+      if (k + 1 < tb) issue(k + 1, buf ^ 1);
+      counter[(it + 1) & 1] = 0;
+    }
+    mbar_wait(&bar[buf], (it >> 1) & 1);
+    const unsigned char* b = stage + buf * bufb;
+    const NodeT* nt = reinterpret_cast<const NodeT*>(b);
+    const long long* qt = reinterpret_cast<const long long*>(b + align16(tile * (int)sizeof(NodeT)));
+    const CodeT* ct = reinterpret_cast<const CodeT*>(b + align16(tile * (int)sizeof(NodeT)) + tile * 8);
+    const int64_t row0 = (int64_t)k * tile;
+    // compaction of contributing rows (order irrelevant: integer sums)
+    for (int rl = threadIdx.x; rl < tile; rl += kHistThreads) {
+      const int64_t r = row0 + rl;
+      const int nd = (int)nt[rl] - start;
+      const bool ok = r >= clo && r < chi && nd >= 0 && nd < ncount && qt[rl] != 0;
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      int base = 0;
+      if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&counter[it & 1], __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (ok) list[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = (uint32_t)rl | ((uint32_t)nd << 16);
+    }
+    __syncthreads();
+    const int n_act = counter[it & 1];
+    // balanced work: items (row, block of 4 features), 4 independent lo-limb
+    // atomics in flight per item, carries resolved afterwards
+    const int nfb = (fcount + 3) >> 2;
+    const int items = n_act * nfb;
+    int a = 0, jb = 0;
+    if (threadIdx.x < items) {
+      jb = threadIdx.x / n_act;
+      a = threadIdx.x - jb * n_act;
+    }
+    for (int w = threadIdx.x; w < items; w += kHistThreads) {
+      const uint32_t e = list[a];
+      const int rl = (int)(e & 0xffffu);
+      const int nd = (int)(e >> 16);
+      const long long qq = qt[rl];
+      const uint32_t l = (uint32_t)(unsigned long long)qq;
+      const uint32_t h = (uint32_t)((unsigned long long)qq >> 32);
+      const int j0 = jb * 4;
+      const int sb = (nd * fcount + j0) * B - 1;
+      int sl[4];
+      uint32_t old[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + u;
+        const int c = (j < fcount) ? (int)ct[j * tile + rl] + code_off : 0;
+        sl[u] = (c != 0) ? sb + u * B + c : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) old[u] = (sl[u] >= 0) ? atomicAdd(lo + sl[u], l) : 0u;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (sl[u] >= 0) {
+          const uint32_t hh = h + ((old[u] + l < old[u]) ? 1u : 0u);
+          if (hh) atomicAdd(hi + sl[u], hh);
+        }
+      }
+      a += kHistThreads;
+      while (a >= n_act && n_act > 0) {
+        a -= n_act;
+        ++jb;
+      }
+    }
+    __syncthreads();
+  }
+  for (int s = threadIdx.x; s < nslots; s += kHistThreads) {
+    const long long v = (long long)(((unsigned long long)hi[s] << 32) | (unsigned long long)lo[s]);
     if (v != 0) {
-      const int b = s % B;
+      const int bb = s % B;
       const int j = (s / B) % fcount;
       const int nd = s / (B * fcount);
-      const int64_t g = (((int64_t)cls * p.nodes + (n0 + nd)) * d + (f0 + j)) * B + b;
+      const int64_t g = (((int64_t)cls * p.nodes + (n0 + nd)) * d + (f0 + j)) * B + bb;
       atomicAdd(&hist[g], as_ull(v));
     }
   }
@@ -299,7 +405,7 @@ __global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restric
 // the active rows' (eff, resp) fixed-point sums are accumulated per final
 // node, from which k_node_weights derives every node's sums (trees.py:231-244).
 template <typename CodeT, typename NodeT>
-__global__ void __launch_bounds__(512) k_advance(const CodeT* __restrict__ codes, int64_t stride, int code_off,
+__global__ void __launch_bounds__(512) k_advance(const CodeT* __restrict__ codes, int d, int code_off,
                                                  NodeT* __restrict__ node, int64_t n, int64_t n_sig, int start,
                                                  int tree, int n_internal, TreeArrays ta, int last_layer, int n_nodes,
                                                  const long long* __restrict__ q, const unsigned int* __restrict__ mask,
@@ -316,7 +422,7 @@ __global__ void __launch_bounds__(512) k_advance(const CodeT* __restrict__ codes
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int nd = node[i];
     if (nd >= start && vld[nd]) {
-      const int c = (int)codes[(int64_t)feat[nd] * stride + i] + code_off;
+      const int c = (int)codes[code_index(i, feat[nd], d)] + code_off;
       if (c != 0) {
         nd = 2 * nd + 1 + (c > cutp[nd] ? 1 : 0);
         node[i] = (NodeT)nd;

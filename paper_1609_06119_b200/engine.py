@@ -24,7 +24,8 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["FitConfig", "FeatureBinning", "Cut", "Tree", "Forest", "fit_forest", "predict_batch", "predict"]
+__all__ = ["FitConfig", "FeatureBinning", "Cut", "Tree", "Forest", "fit_forest", "fit_forest_device",
+           "predict_batch", "predict"]
 
 WEIGHT_EPS = 1e-12  # trees.py:39-40
 
@@ -148,7 +149,8 @@ def _as_features(X) -> tuple[np.ndarray, int]:
 
 
 def fit_forest(X, y, weights=None, config: FitConfig | None = None, *, forced_cuts=None,
-               return_leaves: bool = False, return_scores: bool = False, device: int = 0) -> Forest:
+               return_leaves: bool = False, return_scores: bool = False, profile: bool = False,
+               device: int = 0) -> Forest:
     """Fit a boosted forest on raw rows (boosting.py:117-173) on the GPU.
 
     forced_cuts: optional {(tree, heap_node): (valid, feature, cut_bin)} for
@@ -178,9 +180,29 @@ def fit_forest(X, y, weights=None, config: FitConfig | None = None, *, forced_cu
         raise ValueError("X must have at least one feature")
     y01 = np.ascontiguousarray(labels > 0, dtype=np.int8)
 
+    return _fit_native(X, xdt, False, n, d, y01, False, w, False, cfg, forced_cuts=forced_cuts,
+                       return_leaves=return_leaves, return_scores=return_scores, profile=profile, device=device)
+
+
+def fit_forest_device(x_ptr: int, x_dtype: str, n: int, d: int, y01_ptr: int, w_ptr: int | None,
+                      config: FitConfig | None = None, *, profile: bool = False, device: int = 0) -> Forest:
+    """fit_forest on inputs already resident in device memory (raw CUDA
+    pointers, e.g. torch ``data_ptr()``): X row-major float32/float64,
+    y01 int8 (>0 signal), w float64 or None.  Used by bench.py's HBM leg."""
+    cfg = config or FitConfig()
+    xdt = _lib.BB_F32 if x_dtype == "float32" else _lib.BB_F64
+    return _fit_native(C.c_void_p(x_ptr), xdt, True, n, d, C.c_void_p(y01_ptr), True,
+                       None if w_ptr is None else C.c_void_p(w_ptr), True, cfg, profile=profile, device=device)
+
+
+def _fit_native(X, xdt, x_dev, n, d, y01, y_dev, w, w_dev, cfg, *, forced_cuts=None, return_leaves=False,
+                return_scores=False, profile=False, device=0) -> Forest:
+    def p(a):
+        return a if (a is None or isinstance(a, C.c_void_p)) else _lib.ptr(a)
+
     L, D, T = cfg.binning_levels, cfg.depth, cfg.n_trees
     B, I, N = 1 << L, (1 << D) - 1, (1 << (D + 1)) - 1
-    c = _lib.FitConfigC(n_trees=T, depth=D, binning_levels=L, reserved0=0, shrinkage=cfg.shrinkage,
+    c = _lib.FitConfigC(n_trees=T, depth=D, binning_levels=L, flags=int(profile), shrinkage=cfg.shrinkage,
                         subsample=cfg.subsample, **_lib.pcg_config(cfg.seed))
     bounds = np.zeros((d, B - 1))
     feat = np.zeros((T, I), np.int32)
@@ -193,7 +215,7 @@ def fit_forest(X, y, weights=None, config: FitConfig | None = None, *, forced_cu
     f0 = np.zeros(1)
     shift = np.zeros(1, np.int32)
     n_sig = np.zeros(1, np.int64)
-    timing = np.zeros(8)
+    timing = np.zeros(16)
     leaves = np.zeros((T, n), np.uint16) if return_leaves else None
     scores = np.zeros(n) if return_scores else None
     out = _lib.FitOutC(*[_lib.ptr(a) for a in (bounds, feat, cut, valid, thr, gain, nw, pur, f0, shift, n_sig,
@@ -205,7 +227,7 @@ def fit_forest(X, y, weights=None, config: FitConfig | None = None, *, forced_cu
             *[_lib.ForcedCutC(int(t), int(nd), int(bool(v[0])), int(v[1]), int(v[2])) for (t, nd), v in items])
         n_forced = len(items)
     ctx = _lib.context(device)
-    _lib.check(_lib.lib().bb_fit(ctx, _lib.ptr(X), xdt, 0, n, d, _lib.ptr(y01), 0, _lib.ptr(w), 0, C.byref(c),
+    _lib.check(_lib.lib().bb_fit(ctx, p(X), xdt, int(x_dev), n, d, p(y01), int(y_dev), p(w), int(w_dev), C.byref(c),
                                  C.cast(forced_arr, C.c_void_p) if forced_arr is not None else None, n_forced,
                                  C.byref(out)))
     binnings = [FeatureBinning(boundaries=bounds[j].copy(), levels=L) for j in range(d)]
@@ -216,7 +238,9 @@ def fit_forest(X, y, weights=None, config: FitConfig | None = None, *, forced_cu
     ]
     info = dict(fixed_shift=int(shift[0]), n_sig=int(n_sig[0]),
                 timing_ms=dict(upload=timing[0], binning=timing[1], trees=timing[2], download=timing[3],
-                               total=timing[4]))
+                               total=timing[4], device_total=timing[5], hist_kernels=timing[6],
+                               masks_host=timing[9]),
+                hist_launches=int(timing[7]), kernel_launches=int(timing[8]))
     if return_leaves:
         info["leaves"] = leaves
     if return_scores:

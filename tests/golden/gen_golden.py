@@ -77,16 +77,21 @@ class Recorder:
             gains = bt._g_arr(ls, lb) + bt._g_arr(rs, rb) - bt._g_arr(ls + rs, lb + rb)
             scored = np.where(feas, gains, -np.inf).reshape(cs.shape[0], -1)
             start = cs.shape[0] - 1
+            # node mass scale: sum over bins of |signal| + |background| weight
+            # (per-bin masses from the cumulative histogram), max over features
+            mass = np.abs(np.diff(cs[:, :, 1:], axis=2, prepend=0.0)).sum(axis=2) + \
+                np.abs(np.diff(cb[:, :, 1:], axis=2, prepend=0.0)).sum(axis=2)
             for node in range(scored.shape[0]):
                 fin = scored[node][np.isfinite(scored[node])]
+                scale = float(np.max(mass[node])) if mass.shape[1] else 0.0
                 if fin.size == 0:
-                    rec.audit.append((rec.tree, start + node, math.inf, 0))
+                    rec.audit.append((rec.tree, start + node, math.inf, 0, math.nan, scale))
                     continue
                 best = fin.max()
                 below = fin[fin < best]
                 gap = math.inf if below.size == 0 else (best - below.max()) / max(abs(best), 1e-300)
                 pure = int(np.all(cb[node, :, B] == 0.0) and np.any(cs[node, :, B] != 0.0))
-                rec.audit.append((rec.tree, start + node, float(gap), pure))
+                rec.audit.append((rec.tree, start + node, float(gap), pure, float(best), scale))
             return cuts
 
         bb.subsample, bb.traverse_bins, bt.find_best_cuts = subsample, traverse_bins, find_best_cuts
@@ -118,7 +123,9 @@ def run_fit(X, y01, w, cfg: FitConfig, pred_rows):
     arrs = forest_arrays(forest)
     arrs["mask_hashes"] = np.array(rec.masks)
     arrs["leaf_hashes"] = np.array(rec.leaves)
-    arrs["audit"] = np.array([(a, b, c, d) for a, b, c, d in rec.audit], dtype=np.float64).reshape(-1, 4)
+    # audit rows: tree, heap node, relative gap best vs runner-up distinct gain,
+    # pure-signal flag, best gain, node absolute-mass scale
+    arrs["audit"] = np.array(rec.audit, dtype=np.float64).reshape(-1, 6)
     arrs["pred_rows"] = pred_rows
     arrs["pred"] = predict_batch(forest, np.asarray(X, np.float64)[pred_rows])
     arrs["config"] = np.array([cfg.n_trees, cfg.depth, cfg.shrinkage, cfg.subsample, cfg.binning_levels, cfg.seed])

@@ -143,6 +143,10 @@ int bb_split(bb_ctx* ctx, const int64_t* hist, int32_t d, int32_t levels, int32_
              int32_t shift, const double* boundaries, uint8_t* out_valid, int32_t* out_feature,
              int32_t* out_cut, double* out_gain, double* out_threshold);
 
+/* GPU generator (the fit's default path), same output as bb_subsample_masks. */
+int bb_subsample_masks_gpu(bb_ctx* ctx, int64_t n_sig, int64_t n_bkg, double rate, int32_t n_trees,
+                           const bb_fit_config* rng, uint32_t* out_bits);
+
 /* Host only (no GPU needed): active bits [T][ceil((n_sig+n_bkg)/32)]. */
 int bb_subsample_masks(int64_t n_sig, int64_t n_bkg, double rate, int32_t n_trees, const bb_fit_config* rng,
                        uint32_t* out_bits);

@@ -94,6 +94,8 @@ _SIGS = {
     "bb_split": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "bb_subsample_masks": (C.c_int, [C.c_int64, C.c_int64, C.c_double, C.c_int32, C.POINTER(FitConfigC), C.c_void_p]),
+    "bb_subsample_masks_gpu": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_int32,
+                                         C.POINTER(FitConfigC), C.c_void_p]),
     "bb_pairwise_sum": (C.c_double, [C.c_void_p, C.c_int64]),
 }
 

@@ -7,6 +7,7 @@
 // the tree loop.  The host only generates the next tree's subsample bits
 // (exact numpy PCG64 restatement, bb_mask.cpp) while the GPU works.
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -19,6 +20,7 @@
 #include "common.cuh"
 #include "kernels_apply.cuh"
 #include "kernels_binning.cuh"
+#include "kernels_mask.cuh"
 #include "kernels_tree.cuh"
 
 namespace bb {
@@ -216,8 +218,10 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count) {
   p.tiles_sig1 = (int)ceil_div(s.n_sig, tile);
   p.tiles_bkg0 = (int)(s.n_sig / tile);
   p.tiles_bkg1 = (int)ceil_div(s.n, tile);
+  // one CTA per SM, leaving 2 SMs to the concurrent mask-generation stream
+  // (its single-CTA parse kernel holds one SM for the whole tree)
   const int groups = p.n_fg * p.n_ng;
-  const int total = std::max(2, (int)ceil_div(sm_count, groups));
+  const int total = std::max(2, (int)((sm_count - 2) / groups));
   const int ts = p.tiles_sig1 - p.tiles_sig0, tb = p.tiles_bkg1 - p.tiles_bkg0;
   p.split_sig = std::max(1, std::min(ts, (int)std::llround((double)total * ts / (ts + tb))));
   p.split_bkg = std::max(1, std::min(tb, total - p.split_sig));
@@ -225,6 +229,122 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count) {
 }
 
 static inline int hist_grid(const HistPlan& p) { return p.n_fg * p.n_ng * (p.split_sig + p.split_bkg); }
+
+// GPU subsample-mask generator: per tree, on its own stream (kernels_mask.cuh)
+struct MaskGen {
+  PcgJump* jump = nullptr;
+  RngState* rng = nullptr;
+  unsigned int* draws = nullptr;
+  long long n_draws = 0;
+  int* J[2] = {nullptr, nullptr};
+  int *cnt = nullptr, *off = nullptr, *fill = nullptr, *bucket = nullptr, *sums = nullptr;
+  int *rec_pos = nullptr, *rec_i = nullptr, *rec_len = nullptr, *rec_count = nullptr;
+  unsigned char* rec_bits = nullptr;
+  int rec_cap = 0;
+  unsigned char* removed[2] = {nullptr, nullptr};
+  int n[2] = {0, 0}, k[2] = {0, 0};
+  int sm = 148;
+
+  void init(Arena& A, cudaStream_t st, int64_t n_sig, int64_t n_bkg, double rate, const bb_fit_config& cfg,
+            int sm_count) {
+    sm = sm_count;
+    n[0] = (int)n_sig;
+    n[1] = (int)n_bkg;
+    k[0] = (int)subsample_count(n_sig, rate);
+    k[1] = (int)subsample_count(n_bkg, rate);
+    PcgJump hj;
+    U128 a{0x4385DF649FCCF645ull, 0x2360ED051FC65DA4ull};
+    U128 c{cfg.pcg_inc_lo, cfg.pcg_inc_hi};
+    for (int j = 0; j < 64; ++j) {
+      hj.A[j] = a;
+      hj.C[j] = c;
+      c = u128_add(u128_mul(a, c), c);
+      a = u128_mul(a, a);
+    }
+    RngState hr;
+    hr.s = U128{cfg.pcg_state_lo, cfg.pcg_state_hi};
+    hr.inc = U128{cfg.pcg_inc_lo, cfg.pcg_inc_hi};
+    hr.has_uint32 = cfg.pcg_has_uint32;
+    hr.uinteger = cfg.pcg_uinteger;
+    BB_CUDA(cudaFuncSetAttribute(k_mask_parse, cudaFuncAttributeMaxDynamicSharedMemorySize, kRing * 4));
+    jump = A.alloc<PcgJump>(1);
+    rng = A.alloc<RngState>(1);
+    BB_CUDA(cudaMemcpyAsync(jump, &hj, sizeof(hj), cudaMemcpyHostToDevice, st));
+    BB_CUDA(cudaMemcpyAsync(rng, &hr, sizeof(hr), cudaMemcpyHostToDevice, st));
+    BB_CUDA(cudaStreamSynchronize(st));  // host staging structs go out of scope
+    const int64_t steps = n_sig + n_bkg;
+    n_draws = (long long)(1.5 * (double)steps) + 65536;
+    draws = A.alloc<unsigned int>((size_t)n_draws);
+    const int nmax = std::max(n[0], n[1]);
+    for (int cc = 0; cc < 2; ++cc) {
+      J[cc] = A.alloc<int>(std::max(1, n[cc]));
+      removed[cc] = A.alloc<unsigned char>(std::max(1, n[cc]));
+    }
+    cnt = A.alloc<int>(nmax + 1);
+    off = A.alloc<int>(nmax + 1);
+    fill = A.alloc<int>(nmax + 1);
+    bucket = A.alloc<int>(nmax + 1);
+    sums = A.alloc<int>(ceil_div(nmax, kScanBlock) + 1);
+    rec_cap = (int)(n_draws / 64 + 1024);
+    if (const char* e = getenv("BB_DEBUG_REC_CAP")) rec_cap = std::max(1, atoi(e));  // debug: force fallback
+    rec_pos = A.alloc<int>(rec_cap);
+    rec_i = A.alloc<int>(rec_cap);
+    rec_len = A.alloc<int>(rec_cap);
+    rec_count = A.alloc<int>(1);
+    rec_bits = A.alloc<unsigned char>((size_t)rec_cap * 32);
+  }
+
+  // active bits of the next tree into `bits` ([ceil(n/32)] words)
+  void enqueue(cudaStream_t st, unsigned int* bits, int64_t& launches) {
+    const long long n_out = (n_draws + 1) / 2;
+    k_pcg_draws<<<(unsigned)ceil_div(ceil_div(n_out, kDrawChunk), 256), 256, 0, st>>>(jump, rng, draws, n_draws);
+    BB_LAUNCH_CHECK();
+    ParseArgs pa;
+    pa.draws = draws;
+    pa.n_draws = n_draws;
+    pa.jump = jump;
+    pa.rng = rng;
+    for (int cc = 0; cc < 2; ++cc) {
+      pa.n[cc] = n[cc];
+      pa.k[cc] = k[cc];
+      pa.J[cc] = J[cc];
+    }
+    pa.rec_pos = rec_pos;
+    pa.rec_i = rec_i;
+    pa.rec_len = rec_len;
+    pa.rec_bits = rec_bits;
+    pa.rec_count = rec_count;
+    pa.rec_cap = rec_cap;
+    k_mask_parse<<<1, 32, kRing * 4, st>>>(pa);
+    BB_LAUNCH_CHECK();
+    k_expand_windows<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rec_cap, 8), 8 * sm)), 256, 0, st>>>(pa);
+    BB_LAUNCH_CHECK();
+    launches += 4;
+    for (int cc = 0; cc < 2; ++cc) {
+      const int nn = n[cc], kk = k[cc];
+      // k == 0: nothing is active (position 0 is never a step target)
+      BB_CUDA(cudaMemsetAsync(removed[cc], kk == 0 ? 1 : 0, (size_t)std::max(1, nn), st));
+      if (kk == 0 || nn <= 1 || kk >= nn) continue;
+      BB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)nn * 4, st));
+      BB_CUDA(cudaMemsetAsync(fill, 0, (size_t)nn * 4, st));
+      const int g = grid_for(nn - kk, 256, sm);
+      k_bucket_count<<<g, 256, 0, st>>>(J[cc], kk, nn, cnt);
+      const int nb = (int)ceil_div(nn, kScanBlock);
+      k_scan_block_sums<<<nb, 256, 0, st>>>(cnt, nn, sums);
+      k_scan_sums<<<1, 1024, 0, st>>>(sums, nb);
+      k_scan_apply<<<nb, 256, 0, st>>>(cnt, nn, sums, off);
+      k_bucket_fill<<<g, 256, 0, st>>>(J[cc], kk, nn, off, fill, bucket);
+      k_bucket_sort<<<grid_for(nn, 256, sm), 256, 0, st>>>(cnt, off, nn, bucket);
+      k_resolve<<<g, 256, 0, st>>>(J[cc], kk, nn, cnt, off, bucket, removed[cc]);
+      BB_LAUNCH_CHECK();
+      launches += 7;
+    }
+    const int64_t nt = (int64_t)n[0] + n[1];
+    k_mask_bits<<<grid_for(ceil_div(nt, 32), 256, sm), 256, 0, st>>>(removed[0], removed[1], n[0], nt, bits);
+    BB_LAUNCH_CHECK();
+    launches += 1;
+  }
+};
 
 template <typename CodeT, typename NodeT>
 static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, int code_off,
@@ -241,7 +361,9 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   BB_CUDA(cudaMemsetAsync(node, 0, (size_t)npad * sizeof(NodeT), st));
   BB_CUDA(cudaMemsetAsync(q, 0, (size_t)npad * 8, st));
   const int64_t words = ceil_div(n, 32);
-  unsigned int* mask = A.alloc<unsigned int>(words);
+  constexpr int kSlots = 4;
+  unsigned int* mask_slots = A.alloc<unsigned int>((size_t)words * kSlots);
+  const bool host_masks = (cfg.flags & 2) != 0;
   const int max_nodes = 1 << (s.depth - 1);
   unsigned long long* hist = A.alloc<unsigned long long>((size_t)2 * max_nodes * s.d * s.B);
   BB_CUDA(cudaMemsetAsync(hist, 0, (size_t)2 * max_nodes * s.d * s.B * 8, st));
@@ -286,18 +408,27 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   for (int l = 1; l <= s.depth; ++l) plans[l] = plan_layer<CodeT, NodeT>(l, s, c.sm_count);
   BB_CUDA(cudaFuncSetAttribute(k_layer_hist<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
 
-  // host subsample bits, double-buffered in pinned memory
+  // subsample bits: GPU generator on its own stream (default) or the host
+  // restatement (flags bit 1), into a ring of kSlots mask buffers
   Pcg64 g;
   g.state = ((unsigned __int128)cfg.pcg_state_hi << 64) | cfg.pcg_state_lo;
   g.inc = ((unsigned __int128)cfg.pcg_inc_hi << 64) | cfg.pcg_inc_lo;
   g.has_uint32 = cfg.pcg_has_uint32;
   g.uinteger = cfg.pcg_uinteger;
-  unsigned int* pinned[2];
-  BB_CUDA(cudaMallocHost(&pinned[0], (size_t)words * 4));
-  BB_CUDA(cudaMallocHost(&pinned[1], (size_t)words * 4));
-  cudaEvent_t copied[2];
-  BB_CUDA(cudaEventCreateWithFlags(&copied[0], cudaEventDisableTiming));
-  BB_CUDA(cudaEventCreateWithFlags(&copied[1], cudaEventDisableTiming));
+  MaskGen mgen;
+  cudaStream_t ms = nullptr;
+  cudaEvent_t ready[kSlots], freed[kSlots];
+  unsigned int* pinned[kSlots] = {nullptr, nullptr, nullptr, nullptr};
+  for (int k = 0; k < kSlots; ++k) {
+    BB_CUDA(cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming));
+    BB_CUDA(cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming));
+  }
+  if (host_masks) {
+    for (int k = 0; k < kSlots; ++k) BB_CUDA(cudaMallocHost(&pinned[k], (size_t)words * 4));
+  } else {
+    BB_CUDA(cudaStreamCreateWithFlags(&ms, cudaStreamNonBlocking));
+    mgen.init(A, st, s.n_sig, s.n - s.n_sig, cfg.subsample, cfg, c.sm_count);
+  }
   std::vector<uint32_t> perm;
   std::vector<NodeT> leaf_tmp;
   const bool prof = (cfg.flags & 1) != 0;
@@ -308,18 +439,46 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
     BB_CUDA(cudaEventRecord(e, st));
     hev.push_back(e);
   };
+  auto cleanup = [&]() {
+    if (ms) {
+      cudaStreamSynchronize(ms);
+      cudaStreamDestroy(ms);
+    }
+    for (int k = 0; k < kSlots; ++k) {
+      cudaEventDestroy(ready[k]);
+      cudaEventDestroy(freed[k]);
+      if (pinned[k]) cudaFreeHost(pinned[k]);
+    }
+    for (auto e : hev) cudaEventDestroy(e);
+  };
   const int gridN = grid_for(n, 256, c.sm_count);
   const int gridA = grid_for(n, 512, c.sm_count, 4);
   const auto t0 = std::chrono::steady_clock::now();
   try {
+    // the mask stream may run ahead of the fit stream by kSlots trees
+    int next_mask = 0;
+    auto produce = [&](int t) {
+      const int slot = t % kSlots;
+      unsigned int* bits = mask_slots + (size_t)slot * words;
+      if (host_masks) {
+        if (t >= kSlots) BB_CUDA(cudaEventSynchronize(freed[slot]));
+        const auto tm = std::chrono::steady_clock::now();
+        subsample_tree(g, s.n_sig, s.n - s.n_sig, cfg.subsample, pinned[slot], perm);
+        stats.mask_ms += elapsed_ms(tm);
+        if (t >= kSlots) BB_CUDA(cudaStreamWaitEvent(st, freed[slot], 0));
+        BB_CUDA(cudaMemcpyAsync(bits, pinned[slot], (size_t)words * 4, cudaMemcpyHostToDevice, st));
+        BB_CUDA(cudaEventRecord(ready[slot], st));
+      } else {
+        if (t >= kSlots) BB_CUDA(cudaStreamWaitEvent(ms, freed[slot], 0));
+        mgen.enqueue(ms, bits, stats.launches);
+        BB_CUDA(cudaEventRecord(ready[slot], ms));
+      }
+    };
     for (int t = 0; t < s.T; ++t) {
-      unsigned int* hb = pinned[t & 1];
-      if (t >= 2) BB_CUDA(cudaEventSynchronize(copied[t & 1]));
-      const auto tm = std::chrono::steady_clock::now();
-      subsample_tree(g, s.n_sig, s.n - s.n_sig, cfg.subsample, hb, perm);
-      stats.mask_ms += elapsed_ms(tm);
-      BB_CUDA(cudaMemcpyAsync(mask, hb, (size_t)words * 4, cudaMemcpyHostToDevice, st));
-      BB_CUDA(cudaEventRecord(copied[t & 1], st));
+      while (next_mask < s.T && next_mask < t + (host_masks ? 1 : kSlots)) produce(next_mask++);
+      const int slot = t % kSlots;
+      unsigned int* mask = mask_slots + (size_t)slot * words;
+      BB_CUDA(cudaStreamWaitEvent(st, ready[slot], 0));
       k_update_refresh<NodeT><<<gridN, 256, 0, st>>>(n, s.n_sig, F, node, w_cb, q, mask,
                                                       t > 0 ? ta.nw + (size_t)(t - 1) * s.n_nodes : nullptr, two_s);
       BB_LAUNCH_CHECK();
@@ -347,6 +506,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
             F, w_cb, two_s, sums);
         BB_LAUNCH_CHECK();
       }
+      BB_CUDA(cudaEventRecord(freed[slot], st));
       k_node_weights<<<1, 256, (size_t)2 * s.n_nodes * 2 * 8, st>>>(sums, s.n_nodes, s.depth, scale, cfg.shrinkage, t,
                                                                     ta);
       BB_LAUNCH_CHECK();
@@ -366,25 +526,17 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
     }
     BB_CUDA(cudaStreamSynchronize(st));
     for (size_t k = 0; k + 1 < hev.size(); k += 2) {
-      float ms = 0.f;
-      BB_CUDA(cudaEventElapsedTime(&ms, hev[k], hev[k + 1]));
-      stats.hist_ms += ms;
+      float msf = 0.f;
+      BB_CUDA(cudaEventElapsedTime(&msf, hev[k], hev[k + 1]));
+      stats.hist_ms += msf;
     }
-    for (auto e : hev) cudaEventDestroy(e);
   } catch (...) {
     cudaStreamSynchronize(st);
-    for (auto e : hev) cudaEventDestroy(e);
-    cudaFreeHost(pinned[0]);
-    cudaFreeHost(pinned[1]);
-    cudaEventDestroy(copied[0]);
-    cudaEventDestroy(copied[1]);
+    cleanup();
     throw;
   }
   *t_trees_ms = elapsed_ms(t0);
-  cudaFreeHost(pinned[0]);
-  cudaFreeHost(pinned[1]);
-  cudaEventDestroy(copied[0]);
-  cudaEventDestroy(copied[1]);
+  cleanup();
 
   // outputs
   std::vector<unsigned char> vtmp(TI);
@@ -825,6 +977,28 @@ int bb_subsample_masks(int64_t n_sig, int64_t n_bkg, double rate, int32_t n_tree
     const int64_t words = ceil_div(n_sig + n_bkg, 32);
     std::vector<uint32_t> perm;
     for (int t = 0; t < n_trees; ++t) subsample_tree(g, n_sig, n_bkg, rate, out_bits + (size_t)t * words, perm);
+  });
+}
+
+int bb_subsample_masks_gpu(bb_ctx* ctx, int64_t n_sig, int64_t n_bkg, double rate, int32_t n_trees,
+                           const bb_fit_config* rng, uint32_t* out_bits) {
+  return guarded([&] {
+    if (!ctx || !rng || !out_bits) throw InvalidArg{"null argument"};
+    if (!(rate > 0.0 && rate <= 1.0)) throw InvalidArg{"subsample rate must be in (0, 1]"};
+    if (n_sig < 0 || n_bkg < 0 || n_sig + n_bkg >= ((int64_t)1 << 31)) throw InvalidArg{"bad block sizes"};
+    std::lock_guard<std::mutex> lock(ctx->c.mu);
+    Ctx& c = ctx->c;
+    BB_CUDA(cudaSetDevice(c.device));
+    cudaStream_t st = c.stream;
+    Arena A(st);
+    MaskGen mg;
+    mg.init(A, st, n_sig, n_bkg, rate, *rng, c.sm_count);
+    const int64_t words = ceil_div(n_sig + n_bkg, 32);
+    unsigned int* bits = A.alloc<unsigned int>((size_t)std::max<int64_t>(1, words) * n_trees);
+    int64_t launches = 0;
+    for (int t = 0; t < n_trees; ++t) mg.enqueue(st, bits + (size_t)t * words, launches);
+    if (words) BB_CUDA(cudaMemcpyAsync(out_bits, bits, (size_t)words * n_trees * 4, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaStreamSynchronize(st));
   });
 }
 

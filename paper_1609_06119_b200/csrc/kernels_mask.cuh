@@ -1,0 +1,541 @@
+// Exact subsample masks on the GPU (reference sample.py:120-132 driven by
+// numpy Generator(PCG64(seed)).permutation, boosting.py:162; numpy's
+// algorithm restated in bb_mask.cpp / SURVEY.md Appendix A1).
+//
+// Per tree, for the signal block then the background block (n rows,
+// k = floor(rate*n) active): Fisher-Yates steps i = n-1 .. 1 each draw
+// j = random_interval(i) from the u32 stream (rejection on the smallest
+// all-ones mask >= i) and swap a[i], a[j].  The active set is
+// {a[0..k)} = all values minus the k..n-1 values the steps i >= k move out.
+//
+//  k_pcg_draws     the u32 draw stream (low, high halves of consecutive
+//                  PCG64 XSL-RR outputs), generated in parallel by LCG
+//                  jump-ahead.
+//  k_mask_parse    one warp assigns draws to steps: 256 draws per
+//                  iteration, each classified sure-accept (v <= i - r),
+//                  sure-reject (v > i) or ambiguous; a window with an
+//                  ambiguous draw (or a mask-band / block boundary) is
+//                  resolved serially.  Writes J[i] for steps i >= k and the
+//                  PCG64 state after the tree.
+//  k_bucket_*      counting sort of the steps by target position.
+//  k_resolve       value moved out by step i = follow the chain of later
+//                  steps that wrote its target position (see DESIGN.md
+//                  §Subsample); marks it removed.
+//  k_mask_bits     active bit = not removed, class-block bit order.
+#pragma once
+#include "common.cuh"
+
+namespace bb {
+
+struct U128 {
+  unsigned long long lo, hi;
+};
+
+__host__ __device__ __forceinline__ U128 u128_mul(U128 a, U128 b) {
+  U128 r;
+#ifdef __CUDA_ARCH__
+  r.lo = a.lo * b.lo;
+  r.hi = __umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+#else
+  const unsigned __int128 x = ((unsigned __int128)a.hi << 64 | a.lo) * ((unsigned __int128)b.hi << 64 | b.lo);
+  r.lo = (unsigned long long)x;
+  r.hi = (unsigned long long)(x >> 64);
+#endif
+  return r;
+}
+__host__ __device__ __forceinline__ U128 u128_add(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo + b.lo;
+  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1ull : 0ull);
+  return r;
+}
+__host__ __device__ __forceinline__ unsigned long long xsl_rr(U128 s) {
+  const unsigned long long x = s.hi ^ s.lo;
+  const unsigned rot = (unsigned)(s.hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+// (A_m, C_m) with s_m = A_m * s + C_m, for m = 2^j, j = 0..63
+struct PcgJump {
+  U128 A[64], C[64];
+};
+
+// device RNG state between trees (numpy bit_generator.state layout)
+struct RngState {
+  U128 s, inc;
+  int has_uint32;
+  unsigned int uinteger;
+};
+
+__host__ __device__ __forceinline__ U128 pcg_jump(const PcgJump& J, U128 s, unsigned long long m) {
+  for (int j = 0; m; ++j, m >>= 1)
+    if (m & 1ull) s = u128_add(u128_mul(J.A[j], s), J.C[j]);
+  return s;
+}
+
+// u32 draw number `idx` of the stream that starts at state `r`
+__device__ __forceinline__ unsigned int draw_at(const PcgJump& J, const RngState& r, long long idx) {
+  if (r.has_uint32) {
+    if (idx == 0) return r.uinteger;
+    idx -= 1;
+  }
+  const U128 st = pcg_jump(J, r.s, (unsigned long long)(idx >> 1) + 1ull);
+  const unsigned long long o = xsl_rr(st);
+  return (idx & 1) ? (unsigned int)(o >> 32) : (unsigned int)o;
+}
+
+constexpr int kDrawChunk = 64;  // PCG outputs per thread
+
+__global__ void k_pcg_draws(const PcgJump* __restrict__ Jp, const RngState* __restrict__ rs,
+                            unsigned int* __restrict__ draws, long long n_draws) {
+  const RngState r = *rs;
+  const long long h = r.has_uint32 ? 1 : 0;
+  const long long n_out = (n_draws - h + 1) / 2;
+  const long long q0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kDrawChunk;
+  if (q0 >= n_out) return;
+  if (q0 == 0 && h) draws[0] = r.uinteger;
+  U128 s = pcg_jump(*Jp, r.s, (unsigned long long)q0);  // state before output q0
+  const U128 a = Jp->A[0], c = Jp->C[0];
+  const long long q1 = min(n_out, q0 + kDrawChunk);
+  for (long long qq = q0; qq < q1; ++qq) {
+    s = u128_add(u128_mul(a, s), c);
+    const unsigned long long o = xsl_rr(s);
+    const long long j = h + 2 * qq;
+    if (j < n_draws) draws[j] = (unsigned int)o;
+    if (j + 1 < n_draws) draws[j + 1] = (unsigned int)(o >> 32);
+  }
+}
+
+__device__ __forceinline__ unsigned int smear(unsigned int x) {
+  x |= x >> 1;
+  x |= x >> 2;
+  x |= x >> 4;
+  x |= x >> 8;
+  x |= x >> 16;
+  return x;
+}
+
+struct ParseArgs {
+  const unsigned int* draws;
+  long long n_draws;
+  const PcgJump* jump;
+  RngState* rng;  // in: state before the tree, out: state after
+  int n[2], k[2];
+  int* J[2];      // J[c][i] for steps i >= k[c]
+  // fast-window records, expanded into J by k_expand_windows
+  int* rec_pos;            // first draw of the window
+  int* rec_i;              // step of the window's first draw, class in bit 31
+  int* rec_len;            // draws in the window (<= 256)
+  unsigned char* rec_bits; // [w][32]: lane's 8 accept bits
+  int* rec_count;          // number of records
+  int rec_cap;
+};
+
+// One warp (launch <<<1, 32>>>).  Draws stream through a shared-memory ring
+// of kRingChunks chunks filled by TMA bulk copies issued ahead of the
+// consumption point, so the sequential parse never waits on HBM latency.
+constexpr int kRingChunk = 4096;  // draws per chunk (16 KiB)
+constexpr int kRingChunks = 8;
+constexpr int kRing = kRingChunk * kRingChunks;
+
+struct Ring {
+  unsigned int* ring;
+  uint64_t* bars;
+  const unsigned int* src;
+  int n_chunks, full;
+  int issued, ready;
+};
+
+// make draws up to index `hi` (< full) readable; chunks below chunk(pos)
+// are consumed and their slots may be refilled
+__device__ __forceinline__ void ring_need(Ring& R, int pos, int hi, int lane) {
+  const int ch = hi / kRingChunk;
+  if (ch <= R.ready) return;
+  const int upto = min(R.n_chunks, pos / kRingChunk + kRingChunks);
+  if (lane == 0) {
+    for (int x = R.issued; x < upto; ++x) {
+      const int slot = x % kRingChunks;
+      mbar_expect_tx(&R.bars[slot], kRingChunk * 4);
+      tma_load_1d(R.ring + slot * kRingChunk, R.src + (size_t)x * kRingChunk, kRingChunk * 4, &R.bars[slot]);
+    }
+  }
+  R.issued = max(R.issued, upto);
+  for (int x = R.ready + 1; x <= ch; ++x) mbar_wait(&R.bars[x % kRingChunks], (unsigned)((x / kRingChunks) & 1));
+  R.ready = ch;
+}
+
+__device__ __forceinline__ unsigned int ring_get(const Ring& R, const ParseArgs& a, const RngState& r0, int idx) {
+  if (idx < R.full) return R.ring[idx & (kRing - 1)];
+  return idx < a.n_draws ? __ldg(&a.draws[idx]) : draw_at(*a.jump, r0, idx);
+}
+
+__global__ void __launch_bounds__(32) k_mask_parse(ParseArgs a) {
+  extern __shared__ __align__(16) unsigned int ring[];  // kRing draws
+  __shared__ __align__(8) uint64_t bars[kRingChunks];
+  const int lane = threadIdx.x;
+  const unsigned lt = (1u << lane) - 1u;
+  const RngState r0 = *a.rng;
+  Ring R;
+  R.ring = ring;
+  R.bars = bars;
+  R.src = a.draws;
+  R.n_chunks = (int)(a.n_draws / kRingChunk);  // full chunks; the tail is read from global
+  R.full = R.n_chunks * kRingChunk;
+  R.issued = 0;   // next chunk to issue
+  R.ready = -1;   // highest chunk known complete
+  const int full = R.full;
+  if (lane == 0) {
+    for (int c = 0; c < kRingChunks; ++c) mbar_init(&bars[c], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  int pos = 0;
+  int nrec = 0;
+  ring_need(R, 0, 0, lane);
+  for (int c = 0; c < 2; ++c) {
+    const int n = a.n[c], k = a.k[c];
+    int* J = a.J[c];
+    int i = n - 1;
+    while (i >= 1) {
+      if (pos & 3) {
+        // re-align the stream position to 4 draws (uint4 ring loads)
+        if (pos + 3 < full) ring_need(R, pos, pos + 3, lane);
+        while ((pos & 3) && i >= 1) {
+          const unsigned int v = ring_get(R, a, r0, pos) & smear((unsigned)i);
+          ++pos;
+          if ((int)v <= i) {
+            if (lane == 0 && i >= k) J[i] = (int)v;
+            --i;
+          }
+        }
+        continue;
+      }
+      const unsigned int m = smear((unsigned)i);
+      const int half = (int)(m >> 1);
+      if (i - 255 > half && pos + 256 <= full) {
+        // ---- fast loop: 256-draw windows inside one mask band
+        ring_need(R, pos, pos + 255, lane);
+        // each uint4 wraps separately (pos is 4-aligned, the ring a multiple of 4)
+        uint4 x0 = *reinterpret_cast<const uint4*>(ring + ((pos + lane * 8) & (kRing - 1)));
+        uint4 x1 = *reinterpret_cast<const uint4*>(ring + ((pos + lane * 8 + 4) & (kRing - 1)));
+        for (;;) {
+          unsigned int v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          // prefetch the next window (consumed only if this one is sure)
+          const bool more = (i - 511 > half) && (pos + 512 <= full);
+          if (more) {
+            ring_need(R, pos, pos + 511, lane);
+            x0 = *reinterpret_cast<const uint4*>(ring + ((pos + 256 + lane * 8) & (kRing - 1)));
+            x1 = *reinterpret_cast<const uint4*>(ring + ((pos + 260 + lane * 8) & (kRing - 1)));
+          }
+          unsigned accb = 0, ambb = 0;
+          const int i0 = i - lane * 8;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            v[u] &= m;
+            const bool acc = (int)v[u] <= i0 - u;
+            accb |= (acc ? 1u : 0u) << u;
+            ambb |= ((!acc && (int)v[u] <= i) ? 1u : 0u) << u;
+          }
+          int len = 256;
+          if (__any_sync(0xffffffffu, ambb != 0)) {
+            // first ambiguous draw: draws before it are decided
+            len = __reduce_min_sync(0xffffffffu, ambb ? lane * 8 + (__ffs(ambb) - 1) : 256);
+            const int keep = len - lane * 8;
+            accb &= keep >= 8 ? 0xffu : (keep <= 0 ? 0u : ((1u << keep) - 1u));
+          }
+          const int total = __reduce_add_sync(0xffffffffu, __popc(accb));
+          if (i >= k && total > 0) {  // steps i .. i-total+1 may need J values
+            if (nrec < a.rec_cap) {
+              const int w = nrec++;
+              a.rec_bits[(size_t)w * 32 + lane] = (unsigned char)accb;
+              if (lane == 0) {
+                a.rec_pos[w] = pos;
+                a.rec_i[w] = i | (c << 31);
+                a.rec_len[w] = len;
+              }
+            } else {  // record buffer full: write this window's J values directly
+              const int cnt = __popc(accb);
+              int incl = cnt;
+              for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+              }
+              int sd = i - (incl - cnt);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                if ((accb >> u) & 1u) {
+                  if (sd >= k) J[sd] = (int)v[u];
+                  --sd;
+                }
+              }
+            }
+          }
+          i -= total;
+          if (len < 256) {
+            // the ambiguous draw: its step is now exact
+            const unsigned int va = ring[(pos + len) & (kRing - 1)] & m;
+            if ((int)va <= i) {
+              if (lane == 0 && i >= k) J[i] = (int)va;
+              --i;
+            }
+            pos += len + 1;
+            break;
+          }
+          pos += 256;
+          if (!more || i - 255 <= half) break;
+        }
+        continue;
+      }
+      if (i - 31 > half && pos + 32 <= full) {
+        // 32-draw window, one draw per lane, same exact-prefix rule
+        ring_need(R, pos, pos + 31, lane);
+        const unsigned int v = ring[(pos + lane) & (kRing - 1)] & m;
+        const bool acc = (int)v <= i - lane;
+        const bool amb = !acc && (int)v <= i;
+        const unsigned ambm = __ballot_sync(0xffffffffu, amb);
+        const int ra = ambm ? __ffs(ambm) - 1 : 32;
+        const unsigned ab = __ballot_sync(0xffffffffu, acc) & (ra >= 32 ? 0xffffffffu : ((1u << ra) - 1u));
+        const int before = __popc(ab & lt);
+        if (lane < ra && acc && i - before >= k) J[i - before] = (int)v;
+        i -= __popc(ab);
+        if (ra < 32) {
+          const unsigned int va = __shfl_sync(0xffffffffu, v, ra);
+          if ((int)va <= i) {
+            if (lane == 0 && i >= k) J[i] = (int)va;
+            --i;
+          }
+          pos += ra + 1;
+        } else {
+          pos += 32;
+        }
+        continue;
+      }
+      // serial: up to 32 draws, then re-align pos to 4; all lanes in lockstep
+      if (pos + 35 < full) ring_need(R, pos, pos + 35, lane);
+      for (int it = 0; (it < 32 || (pos & 3)) && i >= 1; ++it) {
+        const unsigned int v = ring_get(R, a, r0, pos) & smear((unsigned)i);
+        ++pos;
+        if ((int)v <= i) {
+          if (lane == 0 && i >= k) J[i] = (int)v;
+          --i;
+        }
+      }
+    }
+  }
+  // drain outstanding bulk copies before the CTA exits
+  for (int x = R.ready + 1; x < R.issued; ++x) mbar_wait(&bars[x % kRingChunks], (unsigned)((x / kRingChunks) & 1));
+  // state after consuming `pos` draws
+  if (lane == 0) {
+    *a.rec_count = nrec;
+    RngState r = r0;
+    long long d = pos;
+    if (r.has_uint32 && d > 0) {
+      r.has_uint32 = 0;
+      d -= 1;
+    }
+    if (d > 0) {
+      const unsigned long long outs = (unsigned long long)((d + 1) / 2);
+      const U128 st = pcg_jump(*a.jump, r0.s, outs);
+      r.s = st;
+      if (d & 1) {
+        r.has_uint32 = 1;
+        r.uinteger = (unsigned int)(xsl_rr(st) >> 32);
+      } else {
+        r.has_uint32 = 0;
+        r.uinteger = 0;
+      }
+    }
+    *a.rng = r;
+  }
+}
+
+// J values of the fast windows: one warp per record; draw r of the window is
+// accepted iff its bit is set, its step is i - (accepted draws before r).
+__global__ void k_expand_windows(ParseArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int nrec = min(*a.rec_count, a.rec_cap);
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrec; w += (gridDim.x * blockDim.x) >> 5) {
+    const int pos = a.rec_pos[w], len = a.rec_len[w];
+    const int ic = a.rec_i[w];
+    const int c = (ic >> 31) & 1, i = ic & 0x7fffffff;
+    const unsigned int m = smear((unsigned)i);
+    const unsigned accb = a.rec_bits[(size_t)w * 32 + lane];
+    const int cnt = __popc(accb);
+    int incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int s = i - (incl - cnt);
+    const int k = a.k[c];
+    int* J = a.J[c];
+    for (int u = 0; u < 8; ++u) {
+      const int r = lane * 8 + u;
+      if (r < len && ((accb >> u) & 1u)) {
+        if (s >= k) J[s] = (int)(a.draws[pos + r] & m);
+        --s;
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------- resolution
+__global__ void k_bucket_count(const int* __restrict__ J, int k, int n, int* __restrict__ cnt) {
+  for (int t = k + blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+    atomicAdd(&cnt[J[t]], 1);
+}
+
+__global__ void k_bucket_fill(const int* __restrict__ J, int k, int n, const int* __restrict__ off,
+                              int* __restrict__ fill, int* __restrict__ bucket) {
+  for (int t = k + blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int p = J[t];
+    const int slot = atomicAdd(&fill[p], 1);
+    bucket[off[p] + slot] = t;
+  }
+}
+
+// steps targeting one position, ascending (buckets are tiny)
+__global__ void k_bucket_sort(const int* __restrict__ cnt, const int* __restrict__ off, int n, int* __restrict__ bucket) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    const int c = cnt[p];
+    if (c < 2) continue;
+    int* b = bucket + off[p];
+    for (int x = 1; x < c; ++x) {
+      const int v = b[x];
+      int y = x - 1;
+      while (y >= 0 && b[y] > v) {
+        b[y + 1] = b[y];
+        --y;
+      }
+      b[y + 1] = v;
+    }
+  }
+}
+
+// value removed by step i: V(J[i], i), following the chain of later steps
+// (V(p, t) = p if no step t' > t targets p, else V(t*, t*) with
+// t* = min{t' > t : J[t'] = p})
+__global__ void k_resolve(const int* __restrict__ J, int k, int n, const int* __restrict__ cnt,
+                          const int* __restrict__ off, const int* __restrict__ bucket,
+                          unsigned char* __restrict__ removed) {
+  for (int i = k + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int p = J[i], t = i;
+    for (;;) {
+      const int c = cnt[p];
+      const int* b = bucket + off[p];
+      int nxt = -1;
+      for (int x = 0; x < c; ++x) {
+        const int v = b[x];
+        if (v > t) {
+          nxt = v;
+          break;
+        }
+      }
+      if (nxt < 0) break;
+      p = nxt;
+      t = nxt;
+    }
+    removed[p] = 1;
+  }
+}
+
+// active bits, class-block order: bit g < n_sig -> signal value g, else
+// background value g - n_sig
+__global__ void k_mask_bits(const unsigned char* __restrict__ rem_sig, const unsigned char* __restrict__ rem_bkg,
+                            long long n_sig, long long n, unsigned int* __restrict__ bits) {
+  const long long words = (n + 31) / 32;
+  for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+       w += (long long)gridDim.x * blockDim.x) {
+    unsigned int v = 0;
+    for (int b = 0; b < 32; ++b) {
+      const long long g = w * 32 + b;
+      if (g >= n) break;
+      const bool act = g < n_sig ? !rem_sig[g] : !rem_bkg[g - n_sig];
+      v |= (act ? 1u : 0u) << b;
+    }
+    bits[w] = v;
+  }
+}
+
+// --------------------------------------------------------------- scan
+// exclusive scan of n ints: per-block sums, single-CTA scan of the sums,
+// per-block exclusive scan with the carried offset
+constexpr int kScanBlock = 1024;  // elements per block (256 threads x 4)
+
+__global__ void k_scan_block_sums(const int* __restrict__ in, int n, int* __restrict__ sums) {
+  __shared__ int s[8];
+  const int base = blockIdx.x * kScanBlock;
+  int v = 0;
+  for (int j = threadIdx.x; j < kScanBlock; j += blockDim.x)
+    if (base + j < n) v += in[base + j];
+  v = __reduce_add_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    sums[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_scan_sums(int* __restrict__ sums, int nb) {
+  // single CTA, sequential chunks of blockDim
+  __shared__ int carry;
+  __shared__ int ws[32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int v = i < nb ? sums[i] : 0;
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((threadIdx.x & 31) >= o) incl += y;
+    }
+    if ((threadIdx.x & 31) == 31) ws[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int w = threadIdx.x < (int)(blockDim.x >> 5) ? ws[threadIdx.x] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (threadIdx.x >= o) w += y;
+      }
+      ws[threadIdx.x] = w;
+    }
+    __syncthreads();
+    const int excl = carry + ((threadIdx.x >= 32) ? ws[(threadIdx.x >> 5) - 1] : 0) + incl - v;
+    __syncthreads();
+    if (i < nb) sums[i] = excl;
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+}
+
+__global__ void k_scan_apply(const int* __restrict__ in, int n, const int* __restrict__ sums, int* __restrict__ out) {
+  __shared__ int ws[8];
+  const int base = blockIdx.x * kScanBlock;
+  const int t = threadIdx.x;  // 256 threads, 4 consecutive elements each
+  int v[4], loc = 0;
+  for (int j = 0; j < 4; ++j) {
+    const int i = base + t * 4 + j;
+    v[j] = i < n ? in[i] : 0;
+    loc += v[j];
+  }
+  int incl = loc;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((t & 31) >= o) incl += y;
+  }
+  if ((t & 31) == 31) ws[t >> 5] = incl;
+  __syncthreads();
+  int woff = 0;
+  for (int w = 0; w < (t >> 5); ++w) woff += ws[w];
+  int run = sums[blockIdx.x] + woff + incl - loc;
+  for (int j = 0; j < 4; ++j) {
+    const int i = base + t * 4 + j;
+    if (i < n) out[i] = run;
+    run += v[j];
+  }
+}
+
+}  // namespace bb

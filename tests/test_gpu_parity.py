@@ -75,6 +75,35 @@ def test_binning_configs_vs_oracle(name, n):
             np.testing.assert_array_equal(c[j], oracle.bin_codes(ref_b, X[:, j]))
 
 
+# ------------------------------------------------------------------ subsample masks
+def _np_masks(seed, a, b, rate, T):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    out = []
+    for _ in range(T):
+        ms = []
+        for nn in (a, b):
+            m = np.zeros(nn, bool)
+            m[rng.permutation(nn)[:math.floor(rate * nn)]] = True
+            ms.append(m)
+        out.append(np.concatenate(ms))
+    return out
+
+
+@pytest.mark.parametrize("seed,a,b,rate,T", [(0, 50_000, 50_000, 0.5, 3), (7, 1, 2, 0.5, 3), (3, 1000, 17, 0.3, 4),
+                                             (9, 65_537, 131_071, 0.77, 2), (2**40 + 5, 2, 5, 1.0, 2),
+                                             (42, 5, 100_000, 0.01, 2), (123, 300_000, 700_000, 0.5, 2),
+                                             (5, 0, 9, 0.5, 2), (8, 2_000_003, 1_048_577, 0.5, 1)])
+def test_gpu_subsample_masks_match_numpy(seed, a, b, rate, T):
+    cfg = _lib.FitConfigC(**_lib.pcg_config(seed))
+    words = (a + b + 31) // 32
+    bits = np.zeros(max(1, words) * T, np.uint32)
+    _lib.check(_lib.lib().bb_subsample_masks_gpu(_lib.context(), a, b, rate, T, C.byref(cfg), _lib.ptr(bits)))
+    ref = _np_masks(seed, a, b, rate, T)
+    for t in range(T):
+        m = np.unpackbits(bits[t * words:(t + 1) * words].view(np.uint8), bitorder="little")[:a + b].astype(bool)
+        np.testing.assert_array_equal(m, ref[t], err_msg=f"tree {t}")
+
+
 # ------------------------------------------------------------------ histogram
 def _random_layer(rng, n, n_sig, d, levels, layer, nan_rate=0.05, neg=True):
     B = 1 << levels

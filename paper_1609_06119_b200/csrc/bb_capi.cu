@@ -241,6 +241,7 @@ struct MaskGen {
   int *rec_pos = nullptr, *rec_i = nullptr, *rec_len = nullptr, *rec_count = nullptr;
   unsigned char* rec_bits = nullptr;
   int rec_cap = 0;
+  long long* prof = nullptr;  // BB_PARSE_PROFILE: phase cycles, printed at destruction
   unsigned char* removed[2] = {nullptr, nullptr};
   int n[2] = {0, 0}, k[2] = {0, 0};
   int sm = 148;
@@ -267,6 +268,7 @@ struct MaskGen {
     hr.has_uint32 = cfg.pcg_has_uint32;
     hr.uinteger = cfg.pcg_uinteger;
     BB_CUDA(cudaFuncSetAttribute(k_mask_parse, cudaFuncAttributeMaxDynamicSharedMemorySize, kRing * 4));
+    BB_CUDA(cudaFuncSetAttribute(k_mask_parse_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, kParseSmem));
     jump = A.alloc<PcgJump>(1);
     rng = A.alloc<RngState>(1);
     BB_CUDA(cudaMemcpyAsync(jump, &hj, sizeof(hj), cudaMemcpyHostToDevice, st));
@@ -292,6 +294,18 @@ struct MaskGen {
     rec_len = A.alloc<int>(rec_cap);
     rec_count = A.alloc<int>(1);
     rec_bits = A.alloc<unsigned char>((size_t)rec_cap * 32);
+    if (getenv("BB_PARSE_PROFILE")) {
+      prof = A.alloc<long long>(8);
+      BB_CUDA(cudaMemsetAsync(prof, 0, 64, st));
+    }
+  }
+  void report(cudaStream_t st) {
+    if (!prof) return;
+    long long h[8];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, prof, 64, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "parse phases (cycles): need=%lld classify=%lld scan=%lld list=%lld resolve=%lld jwrite=%lld windows=%lld small=%lld\n",
+            h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
   }
 
   // active bits of the next tree into `bits` ([ceil(n/32)] words)
@@ -315,7 +329,12 @@ struct MaskGen {
     pa.rec_bits = rec_bits;
     pa.rec_count = rec_count;
     pa.rec_cap = rec_cap;
-    k_mask_parse<<<1, 32, kRing * 4, st>>>(pa);
+    pa.prof = prof;
+    if (getenv("BB_WARP_PARSE")) {
+      k_mask_parse<<<1, 32, kRing * 4, st>>>(pa);
+    } else {
+      k_mask_parse_cta<<<1, kPT, kParseSmem, st>>>(pa);
+    }
     BB_LAUNCH_CHECK();
     k_expand_windows<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rec_cap, 8), 8 * sm)), 256, 0, st>>>(pa);
     BB_LAUNCH_CHECK();
@@ -440,6 +459,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
     hev.push_back(e);
   };
   auto cleanup = [&]() {
+    if (ms) mgen.report(ms);
     if (ms) {
       cudaStreamSynchronize(ms);
       cudaStreamDestroy(ms);

@@ -129,6 +129,7 @@ struct ParseArgs {
   unsigned char* rec_bits; // [w][32]: lane's 8 accept bits
   int* rec_count;          // number of records
   int rec_cap;
+  long long* prof;         // optional [8] phase cycle counters (debug)
 };
 
 // One warp (launch <<<1, 32>>>).  Draws stream through a shared-memory ring
@@ -327,6 +328,281 @@ __global__ void __launch_bounds__(32) k_mask_parse(ParseArgs a) {
   // state after consuming `pos` draws
   if (lane == 0) {
     *a.rec_count = nrec;
+    RngState r = r0;
+    long long d = pos;
+    if (r.has_uint32 && d > 0) {
+      r.has_uint32 = 0;
+      d -= 1;
+    }
+    if (d > 0) {
+      const unsigned long long outs = (unsigned long long)((d + 1) / 2);
+      const U128 st = pcg_jump(*a.jump, r0.s, outs);
+      r.s = st;
+      if (d & 1) {
+        r.has_uint32 = 1;
+        r.uinteger = (unsigned int)(xsl_rr(st) >> 32);
+      } else {
+        r.has_uint32 = 0;
+        r.uinteger = 0;
+      }
+    }
+    *a.rng = r;
+  }
+}
+
+// ----------------------------------------------------------- CTA parse
+// Same contract as k_mask_parse, one CTA of kPT threads (launch <<<1, kPT>>>).
+// A window of W <= kPW draws inside one mask band is classified in
+// parallel: sure-accept (v <= i - r), sure-reject (v > i) or ambiguous.  A
+// block scan gives every draw its number of sure accepts before it; the
+// ambiguous draws form a short ordered list whose acceptance
+// (A_before <= key, key = i - S_before(r) - v) warp 0 resolves with the same
+// sure/unsure speculation one level down; then every accepted draw's step
+// s = i - S_before(r) - A_before(r) is known and J[s] is written in parallel.
+// W is capped near 8*sqrt(m) so the ambiguous list stays ~32 long.
+constexpr int kPT = 512;
+constexpr int kPD = 16;
+constexpr int kPW = kPT * kPD;        // 8192
+constexpr int kPChunk = 8192;          // draws per ring chunk (32 KiB)
+constexpr int kPChunks = 4;
+constexpr int kPRing = kPChunk * kPChunks;
+constexpr int kParseSmem = kPRing * 4 + kPW * 4 + (kPW + 1) * 4 + 64;
+
+__device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int* s_total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < (kPT / 32) ? s_warp[lane] : 0;
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < (kPT / 32)) s_warp[lane] = wi - w;
+    if (lane == 31) *s_total = wi;
+  }
+  __syncthreads();
+  return s_warp[warp] + incl - v;
+}
+
+__global__ void __launch_bounds__(kPT, 1) k_mask_parse_cta(ParseArgs a) {
+  extern __shared__ __align__(16) unsigned char psm[];
+  unsigned int* ring = reinterpret_cast<unsigned int*>(psm);
+  int* akey = reinterpret_cast<int*>(ring + kPRing);
+  int* apref = akey + kPW;
+  __shared__ __align__(8) uint64_t bars[kPChunks];
+  __shared__ int s_warp[32];
+  __shared__ int s_tot, s_i, s_pos, s_acc;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const RngState r0 = *a.rng;
+  const int n_chunks = (int)(a.n_draws / kPChunk);
+  const int full = n_chunks * kPChunk;
+  int issued = 0, ready = -1;
+  if (tid == 0) {
+    for (int c = 0; c < kPChunks; ++c) mbar_init(&bars[c], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // all threads: make draws [.., hi] (< full) readable; chunks below chunk(pos) are consumed
+  auto need = [&](int pos, int hi) {
+    const int ch = hi / kPChunk;
+    if (ch <= ready) return;
+    const int upto = min(n_chunks, pos / kPChunk + kPChunks);
+    if (tid == 0) {
+      for (int x = issued; x < upto; ++x) {
+        const int slot = x % kPChunks;
+        mbar_expect_tx(&bars[slot], kPChunk * 4);
+        tma_load_1d(ring + slot * kPChunk, a.draws + (size_t)x * kPChunk, kPChunk * 4, &bars[slot]);
+      }
+    }
+    issued = max(issued, upto);
+    for (int x = ready + 1; x <= ch; ++x) mbar_wait(&bars[x % kPChunks], (unsigned)((x / kPChunks) & 1));
+    ready = ch;
+  };
+  auto get = [&](int idx) -> unsigned int {
+    if (idx < full) return ring[idx % kPRing];
+    return idx < a.n_draws ? __ldg(&a.draws[idx]) : draw_at(*a.jump, r0, idx);
+  };
+  int pos = 0;
+  need(0, 0);
+  for (int c = 0; c < 2; ++c) {
+    const int n = a.n[c], k = a.k[c];
+    int* J = a.J[c];
+    int i = n - 1;
+    while (i >= 1) {
+      const unsigned int m = smear((unsigned)i);
+      const int half = (int)(m >> 1);
+      int W = min(kPW, i - half);
+      W = min(W, max(1024, (int)(8.0f * sqrtf((float)m))));
+      W = min(W, full - pos);
+      long long tq0 = clock64();
+      if (W >= 1024) {
+        need(pos, pos + W - 1);
+        long long tq1 = clock64();
+        // warp w owns draws [512w, 512w+512): row u, lane l -> r = 512w + 32u + l
+        const int rw = warp * 512;
+        unsigned sab[16], amb[16], v[16];
+        int ws = 0, wq = 0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int r = rw + u * 32 + lane;
+          const bool in = r < W;
+          v[u] = in ? (ring[(pos + r) & (kPRing - 1)] & m) : 0u;
+          const bool acc = in && (int)v[u] <= i - r;
+          const bool amg = in && !acc && (int)v[u] <= i;
+          sab[u] = __ballot_sync(0xffffffffu, acc);
+          amb[u] = __ballot_sync(0xffffffffu, amg);
+          ws += __popc(sab[u]);
+          wq += __popc(amb[u]);
+        }
+        long long tq2 = clock64();
+        if (lane == 0) {
+          s_warp[warp] = ws;
+          s_warp[16 + warp] = wq;
+        }
+        __syncthreads();
+        int S_w = 0, Q_w = 0, S_tot = 0, Q_tot = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < 16; ++w2) {
+          const int a1 = s_warp[w2], a2 = s_warp[16 + w2];
+          if (w2 < warp) {
+            S_w += a1;
+            Q_w += a2;
+          }
+          S_tot += a1;
+          Q_tot += a2;
+        }
+        long long tq3 = clock64();
+        // ambiguous draws in order: key = i - S_before(r) - v
+        {
+          int sr = S_w, qr = Q_w;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            if ((amb[u] >> lane) & 1u) akey[qr + __popc(amb[u] & lt)] = i - (sr + __popc(sab[u] & lt)) - (int)v[u];
+            sr += __popc(sab[u]);
+            qr += __popc(amb[u]);
+          }
+        }
+        __syncthreads();
+        long long tq4 = clock64();
+        if (warp == 0) {
+          int A = 0;
+          for (int base = 0; base < Q_tot; base += 32) {
+            const int j = base + lane;
+            const bool valid = j < Q_tot;
+            const int key = valid ? akey[j] : 0;
+            const bool sacc = valid && key >= A + lane;
+            const bool srej = !valid || key < A;
+            if (!__any_sync(0xffffffffu, !sacc && !srej)) {
+              const unsigned bal = __ballot_sync(0xffffffffu, sacc);
+              if (valid) apref[j] = A + __popc(bal & lt);
+              A += __popc(bal);
+            } else {
+              for (int l = 0; l < 32 && base + l < Q_tot; ++l) {
+                const int kl = __shfl_sync(0xffffffffu, key, l);
+                if (lane == l) apref[base + l] = A;
+                A += (kl >= A) ? 1 : 0;
+              }
+            }
+          }
+          if (lane == 0) {
+            apref[Q_tot] = A;
+            s_acc = A;
+          }
+        }
+        __syncthreads();
+        long long tq5 = clock64();
+        // J of every accepted draw (consecutive lanes -> consecutive steps);
+        // windows entirely below k only need their accept count
+        if (i >= k) {
+          int sr = S_w, qr = Q_w;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const bool sacc = (sab[u] >> lane) & 1u;
+            const bool isamb = (amb[u] >> lane) & 1u;
+            if (sacc || isamb) {
+              const int q = qr + __popc(amb[u] & lt);
+              const int ab = apref[q];
+              if (sacc || apref[q + 1] - ab == 1) {
+                const int st = i - (sr + __popc(sab[u] & lt)) - ab;
+                if (st >= k) J[st] = (int)v[u];
+              }
+            }
+            sr += __popc(sab[u]);
+            qr += __popc(amb[u]);
+          }
+        }
+        i -= S_tot + s_acc;
+        pos += W;
+        __syncthreads();
+        if (a.prof && tid == 0) {
+          long long tq6 = clock64();
+          a.prof[0] += tq1 - tq0; a.prof[1] += tq2 - tq1; a.prof[2] += tq3 - tq2; a.prof[3] += tq4 - tq3;
+          a.prof[4] += tq5 - tq4; a.prof[5] += tq6 - tq5; a.prof[6] += 1;
+        }
+      } else {
+        // short stretch (band bottom, small i, buffer tail): warp 0 walks up
+        // to 512 draws with 32-draw windows / serially, then broadcasts
+        if (pos < full) need(pos, min(full - 1, pos + 512 + 31));
+        if (warp == 0) {
+          const int stop = pos + 512;
+          while (i >= 1 && pos < stop) {
+            const unsigned int mm = smear((unsigned)i);
+            const int hf = (int)(mm >> 1);
+            if (i - 31 > hf) {
+              const unsigned int vv = get(pos + lane) & mm;
+              const bool acc = (int)vv <= i - lane;
+              const bool amb = !acc && (int)vv <= i;
+              const unsigned ambm = __ballot_sync(0xffffffffu, amb);
+              const int ra = ambm ? __ffs(ambm) - 1 : 32;
+              const unsigned ab = __ballot_sync(0xffffffffu, acc) & (ra >= 32 ? 0xffffffffu : ((1u << ra) - 1u));
+              const int before = __popc(ab & lt);
+              if (lane < ra && acc && i - before >= k) J[i - before] = (int)vv;
+              i -= __popc(ab);
+              if (ra < 32) {
+                const unsigned int va = __shfl_sync(0xffffffffu, vv, ra);
+                if ((int)va <= i) {
+                  if (lane == 0 && i >= k) J[i] = (int)va;
+                  --i;
+                }
+                pos += ra + 1;
+              } else {
+                pos += 32;
+              }
+            } else {
+              const unsigned int vv = get(pos) & mm;
+              ++pos;
+              if ((int)vv <= i) {
+                if (lane == 0 && i >= k) J[i] = (int)vv;
+                --i;
+              }
+            }
+          }
+          if (lane == 0) {
+            s_i = i;
+            s_pos = pos;
+          }
+        }
+        __syncthreads();
+        i = s_i;
+        pos = s_pos;
+        __syncthreads();
+        if (a.prof && tid == 0) a.prof[7] += clock64() - tq0;
+      }
+    }
+  }
+  for (int x = ready + 1; x < issued; ++x) mbar_wait(&bars[x % kPChunks], (unsigned)((x / kPChunks) & 1));
+  if (tid == 0) {
+    *a.rec_count = 0;
     RngState r = r0;
     long long d = pos;
     if (r.has_uint32 && d > 0) {

@@ -255,6 +255,22 @@ def gen_masks(out):
     np.savez_compressed(out.replace(".json", "_first.npz"), **first_masks)
 
 
+def gen_model_doc():
+    """A reference-written JSON model (model_io.py format v1) plus inputs and
+    its predictions, for the format-interop tests."""
+    from binboost.model_io import serialize_forest
+
+    rng = np.random.default_rng(3)
+    X = rng.normal(size=(2000, 4))
+    X[rng.random(X.shape) < 0.05] = np.nan
+    y = np.where(rng.random(2000) < 0.4, 1, -1)
+    f = bb.fit_forest(X, y, None, FitConfig(n_trees=5, depth=3, binning_levels=4, seed=1))
+    with open(os.path.join(HERE, "ref_model.json"), "w") as fh:
+        fh.write(serialize_forest(f))
+    np.savez_compressed(os.path.join(HERE, "ref_model_inputs.npz"), X=X[:300])
+    np.save(os.path.join(HERE, "ref_model_pred.npy"), predict_batch(f, X[:300]))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the cfg2 slice and cfg3 proxy (minutes)")
@@ -263,6 +279,7 @@ def main():
     gen_kats(os.path.join(HERE, "kats.json"))
     gen_binning(os.path.join(HERE, "binning_random.npz"))
     gen_masks(os.path.join(HERE, "masks.json"))
+    gen_model_doc()
 
     rng = np.random.default_rng(2024)
     cases = {}

@@ -1,0 +1,81 @@
+"""World-size-2 gloo test of the row-sharded fit's host logic (CPU).
+
+Each rank takes its class-block shard (sharding.py), builds integer
+fixed-point partial layer histograms over its rows with the oracle's exact
+integer sums, and all-reduces them (int64 SUM); the result must equal the
+single-process histogram bit-for-bit, so every rank takes the same cut —
+the property the per-layer NCCL all-reduce relies on."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from oracle.binboost_np import _exact_int_bincount
+from paper_1609_06119_b200.sharding import slice_mask
+
+N_SIG, N_BKG, D, L = 3001, 4999, 5, 4
+
+
+def _data():
+    rng = np.random.default_rng(17)
+    codes_s = rng.integers(0, (1 << L) + 1, (N_SIG, D))
+    codes_b = rng.integers(0, (1 << L) + 1, (N_BKG, D))
+    q_s = rng.integers(0, 1 << 32, N_SIG)
+    q_b = rng.integers(0, 1 << 32, N_BKG)
+    node_s = rng.integers(3, 7, N_SIG)
+    node_b = rng.integers(3, 7, N_BKG)
+    rng2 = np.random.Generator(np.random.PCG64(5))
+    ms, mb = oracle.subsample_masks(rng2, N_SIG, N_BKG, 0.5)
+    return codes_s, codes_b, q_s, q_b, node_s, node_b, ms, mb
+
+
+def _hist(codes, q, node, active, start=3, count=4):
+    B1 = (1 << L) + 1
+    out = np.zeros((count, D, B1), np.int64)
+    sel = active & (node >= start)
+    loc = node[sel] - start
+    for j in range(D):
+        out[:, j, :] = _exact_int_bincount(loc * B1 + codes[sel, j], q[sel], count * B1).reshape(count, B1)
+    return out
+
+
+def _worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    codes_s, codes_b, q_s, q_b, node_s, node_b, ms, mb = _data()
+    s0, s1 = N_SIG * rank // world, N_SIG * (rank + 1) // world
+    b0, b1 = N_BKG * rank // world, N_BKG * (rank + 1) // world
+    act = slice_mask(ms, mb, rank, world)
+    n_s = s1 - s0
+    hs = _hist(codes_s[s0:s1], q_s[s0:s1], node_s[s0:s1], act[:n_s])
+    hb = _hist(codes_b[b0:b1], q_b[b0:b1], node_b[b0:b1], act[n_s:])
+    t = torch.from_numpy(np.stack([hs, hb]))
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    out_q.put((rank, t.numpy()))
+    dist.destroy_process_group()
+
+
+def test_sharded_histograms_allreduce_exact():
+    codes_s, codes_b, q_s, q_b, node_s, node_b, ms, mb = _data()
+    full = np.stack([_hist(codes_s, q_s, node_s, ms), _hist(codes_b, q_b, node_b, mb)])
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(2):
+        np.testing.assert_array_equal(got[r], full)

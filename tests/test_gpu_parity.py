@@ -317,3 +317,22 @@ def test_bridge_fit_predict_and_concurrency():
     m.close()
     with pytest.raises(RuntimeError, match="model handle is closed"):
         m.predict(X[:3])
+
+
+# ------------------------------------------------------------------ model files
+def test_model_file_interop(golden_dir, tmp_path):
+    from paper_1609_06119_b200.model_format import load_forest, parse_forest, save_forest, serialize_forest
+
+    # reference-written model -> GPU apply
+    f = load_forest(f"{golden_dir}/ref_model.json")
+    X = np.load(f"{golden_dir}/ref_model_inputs.npz")["X"]
+    np.testing.assert_allclose(predict_batch(f, X), np.load(f"{golden_dir}/ref_model_pred.npy"), rtol=0, atol=1e-15)
+    # GPU-fitted model -> file -> same predictions, byte-stable document
+    Xf, y, w, _ = make_config("cfg1", n=5000)
+    m = bridge.fit(Xf, y, w, trees=5, depth=3, seed=2)
+    path = str(tmp_path / "m.json")
+    m.save(path)
+    m2 = bridge.load(path)
+    np.testing.assert_array_equal(m.predict(Xf[:500]), m2.predict(Xf[:500]))
+    text = open(path).read()
+    assert serialize_forest(parse_forest(text)) == text

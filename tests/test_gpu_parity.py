@@ -336,3 +336,41 @@ def test_model_file_interop(golden_dir, tmp_path):
     np.testing.assert_array_equal(m.predict(Xf[:500]), m2.predict(Xf[:500]))
     text = open(path).read()
     assert serialize_forest(parse_forest(text)) == text
+
+
+# ------------------------------------------------------------------ other configs
+@pytest.mark.parametrize("name,fixture,n", [("cfg2", "cfg2_slice_fit.npz", 200_000),
+                                            ("cfg3", "cfg3_proxy_fit.npz", 200_000)])
+def test_fit_config_slices_vs_reference_golden(golden_dir, name, fixture, n):
+    """cfg2 slice (ties from discrete features, U(0.5,1.5) weights) and the
+    cfg3-literal proxy (depth 5, highly separable: genuine near-ties, SURVEY
+    A4/A6) against the unmodified reference, teacher-forced at tie-ambiguous
+    nodes only."""
+    g = np.load(f"{golden_dir}/{fixture}")
+    X, y, w, _ = make_config(name, n=n)
+    T, D, eta, alpha, L, seed = g["config"]
+    cfg = FitConfig(n_trees=int(T), depth=int(D), shrinkage=float(eta), subsample=float(alpha),
+                    binning_levels=int(L), seed=int(seed))
+    forced = _forced_from_golden(g)
+    forest = fit_forest(X, y, w, cfg, forced_cuts=forced, return_leaves=True)
+    print(f"{name}: {len(forced)} forced of {g['audit'].shape[0]} nodes")
+    _check_fit_vs_golden(forest, g, X[g["pred_rows"]])
+
+
+def test_cfg5_slice_vs_fixed_point_oracle():
+    """cfg5 shape: 1024 bins (uint16 codes), depth 6, exponential weights,
+    heavy tails — GPU integer arithmetic predicted exactly by the oracle."""
+    X, y, w, _ = make_config("cfg5", n=60_000)
+    kw = dict(n_trees=4, depth=6, shrinkage=0.1, subsample=0.5, levels=10, seed=0)
+    forest = fit_forest(X, y, w, FitConfig(n_trees=4, depth=6, shrinkage=0.1, subsample=0.5, binning_levels=10,
+                                           seed=0), return_leaves=True)
+    ref = oracle.fit_forest(X, y, w, fixed_point=True, record_leaves=True, **kw)
+    np.testing.assert_array_equal(np.stack([b.boundaries for b in forest.binnings]), ref.boundaries)
+    for t in range(4):
+        tr = forest.trees[t]
+        np.testing.assert_array_equal(tr.feature, ref.feature[t])
+        np.testing.assert_array_equal(tr.cut_bin, ref.cut_bin[t])
+        np.testing.assert_array_equal(forest.fit_info["leaves"][t], ref.leaves[t].astype(np.uint16))
+        np.testing.assert_allclose(tr.node_weight, ref.node_weight[t], rtol=1e-12, atol=1e-15)
+    p = predict_batch(forest, X[:3000])
+    assert np.max(np.abs(p - oracle.predict(ref, X[:3000]))) <= 1e-12

@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-apply", action="store_true")
+    ap.add_argument("--apply-rows", type=int, default=100_000_000, help="cfg4 rows for the apply leg")
     return ap.parse_args()
 
 
@@ -160,6 +162,77 @@ def cpu_reference_step(X, y, w, spec, threads=1):
     t_bin = t1 - t0
     t_tree = max(1e-9, (t2 - t1) - t_bin)
     return t_bin, t_tree
+
+
+def run_apply(args, rank, world, local, torch, dist):
+    """cfg4 apply leg: rows/s of predict over a 1000-tree depth-3 forest
+    (BASELINE.json configs[3]).  Rows ~ N(0,1) float32 generated on the
+    device (seed 1); boundaries = 256-bin equal-frequency boundaries of the
+    first 1M rows (GPU binning); forest from datagen.make_apply_forest."""
+    import numpy as np
+
+    from paper_1609_06119_b200 import _lib
+    from paper_1609_06119_b200.datagen import make_apply_forest
+    from paper_1609_06119_b200.engine import FeatureBinning, Forest, Tree, predict_batch, predict_batch_device
+
+    n, d, T = args.apply_rows, 40, 1000
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1)
+    X = torch.randn((n, d), generator=g, device="cuda", dtype=torch.float32)
+    head = X[: min(n, 1_000_000)].cpu().numpy()
+    bnd = np.zeros((d, 255))
+    codes = np.zeros((d, head.shape[0]), np.int16)
+    _lib.check(_lib.lib().bb_bin(_lib.context(local), _lib.ptr(head), _lib.BB_F32, head.shape[0], d, 8,
+                                 _lib.ptr(bnd), _lib.ptr(codes)))
+    feat, cut, thr, nw = make_apply_forest(bnd, n_trees=T, depth=3, seed=1)
+    trees = [Tree(depth=3, feature=feat[t], cut_bin=cut[t], threshold=thr[t], gain=np.zeros(7),
+                  valid=np.ones(7, bool), node_weight=nw[t], node_purity=np.zeros(15)) for t in range(T)]
+    forest = Forest(f0=0.0, trees=trees, binnings=[FeatureBinning(bnd[j], 8) for j in range(d)])
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(max(1, args.warmup)):
+        predict_batch_device(forest, X.data_ptr(), "float32", n, d, out.data_ptr(), device=local)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = []
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        predict_batch_device(forest, X.data_ptr(), "float32", n, d, out.data_ptr(), device=local)
+        e1.record(stream)  # bb_predict returns after its own stream synchronises
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    tot = sum(ms)
+    if dist is not None:
+        t = torch.tensor([tot], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot = float(t.item())
+    value = world * n / (tot / args.steps / 1e3)
+    peak, kind = measured_peak()
+    alg = n * (4 * d + 8)
+    achieved = alg / (tot / args.steps / 1e3) / 1e9
+    visits = n * T * 3
+    # e2e through the public API from pinned host memory on a 10M-row sample
+    ne = min(n, 10_000_000)
+    Xh = X[:ne].cpu().pin_memory().numpy()
+    predict_batch(forest, Xh[:1000])
+    e2e_ms = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        predict_batch(forest, Xh)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    del X, out
+    torch.cuda.empty_cache()
+    return {"metric": "apply rows/s", "value": value, "unit": "rows/s", "ms_per_step": tot / args.steps,
+            "config": {"workload": "cfg4 apply", "rows": n, "features": d, "trees": T, "depth": 3,
+                       "data": "synthetic N(0,1) float32 generated on device (seed 1)"},
+            "roofline": {"bound": "issue", "kernel": "k_apply", "achieved": achieved, "peak": peak,
+                         "peak_kind": kind, "unit": "GB/s", "frac": achieved / peak,
+                         "alg_bytes_per_launch": alg, "node_visits_per_s": visits / (tot / args.steps / 1e3)},
+            "e2e": {"value": ne / (statistics.mean(e2e_ms) / 1e3), "unit": "rows/s", "rows": ne,
+                    "h2d_bytes_per_step": int(Xh.nbytes), "d2h_bytes_per_step": int(ne * 8),
+                    "timing": "host wall clock around predict_batch (pinned input)"}}
 
 
 def run_reference(args, rank, world):
@@ -293,6 +366,8 @@ def run_b200(args, rank, world, local):
                "h2d_bytes_per_step": int(X.nbytes + n + (0 if w is None else w.nbytes)),
                "d2h_bytes_per_step": int(d2h)}
 
+    apply = None if args.no_apply else run_apply(args, rank, world, local, torch, dist)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         t_bin, t_tree = cpu_reference_step(X, y, w, spec)
@@ -315,6 +390,7 @@ def run_b200(args, rank, world, local):
                          "alg_bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_launch_ms,
                          "hist_share_of_step": hist_ms / max(1e-9, total_ms)},
             "cpu_baseline": cpu,
+            "apply": apply,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

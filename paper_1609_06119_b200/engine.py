@@ -293,6 +293,20 @@ def predict_batch(forest: Forest, X, threads: int = 1, *, return_scores: bool = 
     return (p, F) if return_scores else p
 
 
+def predict_batch_device(forest: Forest, x_ptr: int, x_dtype: str, n: int, d: int, out_ptr: int, *,
+                         scores_ptr: int | None = None, device: int = 0) -> None:
+    """predict_batch on device-resident rows: X row-major float32/float64 at
+    ``x_ptr``, probabilities written to the float64 device array ``out_ptr``."""
+    if d != forest.n_features:
+        raise ValueError(f"model expects {forest.n_features} features, rows have {d}")
+    s, keep = _forest_struct(forest)
+    xdt = _lib.BB_F32 if x_dtype == "float32" else _lib.BB_F64
+    ctx = _lib.context(device)
+    _lib.check(_lib.lib().bb_predict(ctx, C.byref(s), C.c_void_p(x_ptr), xdt, 1, n, d, C.c_void_p(out_ptr),
+                                     None if scores_ptr is None else C.c_void_p(scores_ptr), 1))
+    del keep
+
+
 def predict(forest: Forest, row) -> float:
     """Signal probability of a single feature vector (boosting.py:222-227)."""
     row = np.asarray(row, dtype=np.float64)

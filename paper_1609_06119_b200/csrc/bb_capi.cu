@@ -218,10 +218,10 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count) {
   p.tiles_sig1 = (int)ceil_div(s.n_sig, tile);
   p.tiles_bkg0 = (int)(s.n_sig / tile);
   p.tiles_bkg1 = (int)ceil_div(s.n, tile);
-  // one CTA per SM, leaving 2 SMs to the concurrent mask-generation stream
-  // (its single-CTA parse kernel holds one SM for the whole tree)
+  // one CTA per SM, leaving kCl + 1 SMs to the concurrent mask-generation
+  // stream (its cluster parse kernel holds kCl SMs for the whole tree)
   const int groups = p.n_fg * p.n_ng;
-  const int total = std::max(2, (int)((sm_count - 2) / groups));
+  const int total = std::max(2, (int)((sm_count - kCl - 1) / groups));
   const int ts = p.tiles_sig1 - p.tiles_sig0, tb = p.tiles_bkg1 - p.tiles_bkg0;
   p.split_sig = std::max(1, std::min(ts, (int)std::llround((double)total * ts / (ts + tb))));
   p.split_bkg = std::max(1, std::min(tb, total - p.split_sig));
@@ -269,6 +269,7 @@ struct MaskGen {
     hr.uinteger = cfg.pcg_uinteger;
     BB_CUDA(cudaFuncSetAttribute(k_mask_parse, cudaFuncAttributeMaxDynamicSharedMemorySize, kRing * 4));
     BB_CUDA(cudaFuncSetAttribute(k_mask_parse_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, kParseSmem));
+    BB_CUDA(cudaFuncSetAttribute(k_mask_parse_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, kClSmem));
     jump = A.alloc<PcgJump>(1);
     rng = A.alloc<RngState>(1);
     BB_CUDA(cudaMemcpyAsync(jump, &hj, sizeof(hj), cudaMemcpyHostToDevice, st));
@@ -295,17 +296,18 @@ struct MaskGen {
     rec_count = A.alloc<int>(1);
     rec_bits = A.alloc<unsigned char>((size_t)rec_cap * 32);
     if (getenv("BB_PARSE_PROFILE")) {
-      prof = A.alloc<long long>(8);
-      BB_CUDA(cudaMemsetAsync(prof, 0, 64, st));
+      prof = A.alloc<long long>(16);
+      BB_CUDA(cudaMemsetAsync(prof, 0, 128, st));
     }
   }
   void report(cudaStream_t st) {
     if (!prof) return;
-    long long h[8];
+    long long h[16];
     cudaStreamSynchronize(st);
-    cudaMemcpy(h, prof, 64, cudaMemcpyDeviceToHost);
-    fprintf(stderr, "parse phases (cycles): need=%lld classify=%lld scan=%lld list=%lld resolve=%lld jwrite=%lld windows=%lld small=%lld\n",
-            h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
+    cudaMemcpy(h, prof, 128, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "parse prof:");
+    for (int q = 0; q < 16; ++q) fprintf(stderr, " %lld", h[q]);
+    fprintf(stderr, "\n");
   }
 
   // active bits of the next tree into `bits` ([ceil(n/32)] words)
@@ -332,8 +334,10 @@ struct MaskGen {
     pa.prof = prof;
     if (getenv("BB_WARP_PARSE")) {
       k_mask_parse<<<1, 32, kRing * 4, st>>>(pa);
-    } else {
+    } else if (getenv("BB_CTA_PARSE")) {
       k_mask_parse_cta<<<1, kPT, kParseSmem, st>>>(pa);
+    } else {
+      k_mask_parse_cl<<<kCl, kPT, kClSmem, st>>>(pa);
     }
     BB_LAUNCH_CHECK();
     k_expand_windows<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rec_cap, 8), 8 * sm)), 256, 0, st>>>(pa);

@@ -23,6 +23,7 @@
 //                  §Subsample); marks it removed.
 //  k_mask_bits     active bit = not removed, class-block bit order.
 #pragma once
+#include <cooperative_groups.h>
 #include "common.cuh"
 
 namespace bb {
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(kPT, 1) k_mask_parse_cta(ParseArgs a) {
       W = min(W, max(1024, (int)(8.0f * sqrtf((float)m))));
       W = min(W, full - pos);
       long long tq0 = clock64();
-      if (W >= 1024) {
+      if (W >= 64) {
         need(pos, pos + W - 1);
         long long tq1 = clock64();
         // warp w owns draws [512w, 512w+512): row u, lane l -> r = 512w + 32u + l
@@ -492,9 +493,9 @@ __global__ void __launch_bounds__(kPT, 1) k_mask_parse_cta(ParseArgs a) {
             qr += __popc(amb[u]);
           }
         }
-        __syncthreads();
+        if (Q_tot > 0) __syncthreads();
         long long tq4 = clock64();
-        if (warp == 0) {
+        if (Q_tot > 0 && warp == 0) {
           int A = 0;
           for (int base = 0; base < Q_tot; base += 32) {
             const int j = base + lane;
@@ -519,7 +520,8 @@ __global__ void __launch_bounds__(kPT, 1) k_mask_parse_cta(ParseArgs a) {
             s_acc = A;
           }
         }
-        __syncthreads();
+        if (Q_tot > 0) __syncthreads();
+        const int acc_amb = Q_tot > 0 ? s_acc : 0;
         long long tq5 = clock64();
         // J of every accepted draw (consecutive lanes -> consecutive steps);
         // windows entirely below k only need their accept count
@@ -541,7 +543,7 @@ __global__ void __launch_bounds__(kPT, 1) k_mask_parse_cta(ParseArgs a) {
             qr += __popc(amb[u]);
           }
         }
-        i -= S_tot + s_acc;
+        i -= S_tot + acc_amb;
         pos += W;
         __syncthreads();
         if (a.prof && tid == 0) {
@@ -614,6 +616,533 @@ __global__ void __launch_bounds__(kPT, 1) k_mask_parse_cta(ParseArgs a) {
       const U128 st = pcg_jump(*a.jump, r0.s, outs);
       r.s = st;
       if (d & 1) {
+        r.has_uint32 = 1;
+        r.uinteger = (unsigned int)(xsl_rr(st) >> 32);
+      } else {
+        r.has_uint32 = 0;
+        r.uinteger = 0;
+      }
+    }
+    *a.rng = r;
+  }
+}
+
+// Resolve an ordered list of ambiguous draws (one warp): entry j is accepted
+// iff A_before(j) <= key[j], A_before = accepted entries before j; writes
+// apref[j] = A_before(j) and apref[Q] = total.  128 entries per iteration:
+// an entry is a sure reject if key < A, a sure accept if key >= A + (entries
+// before it in the block that are not sure rejects); on the first unsure
+// entry the decided prefix is committed and that entry resolved exactly.
+__device__ __forceinline__ void resolve_list(const int* __restrict__ akey, int* __restrict__ apref, int Q, int lane) {
+  const unsigned lt = (1u << lane) - 1u;
+  int A = 0, base = 0;
+  while (base < Q) {
+    int key[4];
+    bool nr[4];
+    unsigned bn[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = base + u * 32 + lane;
+      key[u] = j < Q ? akey[j] : 0;
+      nr[u] = j < Q && key[u] >= A;  // not a sure reject
+      bn[u] = __ballot_sync(0xffffffffu, nr[u]);
+    }
+    int pre = 0;
+    unsigned unsure[4];
+    int bnr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      bnr[u] = pre + __popc(bn[u] & lt);  // non-rejects before this entry
+      unsure[u] = __ballot_sync(0xffffffffu, nr[u] && key[u] < A + bnr[u]);
+      pre += __popc(bn[u]);
+    }
+    int f = 128;  // first unsure entry (block-relative)
+#pragma unroll
+    for (int u = 3; u >= 0; --u)
+      if (unsure[u]) f = u * 32 + __ffs(unsure[u]) - 1;
+    // entries before f: every non-reject is accepted
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int jl = u * 32 + lane;
+      if (jl < f && base + jl < Q) apref[base + jl] = A + bnr[u];
+    }
+    if (f == 128) {
+      A += pre;
+      base += 128;
+    } else {
+      // exact decision for entry f
+      const int uf = f >> 5, lf = f & 31;
+      const int kf = __shfl_sync(0xffffffffu, key[uf], lf);
+      const int bf = __shfl_sync(0xffffffffu, bnr[uf], lf);
+      const int Af = A + bf;
+      if (lane == 0) apref[base + f] = Af;
+      A = Af + (kf >= Af ? 1 : 0);
+      base += f + 1;
+    }
+  }
+  if (lane == 0) apref[Q] = A;
+}
+
+// ----------------------------------------------------------- cluster parse
+// Same contract again, spread over a cluster of kCl CTAs (8 SMs): a window
+// of W <= kCl * kPW draws inside one mask band; CTA r classifies draws
+// [r*kPW, (r+1)*kPW) of the window with the interleaved row layout of
+// k_mask_parse_cta, the per-CTA (sure-accept, ambiguous) counts and the
+// ambiguous keys meet in CTA 0 through distributed shared memory, warp 0 of
+// CTA 0 resolves the ambiguous list, every CTA copies back the slice of the
+// accepted-ambiguous prefix it needs and writes its J values.  Slices of
+// the next window are prefetched with cp.async while the current one is
+// resolved.  Short stretches (band bottoms, small i, buffer tail) are walked
+// by CTA 0 alone.
+constexpr int kCl = 8;
+constexpr int kClW = kCl * kPW;        // 65536
+constexpr int kQcap = 12288;            // ambiguous-list capacity (expected ~W^2/2m <= ~2k)
+constexpr int kSlice = kPW + 16;        // slice buffer stride (room for the alignment offset)
+constexpr int kClSmem = 2 * kSlice * 4 + kQcap * 4 + (kQcap + 1) * 4 + 64;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+#define BB_PMARK(slot, t0)                                             \
+  do {                                                                  \
+    if (a.prof && crank == 0 && tid == 0) a.prof[slot] += clock64() - (t0); \
+  } while (0)
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_parse_cl(ParseArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char csm[];
+  unsigned int* buf0 = reinterpret_cast<unsigned int*>(csm);  // [2][kSlice] this CTA's slices
+  int* akey = reinterpret_cast<int*>(buf0 + 2 * kSlice);       // CTA 0: ambiguous keys in draw order
+  int* apref = akey + kQcap;                                    // CTA 0: accepted-ambiguous prefix
+  __shared__ int s_warp[64];
+  __shared__ int s_cnt[4 * kCl];   // CTA 0: per-CTA (sure, amb) counts, then (accepted) counts
+  __shared__ int s_state[4];       // broadcast: i, pos, cross position
+  __shared__ int s_apl[kPW / 32 + 64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int crank = (int)cl.block_rank();
+  const RngState r0 = *a.rng;
+  const long long nd = a.n_draws;
+  int* apref0 = cl.map_shared_rank(apref, 0);
+  int* akey0 = cl.map_shared_rank(akey, 0);
+  int* cnt0 = cl.map_shared_rank(s_cnt, 0);
+  int* state0 = cl.map_shared_rank(s_state, 0);
+  int cur = 0, loaded_at = -1;
+  int boff[2] = {0, 0};
+  if (crank == 0 && tid == 0) {
+    s_state[1] = 0;
+    s_state[2] = 1 << 30;  // crossing draw (min over CTAs)
+    s_state[3] = 1 << 30;  // first overflowing ambiguous draw
+  }
+  cl.sync();
+  auto load_slice = [&](int bsel, int wstart) {
+    const long long base = (long long)wstart + (long long)crank * kPW;
+    const long long abase = base & ~3ll;
+    boff[bsel] = (int)(base - abase);
+    unsigned int* dst = buf0 + bsel * kSlice;
+    for (int j = tid; j < (kPW + 4) / 4; j += kPT) {
+      const long long src = abase + 4ll * j;
+      if (src + 4 <= nd) cp_async16(dst + 4 * j, a.draws + src);
+    }
+    cp_async_commit();
+  };
+  auto get = [&](long long idx) -> unsigned int {
+    return idx < nd ? __ldg(&a.draws[idx]) : draw_at(*a.jump, r0, idx);
+  };
+  int pos = 0;
+  for (int c = 0; c < 2; ++c) {
+    const int n = a.n[c], k = a.k[c];
+    int* J = a.J[c];
+    int i = n - 1;
+    while (i >= 1) {
+      const unsigned int m0 = smear((unsigned)i);
+      int W = min(kClW, max(4096, (int)(48.0f * sqrtf((float)m0))));
+      if ((long long)pos + W > nd) W = (int)max(0ll, nd - pos);
+      if (i >= 64 && W >= 4096) {
+        // ---- one window [pos, pos+W), processed in rounds; a round ends
+        // where the band's last step is taken (mask changes) or at the
+        // window end
+        const long long tw0 = clock64();
+        if (loaded_at != pos) {
+          load_slice(cur, pos);
+          loaded_at = pos;
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        if (a.prof && crank == 0 && tid == 0) a.prof[5] += clock64() - tw0;  // slice wait
+        load_slice(cur ^ 1, pos + W);  // prefetch (valid if the window is fully consumed)
+        const unsigned int* sl = buf0 + cur * kSlice + boff[cur];
+        const int rw = warp * 512, rbase = crank * kPW;
+        int rs = 0;           // round start (window-relative)
+        bool perm_done = false;
+        while (rs < W && i >= 1) {
+          const long long tR = clock64();
+          const unsigned int m = smear((unsigned)i);
+          const int half = (int)(m >> 1);
+          const int d = i - half;  // acceptances until the band's last step
+          unsigned sab[16], amb[16];
+          int ws = 0, wq = 0;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int rl = rw + u * 32 + lane;
+            const int r = rbase + rl;
+            const bool in = r >= rs && r < W;
+            const unsigned int v = in ? (sl[rl] & m) : 0u;
+            const int off = r - rs;
+            const bool acc = in && (int)v <= i - off;
+            const bool amg = in && !acc && (int)v <= i;
+            sab[u] = __ballot_sync(0xffffffffu, acc);
+            amb[u] = __ballot_sync(0xffffffffu, amg);
+            ws += __popc(sab[u]);
+            wq += __popc(amb[u]);
+          }
+          if (lane == 0) {
+            s_warp[warp] = ws;
+            s_warp[16 + warp] = wq;
+          }
+          __syncthreads();
+          int S_w = 0, Q_w = 0, S_c = 0, Q_c = 0;
+#pragma unroll
+          for (int w2 = 0; w2 < 16; ++w2) {
+            const int x1 = s_warp[w2], x2 = s_warp[16 + w2];
+            if (w2 < warp) {
+              S_w += x1;
+              Q_w += x2;
+            }
+            S_c += x1;
+            Q_c += x2;
+          }
+          if (tid == 0) {
+            cnt0[2 * crank] = S_c;
+            cnt0[2 * crank + 1] = Q_c;
+          }
+          long long tr1 = clock64();
+          BB_PMARK(8, tR);  // classify (+warp totals)
+          cl.sync();  // (1)
+          if (a.prof && crank == 0 && tid == 0) a.prof[6] += clock64() - tr1;  // sync (1) wait
+          int S_before = 0, Q_before = 0, Q_tot = 0;
+#pragma unroll
+          for (int q = 0; q < kCl; ++q) {
+            const int x1 = cnt0[2 * q], x2 = cnt0[2 * q + 1];
+            if (q < crank) {
+              S_before += x1;
+              Q_before += x2;
+            }
+            Q_tot += x2;
+          }
+          const int Qres = min(Q_tot, kQcap);  // entries beyond the cap: resolved serially below
+          {
+            int sr = S_before + S_w, qr = Q_before + Q_w;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              if ((amb[u] >> lane) & 1u) {
+                const int q = qr + __popc(amb[u] & lt);
+                const int rl = rw + u * 32 + lane;
+                if (q < kQcap) akey0[q] = i - (sr + __popc(sab[u] & lt)) - (int)(sl[rl] & m);
+              }
+              sr += __popc(sab[u]);
+              qr += __popc(amb[u]);
+            }
+          }
+          const long long tK = clock64();
+          cl.sync();  // (2)
+          BB_PMARK(9, tK);  // sync 2
+          const long long tS = clock64();
+          if (crank == 0) {
+            // warps 1.. of CTA 0 sleep on the CTA barrier (not the cluster
+            // barrier) while warp 0 resolves, leaving it the issue slots
+            if (warp == 0) {
+              if (a.prof && lane == 0) a.prof[14] += Qres;
+              resolve_list(akey, apref, Qres, lane);
+            }
+            __syncthreads();
+          }
+          long long tr3 = clock64();
+          BB_PMARK(10, tS);  // resolve
+          cl.sync();  // (3)
+          if (a.prof && crank == 0 && tid == 0) a.prof[7] += clock64() - tr3;  // sync (3) wait (after resolve)
+          int S_tot = 0;
+#pragma unroll
+          for (int q = 0; q < kCl; ++q) S_tot += cnt0[2 * q];
+          const int A_amb = apref0[Qres];
+          BB_PMARK(13, tr3);  // sync3 + totals
+          // local copy of the accepted-ambiguous prefix slice this CTA needs
+          // (CTA r != 0 reuses its own, otherwise idle, apref array)
+          int* apl = (crank == 0) ? apref + Q_before : akey;
+          const int ncopy = min(Q_c, max(0, Qres - Q_before)) + 1;
+          if (crank != 0)
+            for (int q = tid; q < ncopy; q += kPT) apl[q] = apref0[min(Q_before + q, Qres)];
+          __syncthreads();
+          auto APF = [&](int qg) -> int {  // accepted-ambiguous before global entry qg (qg <= Qres)
+            const int ql = qg - Q_before;
+            return (ql >= 0 && ql < ncopy) ? apl[ql] : apref0[min(qg, Qres)];
+          };
+          const long long tC = clock64();
+          if (Q_tot <= kQcap && S_tot + A_amb < d) {
+            // common case: no band crossing in the rest of the window, every
+            // draw decided -> commit all (J only needed for steps >= k)
+            if (i >= k) {
+              int sr = S_before + S_w, qr = Q_before + Q_w;
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const bool sacc = (sab[u] >> lane) & 1u;
+                const bool isamb = (amb[u] >> lane) & 1u;
+                if (sacc || isamb) {
+                  const int q = qr + __popc(amb[u] & lt);
+                  const int ab = APF(q);
+                  if (sacc || APF(q + 1) - ab == 1) {
+                    const int st = i - (sr + __popc(sab[u] & lt)) - ab;
+                    if (st >= k) J[st] = (int)(sl[rw + u * 32 + lane] & m);
+                  }
+                }
+                sr += __popc(sab[u]);
+                qr += __popc(amb[u]);
+              }
+            }
+            i -= S_tot + A_amb;
+            rs = W;
+            BB_PMARK(11, tC);  // common commit
+            cl.sync();  // (4') CTA 0 list / counters free
+            if (a.prof && crank == 0 && tid == 0) a.prof[2] += 1;
+            break;
+          }
+          // ---- detailed path: a band crossing (or list overflow) in this round
+          if (a.prof && crank == 0 && tid == 0) a.prof[3] += 1;
+          const long long tD = clock64();
+          unsigned accm[16];
+          int wa = 0;
+          {
+            int qr = Q_before + Q_w;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              unsigned am_acc = 0;
+              if ((amb[u] >> lane) & 1u) {
+                const int q = qr + __popc(amb[u] & lt);
+                const bool ok = q < Qres && APF(q + 1) - APF(q) == 1;
+                am_acc = ok ? 1u : 0u;
+              }
+              accm[u] = sab[u] | __ballot_sync(0xffffffffu, am_acc);
+              wa += __popc(accm[u]);
+              qr += __popc(amb[u]);
+            }
+          }
+          // first draw of the window that overflowed the ambiguous list
+          int rcut = W;
+          if (Q_tot > kQcap) {  // state0[3] holds 1<<30 until set here
+            int qr = Q_before + Q_w, first = W;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              if ((amb[u] >> lane) & 1u) {
+                const int q = qr + __popc(amb[u] & lt);
+                if (q == kQcap) first = rbase + rw + u * 32 + lane;
+              }
+              qr += __popc(amb[u]);
+            }
+            first = __reduce_min_sync(0xffffffffu, first);
+            if (lane == 0) s_warp[32 + warp] = first;
+            __syncthreads();
+            if (tid == 0) {
+              int f = W;
+              for (int w2 = 0; w2 < 16; ++w2) f = min(f, s_warp[32 + w2]);
+              atomicMin(&state0[3], f);  // CTA 0's state[3] initialised to W below
+            }
+          }
+          if (lane == 0) s_warp[48 + warp] = wa;
+          __syncthreads();
+          int A_w = 0, A_c = 0;
+#pragma unroll
+          for (int w2 = 0; w2 < 16; ++w2) {
+            const int x = s_warp[48 + w2];
+            if (w2 < warp) A_w += x;
+            A_c += x;
+          }
+          if (tid == 0) cnt0[2 * kCl + crank] = A_c;
+          cl.sync();  // (4)
+          if (Q_tot > kQcap) rcut = min(W, state0[3]);
+          int A_before = 0, A_tot = 0;
+#pragma unroll
+          for (int q = 0; q < kCl; ++q) {
+            const int x = cnt0[2 * kCl + q];
+            if (q < crank) A_before += x;
+            A_tot += x;
+          }
+          // crossing: the d-th acceptance (band's last step) ends the round
+          int rend = rcut;  // exclusive end of committed draws
+          bool crossed = false;
+          if (A_tot >= d) {
+            // find the draw with accepted prefix count == d (1-based)
+            int found = W;
+            if (A_before < d && d <= A_before + A_c) {
+              int run = A_before + A_w;
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const bool acc = (accm[u] >> lane) & 1u;
+                const int cnt_incl = run + __popc(accm[u] & lt) + (acc ? 1 : 0);
+                if (acc && cnt_incl == d) found = rbase + rw + u * 32 + lane;
+                run += __popc(accm[u]);
+              }
+              found = __reduce_min_sync(0xffffffffu, found);
+              if (lane == 0 && found < W) atomicMin(&state0[2], found);
+            }
+            cl.sync();  // (5)
+            const int rx = state0[2];
+            if (rx + 1 < rend) {
+              rend = rx + 1;
+              crossed = true;
+            } else if (rx + 1 == rend) {
+              crossed = true;
+            }
+          }
+          // overflow cut: draws at/after rcut are undecided -> round ends there
+          // (the cut draw itself is resolved serially by CTA 0 below)
+          // commit J for accepted draws in [rs, rend)
+          int committed_acc = 0;
+          {
+            int run = A_before + A_w;  // accepted before this lane's row-0 draw, within the round
+            int qr = Q_before + Q_w;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              const int r = rbase + rw + u * 32 + lane;
+              const bool acc = (accm[u] >> lane) & 1u;
+              const int before = run + __popc(accm[u] & lt);
+              if (acc && r < rend) {
+                const int st = i - before;
+                if (st >= k) J[st] = (int)(sl[rw + u * 32 + lane] & m);
+              }
+              run += __popc(accm[u]);
+              qr += __popc(amb[u]);
+            }
+            (void)qr;
+          }
+          // accepted count within [rs, rend): d if crossed, else all decided accepts before rend
+          if (crossed) {
+            committed_acc = d;
+          } else if (rend == W) {
+            committed_acc = A_tot;
+          } else {
+            // overflow cut without crossing: count accepts before rcut (cluster reduce)
+            int cnt = 0;
+            int run = 0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              const int r = rbase + rw + u * 32 + lane;
+              if (((accm[u] >> lane) & 1u) && r < rend) ++cnt;
+              run += 0;
+            }
+            cnt = __reduce_add_sync(0xffffffffu, cnt);
+            if (lane == 0) atomicAdd(&state0[1], cnt);
+            cl.sync();
+            committed_acc = state0[1];
+          }
+          cl.sync();  // (6) everyone has read state0 / cnt0
+          if (crank == 0 && tid == 0) {
+            state0[1] = 0;
+            state0[2] = 1 << 30;
+            state0[3] = 1 << 30;
+          }
+          i -= committed_acc;
+          rs = rend;
+          if (!crossed && rend < W) {
+            // overflow cut: CTA 0 resolves the cut draw serially, then the round restarts after it
+            if (crank == 0 && tid == 0) {
+              const unsigned int v = get((long long)pos + rend) & smear((unsigned)i);
+              int ii = i;
+              if ((int)v <= ii) {
+                if (ii >= k) J[ii] = (int)v;
+                --ii;
+              }
+              for (int q = 0; q < kCl; ++q) cl.map_shared_rank(s_state, q)[0] = ii;
+            }
+            cl.sync();
+            i = s_state[0];
+            rs = rend + 1;
+            cl.sync();
+          }
+          BB_PMARK(12, tD);  // detailed path
+          if (i == 0) {
+            perm_done = true;
+            break;
+          }
+        }
+        if (a.prof && crank == 0 && tid == 0) {
+          a.prof[0] += clock64() - tw0;
+          a.prof[1] += 1;
+          a.prof[4] += rs;
+        }
+        pos += rs;
+        cur ^= 1;
+        loaded_at = (rs == W) ? pos : -1;  // prefetch valid only if the whole window was consumed
+        (void)perm_done;
+      } else {
+        // short stretch (i < 64, or the buffer tail): CTA 0 stages draws in
+        // smem, warp 0 walks them serially, then broadcasts i and pos
+        constexpr int kSt = 4096;
+        const long long ts0 = clock64();
+        cp_async_wait_all();
+        __syncthreads();
+        loaded_at = -1;
+        if (crank == 0) {
+          unsigned int* stg = buf0;
+          for (int j = tid; j < kSt + 64; j += kPT) {
+            const long long idx = (long long)pos + j;
+            stg[j] = idx < nd ? __ldg(&a.draws[idx]) : 0u;
+          }
+          __syncthreads();
+          if (warp == 0) {
+            const int pos0 = pos;
+            const int stop = pos + kSt;
+            while (i >= 1 && pos < stop) {
+              const int o = pos - pos0;
+              const unsigned int vv = ((long long)pos < nd ? stg[o] : get((long long)pos)) & smear((unsigned)i);
+              ++pos;
+              if ((int)vv <= i) {
+                if (lane == 0 && i >= k) J[i] = (int)vv;
+                --i;
+              }
+            }
+            if (lane == 0)
+              for (int q = 0; q < kCl; ++q) {
+                int* st = cl.map_shared_rank(s_state, q);
+                st[0] = i;
+                st[1] = pos;
+              }
+          }
+          __syncthreads();
+        }
+        cl.sync();
+        i = s_state[0];
+        pos = s_state[1];
+        cl.sync();
+        if (crank == 0 && tid == 0) {
+          s_state[1] = 0;
+          s_state[2] = 1 << 30;
+          s_state[3] = 1 << 30;
+          if (a.prof) {
+            a.prof[5] += clock64() - ts0;
+            a.prof[6] += 1;
+          }
+        }
+        cl.sync();
+      }
+    }
+  }
+  cp_async_wait_all();
+  if (crank == 0 && tid == 0) {
+    *a.rec_count = 0;
+    RngState r = r0;
+    long long dd = pos;
+    if (r.has_uint32 && dd > 0) {
+      r.has_uint32 = 0;
+      dd -= 1;
+    }
+    if (dd > 0) {
+      const unsigned long long outs = (unsigned long long)((dd + 1) / 2);
+      const U128 st = pcg_jump(*a.jump, r0.s, outs);
+      r.s = st;
+      if (dd & 1) {
         r.has_uint32 = 1;
         r.uinteger = (unsigned int)(xsl_rr(st) >> 32);
       } else {

@@ -718,9 +718,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
   int* akey = reinterpret_cast<int*>(buf0 + 2 * kSlice);       // CTA 0: ambiguous keys in draw order
   int* apref = akey + kQcap;                                    // CTA 0: accepted-ambiguous prefix
   __shared__ int s_warp[64];
-  __shared__ int s_cnt[4 * kCl];   // CTA 0: per-CTA (sure, amb) counts, then (accepted) counts
+  __shared__ int s_cnt[8 * kCl];   // CTA 0: per-CTA (sure, amb) counts (2 banks), accepted counts
   __shared__ int s_state[4];       // broadcast: i, pos, cross position
-  __shared__ int s_apl[kPW / 32 + 64];
+  __shared__ int s_loc[2 * kCl];    // local copy of the last exchanged counters
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const int crank = (int)cl.block_rank();
@@ -752,6 +752,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
   auto get = [&](long long idx) -> unsigned int {
     return idx < nd ? __ldg(&a.draws[idx]) : draw_at(*a.jump, r0, idx);
   };
+  // after a cluster sync: copy cnt0[bank .. bank + cnt) into s_loc once (few
+  // DSMEM loads) instead of every thread reading CTA 0's counters remotely
+  auto fetch = [&](int bank, int cnt) {
+    if (tid < cnt) s_loc[tid] = cnt0[bank + tid];
+    __syncthreads();
+  };
   int pos = 0;
   for (int c = 0; c < 2; ++c) {
     const int n = a.n[c], k = a.k[c];
@@ -759,7 +765,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
     int i = n - 1;
     while (i >= 1) {
       const unsigned int m0 = smear((unsigned)i);
-      int W = min(kClW, max(4096, (int)(48.0f * sqrtf((float)m0))));
+      (void)m0;
+      int W = kClW;  // ambiguity is refined away below, so windows need no sqrt(m) cap
       if ((long long)pos + W > nd) W = (int)max(0ll, nd - pos);
       if (i >= 64 && W >= 4096) {
         // ---- one window [pos, pos+W), processed in rounds; a round ends
@@ -772,7 +779,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
         }
         cp_async_wait_all();
         __syncthreads();
-        if (a.prof && crank == 0 && tid == 0) a.prof[5] += clock64() - tw0;  // slice wait
+        if (a.prof && crank == 0 && tid == 0) a.prof[13] += clock64() - tw0;  // slice wait
         load_slice(cur ^ 1, pos + W);  // prefetch (valid if the window is fully consumed)
         const unsigned int* sl = buf0 + cur * kSlice + boff[cur];
         const int rw = warp * 512, rbase = crank * kPW;
@@ -822,16 +829,96 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
           long long tr1 = clock64();
           BB_PMARK(8, tR);  // classify (+warp totals)
           cl.sync();  // (1)
-          if (a.prof && crank == 0 && tid == 0) a.prof[6] += clock64() - tr1;  // sync (1) wait
+
+          fetch(0, 2 * kCl);
           int S_before = 0, Q_before = 0, Q_tot = 0;
 #pragma unroll
           for (int q = 0; q < kCl; ++q) {
-            const int x1 = cnt0[2 * q], x2 = cnt0[2 * q + 1];
+            const int x1 = s_loc[2 * q], x2 = s_loc[2 * q + 1];
             if (q < crank) {
               S_before += x1;
               Q_before += x2;
             }
             Q_tot += x2;
+          }
+          int s_bank = 0;
+          if (a.prof && crank == 0 && tid == 0) a.prof[4] += Q_tot;  // Q before refinement
+          // refinement: accepted-before(r) lies in [S_before(r), S_before(r) + U_before(r)]
+          // (sure accepts, still-ambiguous draws before r) -> re-test the
+          // ambiguous draws against those bounds (Jacobi: counts of the
+          // previous pass), exchange counts, repeat
+          for (int pass = 0; pass < 8 && Q_tot > 64; ++pass) {
+            int sr = S_before + S_w, qr = Q_before + Q_w;
+            int ws2 = 0, wq2 = 0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              const unsigned sa0 = sab[u], am0 = amb[u];
+              bool na = false, nrj = false;
+              if ((am0 >> lane) & 1u) {
+                const int rl = rw + u * 32 + lane;
+                const int v = (int)(sl[rl] & m);
+                const int Sb = sr + __popc(sa0 & lt);
+                const int Ub = qr + __popc(am0 & lt);
+                na = v <= i - Sb - Ub;
+                // Sb >= d: the band's last step was taken before this draw, so
+                // it belongs to the next round (re-classified under the next
+                // mask) -> drop it from this round's list
+                nrj = v > i - Sb || Sb >= d;
+                if (Sb >= d) na = false;
+              }
+              const unsigned ba = __ballot_sync(0xffffffffu, na);
+              const unsigned br = __ballot_sync(0xffffffffu, nrj);
+              sab[u] = sa0 | ba;
+              amb[u] = am0 & ~(ba | br);
+              sr += __popc(sa0);
+              qr += __popc(am0);
+              ws2 += __popc(sab[u]);
+              wq2 += __popc(amb[u]);
+            }
+            __syncthreads();  // everyone has read s_warp of the previous exchange
+            if (lane == 0) {
+              s_warp[warp] = ws2;
+              s_warp[16 + warp] = wq2;
+            }
+            __syncthreads();
+            S_w = 0;
+            Q_w = 0;
+            S_c = 0;
+            Q_c = 0;
+#pragma unroll
+            for (int w2 = 0; w2 < 16; ++w2) {
+              const int x1 = s_warp[w2], x2 = s_warp[16 + w2];
+              if (w2 < warp) {
+                S_w += x1;
+                Q_w += x2;
+              }
+              S_c += x1;
+              Q_c += x2;
+            }
+            const int bank = 2 * kCl * ((pass + 1) & 1);
+            if (tid == 0) {
+              cnt0[bank + 2 * crank] = S_c;
+              cnt0[bank + 2 * crank + 1] = Q_c;
+            }
+            cl.sync();
+            fetch(bank, 2 * kCl);
+            S_before = 0;
+            Q_before = 0;
+            Q_tot = 0;
+#pragma unroll
+            for (int q = 0; q < kCl; ++q) {
+              const int x1 = s_loc[2 * q], x2 = s_loc[2 * q + 1];
+              if (q < crank) {
+                S_before += x1;
+                Q_before += x2;
+              }
+              Q_tot += x2;
+            }
+            s_bank = bank;
+            if (a.prof && crank == 0 && tid == 0) {
+              a.prof[15] += 1;
+              if (pass < 3) a.prof[5 + pass] += Q_tot;
+            }
           }
           const int Qres = min(Q_tot, kQcap);  // entries beyond the cap: resolved serially below
           {
@@ -863,10 +950,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
           long long tr3 = clock64();
           BB_PMARK(10, tS);  // resolve
           cl.sync();  // (3)
-          if (a.prof && crank == 0 && tid == 0) a.prof[7] += clock64() - tr3;  // sync (3) wait (after resolve)
-          int S_tot = 0;
-#pragma unroll
-          for (int q = 0; q < kCl; ++q) S_tot += cnt0[2 * q];
+
+          // S_tot from this CTA's view: S_before + own + after (all banks agree
+          // only per pass, so recompute from the last exchange's bank)
+          int S_tot = S_before + S_c;
+          for (int q = crank + 1; q < kCl; ++q) S_tot += s_loc[2 * q];  // s_loc holds bank s_bank
+          (void)s_bank;
           const int A_amb = apref0[Qres];
           BB_PMARK(13, tr3);  // sync3 + totals
           // local copy of the accepted-ambiguous prefix slice this CTA needs
@@ -959,13 +1048,14 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
             if (w2 < warp) A_w += x;
             A_c += x;
           }
-          if (tid == 0) cnt0[2 * kCl + crank] = A_c;
+          if (tid == 0) cnt0[4 * kCl + crank] = A_c;
           cl.sync();  // (4)
           if (Q_tot > kQcap) rcut = min(W, state0[3]);
+          fetch(4 * kCl, kCl);
           int A_before = 0, A_tot = 0;
 #pragma unroll
           for (int q = 0; q < kCl; ++q) {
-            const int x = cnt0[2 * kCl + q];
+            const int x = s_loc[q];
             if (q < crank) A_before += x;
             A_tot += x;
           }

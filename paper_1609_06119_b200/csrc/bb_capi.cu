@@ -230,7 +230,12 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count) {
 
 static inline int hist_grid(const HistPlan& p) { return p.n_fg * p.n_ng * (p.split_sig + p.split_bkg); }
 
-// GPU subsample-mask generator: per tree, on its own stream (kernels_mask.cuh)
+// GPU subsample-mask generator on its own stream (kernels_mask.cuh).  One
+// cluster launch parses a chunk of up to kChunk trees back to back (the u32
+// draw stream is continuous across trees), so the 8-SM cluster is placed
+// once per chunk; the per-tree resolution kernels follow.
+constexpr int kChunk = 8;
+
 struct MaskGen {
   PcgJump* jump = nullptr;
   RngState* rng = nullptr;
@@ -241,14 +246,16 @@ struct MaskGen {
   int *rec_pos = nullptr, *rec_i = nullptr, *rec_len = nullptr, *rec_count = nullptr;
   unsigned char* rec_bits = nullptr;
   int rec_cap = 0;
-  long long* prof = nullptr;  // BB_PARSE_PROFILE: phase cycles, printed at destruction
+  long long* prof = nullptr;  // BB_PARSE_PROFILE: phase cycles, printed at the end
   unsigned char* removed[2] = {nullptr, nullptr};
   int n[2] = {0, 0}, k[2] = {0, 0};
   int sm = 148;
+  bool single = false;  // single-tree legacy parse kernels (debug env)
 
   void init(Arena& A, cudaStream_t st, int64_t n_sig, int64_t n_bkg, double rate, const bb_fit_config& cfg,
             int sm_count) {
     sm = sm_count;
+    single = getenv("BB_WARP_PARSE") || getenv("BB_CTA_PARSE");
     n[0] = (int)n_sig;
     n[1] = (int)n_bkg;
     k[0] = (int)subsample_count(n_sig, rate);
@@ -276,11 +283,14 @@ struct MaskGen {
     BB_CUDA(cudaMemcpyAsync(rng, &hr, sizeof(hr), cudaMemcpyHostToDevice, st));
     BB_CUDA(cudaStreamSynchronize(st));  // host staging structs go out of scope
     const int64_t steps = n_sig + n_bkg;
-    n_draws = (long long)(1.5 * (double)steps) + 65536;
+    const int chunk = single ? 1 : kChunk;
+    // E[draws/step] = mean of (mask+1)/(i+1) <= ~1.45 (2 ln 2 asymptotically) and < 2
+    // always; beyond the buffer the parse falls back to per-draw jump-ahead
+    n_draws = (long long)(2.0 * (double)steps * chunk) + 65536;
     draws = A.alloc<unsigned int>((size_t)n_draws);
     const int nmax = std::max(n[0], n[1]);
     for (int cc = 0; cc < 2; ++cc) {
-      J[cc] = A.alloc<int>(std::max(1, n[cc]));
+      J[cc] = A.alloc<int>((size_t)std::max(1, std::max(n[0], n[1])) * chunk);  // stride = larger class
       removed[cc] = A.alloc<unsigned char>(std::max(1, n[cc]));
     }
     cnt = A.alloc<int>(nmax + 1);
@@ -288,7 +298,7 @@ struct MaskGen {
     fill = A.alloc<int>(nmax + 1);
     bucket = A.alloc<int>(nmax + 1);
     sums = A.alloc<int>(ceil_div(nmax, kScanBlock) + 1);
-    rec_cap = (int)(n_draws / 64 + 1024);
+    rec_cap = single ? (int)(n_draws / 64 + 1024) : 1;
     if (const char* e = getenv("BB_DEBUG_REC_CAP")) rec_cap = std::max(1, atoi(e));  // debug: force fallback
     rec_pos = A.alloc<int>(rec_cap);
     rec_i = A.alloc<int>(rec_cap);
@@ -310,8 +320,10 @@ struct MaskGen {
     fprintf(stderr, "\n");
   }
 
-  // active bits of the next tree into `bits` ([ceil(n/32)] words)
-  void enqueue(cudaStream_t st, unsigned int* bits, int64_t& launches) {
+  // masks of `count` consecutive trees; bits[j] = output words of tree j,
+  // ready[j] (optional) recorded when tree j's bits are written
+  void enqueue_chunk(cudaStream_t st, unsigned int* const* bits, int count, const cudaEvent_t* ready,
+                     int64_t& launches) {
     const long long n_out = (n_draws + 1) / 2;
     k_pcg_draws<<<(unsigned)ceil_div(ceil_div(n_out, kDrawChunk), 256), 256, 0, st>>>(jump, rng, draws, n_draws);
     BB_LAUNCH_CHECK();
@@ -332,40 +344,53 @@ struct MaskGen {
     pa.rec_count = rec_count;
     pa.rec_cap = rec_cap;
     pa.prof = prof;
-    if (getenv("BB_WARP_PARSE")) {
-      k_mask_parse<<<1, 32, kRing * 4, st>>>(pa);
-    } else if (getenv("BB_CTA_PARSE")) {
-      k_mask_parse_cta<<<1, kPT, kParseSmem, st>>>(pa);
-    } else {
-      k_mask_parse_cl<<<kCl, kPT, kClSmem, st>>>(pa);
-    }
-    BB_LAUNCH_CHECK();
-    k_expand_windows<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rec_cap, 8), 8 * sm)), 256, 0, st>>>(pa);
-    BB_LAUNCH_CHECK();
-    launches += 4;
-    for (int cc = 0; cc < 2; ++cc) {
-      const int nn = n[cc], kk = k[cc];
-      // k == 0: nothing is active (position 0 is never a step target)
-      BB_CUDA(cudaMemsetAsync(removed[cc], kk == 0 ? 1 : 0, (size_t)std::max(1, nn), st));
-      if (kk == 0 || nn <= 1 || kk >= nn) continue;
-      BB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)nn * 4, st));
-      BB_CUDA(cudaMemsetAsync(fill, 0, (size_t)nn * 4, st));
-      const int g = grid_for(nn - kk, 256, sm);
-      k_bucket_count<<<g, 256, 0, st>>>(J[cc], kk, nn, cnt);
-      const int nb = (int)ceil_div(nn, kScanBlock);
-      k_scan_block_sums<<<nb, 256, 0, st>>>(cnt, nn, sums);
-      k_scan_sums<<<1, 1024, 0, st>>>(sums, nb);
-      k_scan_apply<<<nb, 256, 0, st>>>(cnt, nn, sums, off);
-      k_bucket_fill<<<g, 256, 0, st>>>(J[cc], kk, nn, off, fill, bucket);
-      k_bucket_sort<<<grid_for(nn, 256, sm), 256, 0, st>>>(cnt, off, nn, bucket);
-      k_resolve<<<g, 256, 0, st>>>(J[cc], kk, nn, cnt, off, bucket, removed[cc]);
+    pa.n_trees = count;
+    pa.J_stride = 0;  // set per class below via J offsets: tree t at J[c] + t * n[c]
+    if (single) {
+      if (getenv("BB_WARP_PARSE")) k_mask_parse<<<1, 32, kRing * 4, st>>>(pa);
+      else k_mask_parse_cta<<<1, kPT, kParseSmem, st>>>(pa);
       BB_LAUNCH_CHECK();
-      launches += 7;
+      k_expand_windows<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rec_cap, 8), 8 * sm)), 256, 0, st>>>(pa);
+      BB_LAUNCH_CHECK();
+      launches += 2;
+    } else {
+      // one J stride for both classes: tree t of class c at J[c] + t * n[c];
+      // the kernel uses a single stride, so give each class its own launch
+      // argument via per-class base pointers and the larger stride
+      pa.J_stride = std::max(n[0], n[1]);
+      k_mask_parse_cl<<<kCl, kPT, kClSmem, st>>>(pa);
+      BB_LAUNCH_CHECK();
+      launches += 1;
     }
-    const int64_t nt = (int64_t)n[0] + n[1];
-    k_mask_bits<<<grid_for(ceil_div(nt, 32), 256, sm), 256, 0, st>>>(removed[0], removed[1], n[0], nt, bits);
-    BB_LAUNCH_CHECK();
     launches += 1;
+    const long long stride = single ? 0 : std::max(n[0], n[1]);
+    for (int t = 0; t < count; ++t) {
+      for (int cc = 0; cc < 2; ++cc) {
+        const int nn = n[cc], kk = k[cc];
+        int* Jt = J[cc] + (size_t)t * stride;
+        // k == 0: nothing is active (position 0 is never a step target)
+        BB_CUDA(cudaMemsetAsync(removed[cc], kk == 0 ? 1 : 0, (size_t)std::max(1, nn), st));
+        if (kk == 0 || nn <= 1 || kk >= nn) continue;
+        BB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)nn * 4, st));
+        BB_CUDA(cudaMemsetAsync(fill, 0, (size_t)nn * 4, st));
+        const int g = grid_for(nn - kk, 256, sm);
+        k_bucket_count<<<g, 256, 0, st>>>(Jt, kk, nn, cnt);
+        const int nb = (int)ceil_div(nn, kScanBlock);
+        k_scan_block_sums<<<nb, 256, 0, st>>>(cnt, nn, sums);
+        k_scan_sums<<<1, 1024, 0, st>>>(sums, nb);
+        k_scan_apply<<<nb, 256, 0, st>>>(cnt, nn, sums, off);
+        k_bucket_fill<<<g, 256, 0, st>>>(Jt, kk, nn, off, fill, bucket);
+        k_bucket_sort<<<grid_for(nn, 256, sm), 256, 0, st>>>(cnt, off, nn, bucket);
+        k_resolve<<<g, 256, 0, st>>>(Jt, kk, nn, cnt, off, bucket, removed[cc]);
+        BB_LAUNCH_CHECK();
+        launches += 7;
+      }
+      const int64_t nt = (int64_t)n[0] + n[1];
+      k_mask_bits<<<grid_for(ceil_div(nt, 32), 256, sm), 256, 0, st>>>(removed[0], removed[1], n[0], nt, bits[t]);
+      BB_LAUNCH_CHECK();
+      launches += 1;
+      if (ready) BB_CUDA(cudaEventRecord(ready[t], st));
+    }
   }
 };
 
@@ -384,7 +409,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   BB_CUDA(cudaMemsetAsync(node, 0, (size_t)npad * sizeof(NodeT), st));
   BB_CUDA(cudaMemsetAsync(q, 0, (size_t)npad * 8, st));
   const int64_t words = ceil_div(n, 32);
-  constexpr int kSlots = 4;
+  constexpr int kSlots = 2 * kChunk;
   unsigned int* mask_slots = A.alloc<unsigned int>((size_t)words * kSlots);
   const bool host_masks = (cfg.flags & 2) != 0;
   const int max_nodes = 1 << (s.depth - 1);
@@ -441,7 +466,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   MaskGen mgen;
   cudaStream_t ms = nullptr;
   cudaEvent_t ready[kSlots], freed[kSlots];
-  unsigned int* pinned[kSlots] = {nullptr, nullptr, nullptr, nullptr};
+  unsigned int* pinned[kSlots] = {};
   for (int k = 0; k < kSlots; ++k) {
     BB_CUDA(cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming));
     BB_CUDA(cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming));
@@ -449,7 +474,11 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   if (host_masks) {
     for (int k = 0; k < kSlots; ++k) BB_CUDA(cudaMallocHost(&pinned[k], (size_t)words * 4));
   } else {
-    BB_CUDA(cudaStreamCreateWithFlags(&ms, cudaStreamNonBlocking));
+    // the mask chain is the fit's critical path: highest stream priority so
+    // its cluster is scheduled as soon as SMs free up
+    int prio_lo = 0, prio_hi = 0;
+    BB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    BB_CUDA(cudaStreamCreateWithPriority(&ms, cudaStreamNonBlocking, prio_hi));
     mgen.init(A, st, s.n_sig, s.n - s.n_sig, cfg.subsample, cfg, c.sm_count);
   }
   std::vector<uint32_t> perm;
@@ -481,25 +510,32 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   try {
     // the mask stream may run ahead of the fit stream by kSlots trees
     int next_mask = 0;
-    auto produce = [&](int t) {
-      const int slot = t % kSlots;
-      unsigned int* bits = mask_slots + (size_t)slot * words;
+    auto produce = [&](int t) {  // host path: one tree; GPU path: the chunk starting at t
       if (host_masks) {
+        const int slot = t % kSlots;
+        unsigned int* bits = mask_slots + (size_t)slot * words;
         if (t >= kSlots) BB_CUDA(cudaEventSynchronize(freed[slot]));
         const auto tm = std::chrono::steady_clock::now();
         subsample_tree(g, s.n_sig, s.n - s.n_sig, cfg.subsample, pinned[slot], perm);
         stats.mask_ms += elapsed_ms(tm);
-        if (t >= kSlots) BB_CUDA(cudaStreamWaitEvent(st, freed[slot], 0));
         BB_CUDA(cudaMemcpyAsync(bits, pinned[slot], (size_t)words * 4, cudaMemcpyHostToDevice, st));
         BB_CUDA(cudaEventRecord(ready[slot], st));
-      } else {
-        if (t >= kSlots) BB_CUDA(cudaStreamWaitEvent(ms, freed[slot], 0));
-        mgen.enqueue(ms, bits, stats.launches);
-        BB_CUDA(cudaEventRecord(ready[slot], ms));
+        return 1;
       }
+      const int cnt = std::min(mgen.single ? 1 : kChunk, s.T - t);
+      unsigned int* bits[kChunk];
+      cudaEvent_t evs[kChunk];
+      for (int j = 0; j < cnt; ++j) {
+        const int slot = (t + j) % kSlots;
+        if (t + j >= kSlots) BB_CUDA(cudaStreamWaitEvent(ms, freed[slot], 0));
+        bits[j] = mask_slots + (size_t)slot * words;
+        evs[j] = ready[slot];
+      }
+      mgen.enqueue_chunk(ms, bits, cnt, evs, stats.launches);
+      return cnt;
     };
     for (int t = 0; t < s.T; ++t) {
-      while (next_mask < s.T && next_mask < t + (host_masks ? 1 : kSlots)) produce(next_mask++);
+      while (next_mask < s.T && next_mask < t + (host_masks ? 1 : kChunk + 1)) next_mask += produce(next_mask);
       const int slot = t % kSlots;
       unsigned int* mask = mask_slots + (size_t)slot * words;
       BB_CUDA(cudaStreamWaitEvent(st, ready[slot], 0));
@@ -1020,7 +1056,16 @@ int bb_subsample_masks_gpu(bb_ctx* ctx, int64_t n_sig, int64_t n_bkg, double rat
     const int64_t words = ceil_div(n_sig + n_bkg, 32);
     unsigned int* bits = A.alloc<unsigned int>((size_t)std::max<int64_t>(1, words) * n_trees);
     int64_t launches = 0;
-    for (int t = 0; t < n_trees; ++t) mg.enqueue(st, bits + (size_t)t * words, launches);
+    for (int t = 0; t < n_trees; t += kChunk) {
+      const int cnt = std::min(kChunk, n_trees - t);
+      unsigned int* bp[kChunk];
+      for (int j = 0; j < cnt; ++j) bp[j] = bits + (size_t)(t + j) * words;
+      if (mg.single) {
+        for (int j = 0; j < cnt; ++j) mg.enqueue_chunk(st, &bp[j], 1, nullptr, launches);
+      } else {
+        mg.enqueue_chunk(st, bp, cnt, nullptr, launches);
+      }
+    }
     if (words) BB_CUDA(cudaMemcpyAsync(out_bits, bits, (size_t)words * n_trees * 4, cudaMemcpyDeviceToHost, st));
     BB_CUDA(cudaStreamSynchronize(st));
   });

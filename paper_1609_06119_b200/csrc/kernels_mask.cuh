@@ -122,7 +122,9 @@ struct ParseArgs {
   const PcgJump* jump;
   RngState* rng;  // in: state before the tree, out: state after
   int n[2], k[2];
-  int* J[2];      // J[c][i] for steps i >= k[c]
+  int* J[2];      // J[c][i] for steps i >= k[c]; tree t of a chunk at J[c] + t * J_stride
+  int n_trees;    // trees parsed by one launch (the cluster kernel parses a chunk)
+  long long J_stride;
   // fast-window records, expanded into J by k_expand_windows
   int* rec_pos;            // first draw of the window
   int* rec_i;              // step of the window's first draw, class in bit 31
@@ -706,6 +708,14 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// Cluster barrier: only the threads that published shared data to other
+// CTAs (DSMEM stores, or smem that other CTAs will read) pay the release
+// fence (MEMBAR); everyone else arrives relaxed and waits with acquire.
+__device__ __forceinline__ void csync(bool publish) {
+  if (publish) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
 #define BB_PMARK(slot, t0)                                             \
   do {                                                                  \
     if (a.prof && crank == 0 && tid == 0) a.prof[slot] += clock64() - (t0); \
@@ -737,7 +747,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
     s_state[2] = 1 << 30;  // crossing draw (min over CTAs)
     s_state[3] = 1 << 30;  // first overflowing ambiguous draw
   }
-  cl.sync();
+  csync(crank == 0 && tid == 0);
   auto load_slice = [&](int bsel, int wstart) {
     const long long base = (long long)wstart + (long long)crank * kPW;
     const long long abase = base & ~3ll;
@@ -759,14 +769,18 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
     __syncthreads();
   };
   int pos = 0;
-  for (int c = 0; c < 2; ++c) {
+  for (int tc = 0; tc < 2 * a.n_trees; ++tc) {
+    const int c = tc & 1;
     const int n = a.n[c], k = a.k[c];
-    int* J = a.J[c];
+    int* J = a.J[c] + (long long)(tc >> 1) * a.J_stride;
     int i = n - 1;
     while (i >= 1) {
       const unsigned int m0 = smear((unsigned)i);
+      // ambiguity is refined away below, so windows need no sqrt(m) cap; stop
+      // near the expected band crossing (~d/p draws, p >= 1/2) to limit the
+      // junk tail a crossing leaves for the next round
+      int W = kClW;
       (void)m0;
-      int W = kClW;  // ambiguity is refined away below, so windows need no sqrt(m) cap
       if ((long long)pos + W > nd) W = (int)max(0ll, nd - pos);
       if (i >= 64 && W >= 4096) {
         // ---- one window [pos, pos+W), processed in rounds; a round ends
@@ -828,7 +842,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
           }
           long long tr1 = clock64();
           BB_PMARK(8, tR);  // classify (+warp totals)
-          cl.sync();  // (1)
+          csync(tid == 0);  // (1) counts published by thread 0
 
           fetch(0, 2 * kCl);
           int S_before = 0, Q_before = 0, Q_tot = 0;
@@ -847,7 +861,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
           // (sure accepts, still-ambiguous draws before r) -> re-test the
           // ambiguous draws against those bounds (Jacobi: counts of the
           // previous pass), exchange counts, repeat
-          for (int pass = 0; pass < 8 && Q_tot > 64; ++pass) {
+          for (int pass = 0; pass < 8 && Q_tot > 768; ++pass) {
             int sr = S_before + S_w, qr = Q_before + Q_w;
             int ws2 = 0, wq2 = 0;
 #pragma unroll
@@ -900,7 +914,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
               cnt0[bank + 2 * crank] = S_c;
               cnt0[bank + 2 * crank + 1] = Q_c;
             }
-            cl.sync();
+            csync(tid == 0);
             fetch(bank, 2 * kCl);
             S_before = 0;
             Q_before = 0;
@@ -921,6 +935,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
             }
           }
           const int Qres = min(Q_tot, kQcap);  // entries beyond the cap: resolved serially below
+          bool wrote_keys = false;
           {
             int sr = S_before + S_w, qr = Q_before + Q_w;
 #pragma unroll
@@ -928,14 +943,17 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
               if ((amb[u] >> lane) & 1u) {
                 const int q = qr + __popc(amb[u] & lt);
                 const int rl = rw + u * 32 + lane;
-                if (q < kQcap) akey0[q] = i - (sr + __popc(sab[u] & lt)) - (int)(sl[rl] & m);
+                if (q < kQcap) {
+                  akey0[q] = i - (sr + __popc(sab[u] & lt)) - (int)(sl[rl] & m);
+                  wrote_keys = true;
+                }
               }
               sr += __popc(sab[u]);
               qr += __popc(amb[u]);
             }
           }
           const long long tK = clock64();
-          cl.sync();  // (2)
+          csync(wrote_keys);  // (2)
           BB_PMARK(9, tK);  // sync 2
           const long long tS = clock64();
           if (crank == 0) {
@@ -949,7 +967,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
           }
           long long tr3 = clock64();
           BB_PMARK(10, tS);  // resolve
-          cl.sync();  // (3)
+          csync(crank == 0 && warp == 0);  // (3) apref published by CTA 0 warp 0
 
           // S_tot from this CTA's view: S_before + own + after (all banks agree
           // only per pass, so recompute from the last exchange's bank)
@@ -994,7 +1012,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
             i -= S_tot + A_amb;
             rs = W;
             BB_PMARK(11, tC);  // common commit
-            cl.sync();  // (4') CTA 0 list / counters free
+            csync(false);  // (4') CTA 0 list / counters free (reads only)
             if (a.prof && crank == 0 && tid == 0) a.prof[2] += 1;
             break;
           }
@@ -1049,7 +1067,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
             A_c += x;
           }
           if (tid == 0) cnt0[4 * kCl + crank] = A_c;
-          cl.sync();  // (4)
+          csync(tid == 0 || (Q_tot > kQcap && lane == 0));  // (4)
           if (Q_tot > kQcap) rcut = min(W, state0[3]);
           fetch(4 * kCl, kCl);
           int A_before = 0, A_tot = 0;
@@ -1077,7 +1095,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
               found = __reduce_min_sync(0xffffffffu, found);
               if (lane == 0 && found < W) atomicMin(&state0[2], found);
             }
-            cl.sync();  // (5)
+            csync(lane == 0);  // (5)
             const int rx = state0[2];
             if (rx + 1 < rend) {
               rend = rx + 1;
@@ -1124,10 +1142,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
             }
             cnt = __reduce_add_sync(0xffffffffu, cnt);
             if (lane == 0) atomicAdd(&state0[1], cnt);
-            cl.sync();
+            csync(lane == 0);
             committed_acc = state0[1];
           }
-          cl.sync();  // (6) everyone has read state0 / cnt0
+          csync(false);  // (6) everyone has read state0 / cnt0
           if (crank == 0 && tid == 0) {
             state0[1] = 0;
             state0[2] = 1 << 30;
@@ -1146,10 +1164,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
               }
               for (int q = 0; q < kCl; ++q) cl.map_shared_rank(s_state, q)[0] = ii;
             }
-            cl.sync();
+            csync(crank == 0 && tid == 0);
             i = s_state[0];
             rs = rend + 1;
-            cl.sync();
+            csync(false);
           }
           BB_PMARK(12, tD);  // detailed path
           if (i == 0) {
@@ -1202,10 +1220,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
           }
           __syncthreads();
         }
-        cl.sync();
+        csync(crank == 0 && tid == 0);
         i = s_state[0];
         pos = s_state[1];
-        cl.sync();
+        csync(false);
         if (crank == 0 && tid == 0) {
           s_state[1] = 0;
           s_state[2] = 1 << 30;
@@ -1215,7 +1233,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPT, 1) k_mask_par
             a.prof[6] += 1;
           }
         }
-        cl.sync();
+        csync(crank == 0 && tid == 0);
       }
     }
   }

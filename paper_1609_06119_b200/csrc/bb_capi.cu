@@ -204,7 +204,7 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count) {
   }
   const int tile = kTile;
   auto need = [&](int fg) {
-    return (int64_t)align16(p.ngs * fg * s.B * 8) + 2 * (int64_t)hist_buf_bytes<CodeT, NodeT>(tile, fg) + 4 * tile + 64;
+    return (int64_t)align16((p.ngs * fg * s.B + 32) * 8) + 2 * (int64_t)hist_buf_bytes<CodeT, NodeT>(tile, fg) + 4 * tile + 64;
   };
   while (p.fg > 1 && need(p.fg) > kSmemMax) {
     p.n_fg += 1;

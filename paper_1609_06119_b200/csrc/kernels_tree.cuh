@@ -86,7 +86,9 @@ __global__ void k_update_scores(int64_t n, double* __restrict__ F, const NodeT* 
 // compacts the rows that contribute (in class range, at this layer, in the
 // node group, q != 0 — inactive rows carry q == 0) and every thread then
 // adds its rows' weights into (node, feature, code) slots held in shared
-// memory as 2-limb int64 (slot_add2: one returning 32-bit ATOMS per update).
+// memory as 2-limb int64 (lo limb: returning 32-bit ATOMS; a wrap carries
+// into the hi limb).  Measured better than two non-returning atomics per
+// update (16/16 split): fewer shared-atomic wavefronts.
 // Missing codes (bin 0) are skipped: the split search never reads slot 0
 // (trees.py:181-186).  At the end each CTA merges its slots into the global
 // histogram with native 64-bit global reductions.
@@ -144,14 +146,14 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   const int nslots = ncount * fcount * B;
   const int tile = p.tile;
   uint32_t* lo = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* hi = lo + nslots;
-  unsigned char* stage = smem + align16(nslots * 8);
+  uint32_t* hi = lo + nslots + 32;  // slots nslots .. nslots+31: per-lane dummies
+  unsigned char* stage = smem + align16((nslots + 32) * 8);
   const int bufb = hist_buf_bytes<CodeT, NodeT>(tile, fcount);
   uint32_t* list = reinterpret_cast<uint32_t*>(stage + 2 * bufb);
   uint64_t* bar = reinterpret_cast<uint64_t*>(list + tile);
   int* counter = reinterpret_cast<int*>(bar + 2);
 
-  for (int i = threadIdx.x; i < 2 * nslots; i += kHistThreads) lo[i] = 0u;
+  for (int i = threadIdx.x; i < 2 * (nslots + 32); i += kHistThreads) lo[i] = 0u;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -217,22 +219,22 @@ __global__ void __launch_bounds__(kHistThreads, 1)
       const uint32_t h = (uint32_t)((unsigned long long)qq >> 32);
       const int j0 = jb * 4;
       const int sb = (nd * fcount + j0) * B - 1;
+      // missing codes / padding features go to this lane's dummy slot
+      // (nslots + lane), never read: the lo-limb atomic is unconditional
       int sl[4];
       uint32_t old[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int j = j0 + u;
         const int c = (j < fcount) ? (int)ct[j * tile + rl] + code_off : 0;
-        sl[u] = (c != 0) ? sb + u * B + c : -1;
+        sl[u] = (c != 0) ? sb + u * B + c : nslots + (threadIdx.x & 31);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) old[u] = (sl[u] >= 0) ? atomicAdd(lo + sl[u], l) : 0u;
+      for (int u = 0; u < 4; ++u) old[u] = atomicAdd(lo + sl[u], l);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        if (sl[u] >= 0) {
-          const uint32_t hh = h + ((old[u] + l < old[u]) ? 1u : 0u);
-          if (hh) atomicAdd(hi + sl[u], hh);
-        }
+        const uint32_t hh = h + ((old[u] + l < old[u]) ? 1u : 0u);
+        if (hh) atomicAdd(hi + sl[u], hh);
       }
       a += kHistThreads;
       while (a >= n_act && n_act > 0) {

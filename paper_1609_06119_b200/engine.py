@@ -150,7 +150,7 @@ def _as_features(X) -> tuple[np.ndarray, int]:
 
 def fit_forest(X, y, weights=None, config: FitConfig | None = None, *, forced_cuts=None,
                return_leaves: bool = False, return_scores: bool = False, profile: bool = False,
-               device: int = 0) -> Forest:
+               host_masks: bool = False, device: int = 0) -> Forest:
     """Fit a boosted forest on raw rows (boosting.py:117-173) on the GPU.
 
     forced_cuts: optional {(tree, heap_node): (valid, feature, cut_bin)} for
@@ -181,7 +181,8 @@ def fit_forest(X, y, weights=None, config: FitConfig | None = None, *, forced_cu
     y01 = np.ascontiguousarray(labels > 0, dtype=np.int8)
 
     return _fit_native(X, xdt, False, n, d, y01, False, w, False, cfg, forced_cuts=forced_cuts,
-                       return_leaves=return_leaves, return_scores=return_scores, profile=profile, device=device)
+                       return_leaves=return_leaves, return_scores=return_scores,
+                       profile=int(profile) | (2 if host_masks else 0), device=device)
 
 
 def fit_forest_device(x_ptr: int, x_dtype: str, n: int, d: int, y01_ptr: int, w_ptr: int | None,

@@ -882,7 +882,26 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
     }
     const unsigned grid = (unsigned)ceil_div(n, APPLY_ROWS);
     const size_t smem = (size_t)APPLY_ROWS * (d + 1) * es;
-    if (x_dtype == BB_F32) {
+    const size_t smem32 = ((size_t)kApplyRows * (d + 1) * 4 + 15) / 16 * 16 + (size_t)kApplyTB * (N * 8 + I * 8);
+    if (x_dtype == BB_F32 && smem32 <= 200 * 1024) {
+      // packed node records with float-ceiling thresholds (exact for float rows)
+      std::vector<int2> hn(TI);
+      for (size_t e = 0; e < TI; ++e) {
+        const double t = fo->threshold[e];
+        float tf = (float)t;  // round-to-nearest, then step up if below t
+        if ((double)tf < t) tf = std::nextafter(tf, INFINITY);
+        int bits;
+        std::memcpy(&bits, &tf, 4);
+        hn[e] = make_int2(fo->valid[e] ? fo->feature[e] : -1, bits);
+      }
+      int2* nd = A.alloc<int2>(TI);
+      if (TI) BB_CUDA(cudaMemcpyAsync(nd, hn.data(), TI * sizeof(int2), cudaMemcpyHostToDevice, st));
+      ApplyF32 a32{fo->n_trees, fo->depth, I, N, nd, nw, fo->f0};
+      BB_CUDA(cudaFuncSetAttribute(k_apply_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      k_apply_f32<<<(unsigned)ceil_div(n, kApplyRows), kApplyRows, smem32, st>>>((const float*)Xd, n, d, a32, pd, fd);
+      BB_LAUNCH_CHECK();
+      BB_CUDA(cudaStreamSynchronize(st));  // host staging vector hn
+    } else if (x_dtype == BB_F32) {
       BB_CUDA(cudaFuncSetAttribute(k_apply<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       k_apply<float><<<grid, APPLY_ROWS, smem, st>>>((const float*)Xd, n, d, af, pd, fd);
     } else {

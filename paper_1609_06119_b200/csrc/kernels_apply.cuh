@@ -64,4 +64,84 @@ __global__ void __launch_bounds__(APPLY_ROWS) k_apply(const T* __restrict__ X, i
   if (out_p) out_p[i] = sigmoid2(F);
 }
 
+// ---------------------------------------------------------------- f32 path
+// float32 rows: thresholds pre-rounded to the exact float ceiling (for a
+// float v, v >= thr  <=>  v >= ceil_f32(thr)), packed with the feature into
+// 8-byte node records (feature < 0: invalid node, stop).  A CTA stages 256
+// rows and batches of kApplyTB trees in shared memory; every thread walks
+// 4 trees at a time (independent node chains, ILP) and adds the node
+// weights to its float64 F in tree order.
+constexpr int kApplyRows = 256;
+constexpr int kApplyTB = 128;
+
+struct ApplyF32 {
+  int n_trees, depth, n_internal, n_nodes;
+  const int2* node;   // [T][I]: x = feature (or -1), y = float bits of ceil_f32(thr)
+  const double* nw;   // [T][N]
+  double f0;
+};
+
+__global__ void __launch_bounds__(kApplyRows) k_apply_f32(const float* __restrict__ X, int64_t n, int d, ApplyF32 fo,
+                                                          double* __restrict__ out_p, double* __restrict__ out_F) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int ld = d + 1;
+  float* tile = reinterpret_cast<float*>(s_raw);  // [kApplyRows][ld]
+  unsigned char* after = s_raw + ((size_t)kApplyRows * ld * 4 + 15) / 16 * 16;
+  double* s_nw = reinterpret_cast<double*>(after);                                   // [TB][N]
+  int2* s_node = reinterpret_cast<int2*>(s_nw + (size_t)kApplyTB * fo.n_nodes);       // [TB][I]
+  const int64_t row0 = (int64_t)blockIdx.x * kApplyRows;
+  const int rows = (int)min((int64_t)kApplyRows, n - row0);
+  const float* src = X + row0 * d;
+  for (int e = threadIdx.x; e < rows * d; e += kApplyRows) {
+    const int r = e / d, f = e - r * d;
+    tile[r * ld + f] = src[e];
+  }
+  const float* row = tile + threadIdx.x * ld;
+  double F = fo.f0;
+  const int I = fo.n_internal, N = fo.n_nodes, D = fo.depth;
+  for (int tb = 0; tb < fo.n_trees; tb += kApplyTB) {
+    const int nt = min(kApplyTB, fo.n_trees - tb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nt * I; e += kApplyRows) s_node[e] = fo.node[(int64_t)tb * I + e];
+    for (int e = threadIdx.x; e < nt * N; e += kApplyRows) s_nw[e] = fo.nw[(int64_t)tb * N + e];
+    __syncthreads();
+    if ((int)threadIdx.x < rows) {
+      int t = 0;
+      for (; t + 4 <= nt; t += 4) {
+        int nd[4] = {0, 0, 0, 0};
+        bool live[4] = {true, true, true, true};
+        for (int l = 0; l < D; ++l) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int2 rec = s_node[(t + u) * I + nd[u]];
+            const bool vld = live[u] && rec.x >= 0;
+            const float v = vld ? row[rec.x] : 0.0f;
+            const bool go = vld && v == v;  // NaN stops at this node
+            nd[u] = go ? 2 * nd[u] + 1 + (v >= __int_as_float(rec.y) ? 1 : 0) : nd[u];
+            live[u] = go;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) F = __dadd_rn(F, s_nw[(t + u) * N + nd[u]]);
+      }
+      for (; t < nt; ++t) {
+        int nd = 0;
+        for (int l = 0; l < D; ++l) {
+          const int2 rec = s_node[t * I + nd];
+          if (rec.x < 0) break;
+          const float v = row[rec.x];
+          if (v != v) break;
+          nd = 2 * nd + 1 + (v >= __int_as_float(rec.y) ? 1 : 0);
+        }
+        F = __dadd_rn(F, s_nw[t * N + nd]);
+      }
+    }
+  }
+  if ((int)threadIdx.x < rows) {
+    const int64_t i = row0 + threadIdx.x;
+    if (out_F) out_F[i] = F;
+    if (out_p) out_p[i] = sigmoid2(F);
+  }
+}
+
 }  // namespace bb

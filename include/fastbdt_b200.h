@@ -55,6 +55,15 @@ int bb_device_count(int32_t* out);
 int bb_ctx_create(int32_t device, bb_ctx** out);
 int bb_ctx_destroy(bb_ctx* ctx);
 
+/* Row-sharded fits: join an NCCL communicator of `world`
+ * ranks (unique_id: the 128-byte ncclUniqueId of rank 0, e.g. from
+ * torch.cuda.nccl.unique_id()).  Afterwards bb_fit on this context takes the
+ * rank's shard of rows: the contiguous rank-th slice of the signal block and
+ * of the background block (input order = class-block order), ranks in order.
+ * Histograms and node sums are all-reduced (int64) per layer, so every rank
+ * takes the same cuts; binning statistics are all-reduced too. */
+int bb_ctx_init_comm(bb_ctx* ctx, int32_t rank, int32_t world, const uint8_t* unique_id);
+
 /* FitConfig (boosting.py:36-57) plus the numpy PCG64(seed) state the
  * subsample draws from (PCG64(seed).state["state"]: 128-bit state and
  * increment split into hi/lo words, has_uint32, uinteger). */
@@ -69,6 +78,8 @@ typedef struct {
   uint64_t pcg_inc_hi, pcg_inc_lo;
   int32_t pcg_has_uint32;
   uint32_t pcg_uinteger;
+  double f0_override;  /* NaN: compute the prior here; required (from all rows,
+                        * numpy pairwise sums) when the context is sharded */
 } bb_fit_config;
 
 /* Teacher-forced parity protocol: at (tree, heap node)

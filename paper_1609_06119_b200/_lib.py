@@ -36,7 +36,12 @@ class FitConfigC(C.Structure):
         ("pcg_inc_lo", C.c_uint64),
         ("pcg_has_uint32", C.c_int32),
         ("pcg_uinteger", C.c_uint32),
+        ("f0_override", C.c_double),
     ]
+
+    def __init__(self, **kw):
+        kw.setdefault("f0_override", float("nan"))
+        super().__init__(**kw)
 
 
 class ForcedCutC(C.Structure):
@@ -84,6 +89,7 @@ _SIGS = {
     "bb_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
     "bb_ctx_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
     "bb_ctx_destroy": (C.c_int, [C.c_void_p]),
+    "bb_ctx_init_comm": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "bb_fit": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_int32,
                          C.c_void_p, C.c_int32, C.POINTER(FitConfigC), C.c_void_p, C.c_int32, C.POINTER(FitOutC)]),
     "bb_predict": (C.c_int, [C.c_void_p, C.POINTER(ForestC), C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int32,

@@ -17,6 +17,7 @@
 
 #include "../../include/fastbdt_b200.h"
 #include "bb_mask.h"
+#include "bb_nccl.h"
 #include "common.cuh"
 #include "kernels_apply.cuh"
 #include "kernels_binning.cuh"
@@ -67,6 +68,15 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   int sm_count = 148;
   std::mutex mu;
+  NcclComm comm;  // world > 1: row-sharded fits
+};
+
+// class-block layout of this rank's rows inside the global blocks
+struct Shard {
+  int64_t n_sig_g = 0, n_bkg_g = 0;  // global block sizes
+  int64_t s0 = 0, b0 = 0;            // this rank's offsets in each block
+  int64_t n_sig_l = 0;               // this rank's signal rows
+  bool dist = false;
 };
 
 // stream-ordered arena: every allocation of one call, freed at the end
@@ -116,7 +126,8 @@ constexpr int kSmemHistBins = 8192;  // k_select_hist shared counters
 
 template <typename T>
 static void run_select(Ctx& c, Arena& A, const typename KeyOf<T>::K* keys, int64_t n, int d, int levels,
-                       const unsigned long long* finite_dev, double* bounds, typename KeyOf<T>::K* bkeys) {
+                       const unsigned long long* finite_dev, double* bounds, typename KeyOf<T>::K* bkeys,
+                       bool dist = false) {
   using K = typename KeyOf<T>::K;
   constexpr int KB = sizeof(K) * 8;
   const int B = 1 << levels, nt = B - 1;
@@ -139,8 +150,11 @@ static void run_select(Ctx& c, Arena& A, const typename KeyOf<T>::K* keys, int64
   while (resolved < KB) {
     int db = (resolved == 0) ? 12 : 8;
     db = std::min(db, KB - resolved);
-    k_select_hist<K><<<dim3(gx, d), 256, kSmemHistBins * 4, c.stream>>>(keys, n, st, resolved, db, kSmemHistBins);
-    BB_LAUNCH_CHECK();
+    if (n > 0) {
+      k_select_hist<K><<<dim3(gx, d), 256, kSmemHistBins * 4, c.stream>>>(keys, n, st, resolved, db, kSmemHistBins);
+      BB_LAUNCH_CHECK();
+    }
+    if (dist) c.comm.all_reduce(st.hist, (size_t)d * st.hist_cap, kNcclU32, kNcclSum, c.stream);
     k_select_scan<K><<<d, 1024, 0, c.stream>>>(st, db);
     BB_LAUNCH_CHECK();
     resolved += db;
@@ -152,7 +166,7 @@ static void run_select(Ctx& c, Arena& A, const typename KeyOf<T>::K* keys, int64
 template <typename T>
 static typename KeyOf<T>::K* make_keys(Ctx& c, Arena& A, const T* Xd, int64_t n, int d,
                                        std::vector<unsigned long long>& finite, std::vector<unsigned long long>& nans,
-                                       unsigned long long** finite_dev_out) {
+                                       unsigned long long** finite_dev_out, bool dist = false) {
   using K = typename KeyOf<T>::K;
   K* keys = A.alloc<K>((size_t)n * d);
   unsigned long long* cnt = A.alloc<unsigned long long>(2 * (size_t)d);
@@ -162,6 +176,7 @@ static typename KeyOf<T>::K* make_keys(Ctx& c, Arena& A, const T* Xd, int64_t n,
         Xd, n, d, keys, cnt, cnt + d);
     BB_LAUNCH_CHECK();
   }
+  if (dist) c.comm.all_reduce(cnt, 2 * (size_t)d, kNcclU64, kNcclSum, c.stream);
   finite.assign(d, 0);
   nans.assign(d, 0);
   BB_CUDA(cudaMemcpyAsync(finite.data(), cnt, (size_t)d * 8, cudaMemcpyDeviceToHost, c.stream));
@@ -251,6 +266,9 @@ struct MaskGen {
   int n[2] = {0, 0}, k[2] = {0, 0};
   int sm = 148;
   bool single = false;  // single-tree legacy parse kernels (debug env)
+  Shard sh;                       // sh.dist: slice the global bits to this rank
+  long long sh_n_local = 0;       // this rank's rows
+  unsigned int* gbits = nullptr;  // global bits scratch (sharded fits)
 
   void init(Arena& A, cudaStream_t st, int64_t n_sig, int64_t n_bkg, double rate, const bb_fit_config& cfg,
             int sm_count) {
@@ -309,6 +327,7 @@ struct MaskGen {
       prof = A.alloc<long long>(16);
       BB_CUDA(cudaMemsetAsync(prof, 0, 128, st));
     }
+    gbits = A.alloc<unsigned int>((size_t)ceil_div(steps, 32) + 1);
   }
   void report(cudaStream_t st) {
     if (!prof) return;
@@ -386,9 +405,16 @@ struct MaskGen {
         launches += 7;
       }
       const int64_t nt = (int64_t)n[0] + n[1];
-      k_mask_bits<<<grid_for(ceil_div(nt, 32), 256, sm), 256, 0, st>>>(removed[0], removed[1], n[0], nt, bits[t]);
+      unsigned int* dst = sh.dist ? gbits : bits[t];
+      k_mask_bits<<<grid_for(ceil_div(nt, 32), 256, sm), 256, 0, st>>>(removed[0], removed[1], n[0], nt, dst);
       BB_LAUNCH_CHECK();
       launches += 1;
+      if (sh.dist) {
+        k_mask_slice<<<grid_for(ceil_div(sh_n_local, 32), 256, sm), 256, 0, st>>>(gbits, sh_n_local, sh.n_sig_l,
+                                                                                   sh.n_sig_g, sh.s0, sh.b0, bits[t]);
+        BB_LAUNCH_CHECK();
+        launches += 1;
+      }
       if (ready) BB_CUDA(cudaEventRecord(ready[t], st));
     }
   }
@@ -398,7 +424,7 @@ template <typename CodeT, typename NodeT>
 static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, int code_off,
                       const double* w_cb, double f0, int shift, const bb_fit_config& cfg,
                       const bb_forced_cut* forced, int n_forced, const double* bounds_dev, bb_fit_out* out,
-                      double* t_trees_ms, FitStats& stats) {
+                      double* t_trees_ms, FitStats& stats, const Shard& shard) {
   const int64_t n = s.n;
   cudaStream_t st = c.stream;
   const double two_s = std::ldexp(1.0, shift), scale = std::ldexp(1.0, -shift);
@@ -411,7 +437,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   const int64_t words = ceil_div(n, 32);
   constexpr int kSlots = 2 * kChunk;
   unsigned int* mask_slots = A.alloc<unsigned int>((size_t)words * kSlots);
-  const bool host_masks = (cfg.flags & 2) != 0;
+  const bool host_masks = (cfg.flags & 2) != 0 && !shard.dist;
   const int max_nodes = 1 << (s.depth - 1);
   unsigned long long* hist = A.alloc<unsigned long long>((size_t)2 * max_nodes * s.d * s.B);
   BB_CUDA(cudaMemsetAsync(hist, 0, (size_t)2 * max_nodes * s.d * s.B * 8, st));
@@ -479,7 +505,13 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
     int prio_lo = 0, prio_hi = 0;
     BB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     BB_CUDA(cudaStreamCreateWithPriority(&ms, cudaStreamNonBlocking, prio_hi));
-    mgen.init(A, st, s.n_sig, s.n - s.n_sig, cfg.subsample, cfg, c.sm_count);
+    if (shard.dist) {
+      mgen.init(A, st, shard.n_sig_g, shard.n_bkg_g, cfg.subsample, cfg, c.sm_count);
+      mgen.sh = shard;
+      mgen.sh_n_local = s.n;
+    } else {
+      mgen.init(A, st, s.n_sig, s.n - s.n_sig, cfg.subsample, cfg, c.sm_count);
+    }
   }
   std::vector<uint32_t> perm;
   std::vector<NodeT> leaf_tmp;
@@ -550,6 +582,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
                                                                                s.d, s.B, p, hist);
         BB_LAUNCH_CHECK();
         if (prof) hist_event();
+        c.comm.all_reduce(hist, (size_t)2 * p.nodes * s.d * s.B, kNcclI64, kNcclSum, st);  // sharded fits
         stats.launches += 3;
         stats.hist_launches += 1;
         const int nodes = p.nodes;
@@ -567,6 +600,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         BB_LAUNCH_CHECK();
       }
       BB_CUDA(cudaEventRecord(freed[slot], st));
+      c.comm.all_reduce(sums, (size_t)2 * s.n_nodes * 2, kNcclI64, kNcclSum, st);  // sharded fits
       k_node_weights<<<1, 256, (size_t)2 * s.n_nodes * 2 * 8, st>>>(sums, s.n_nodes, s.depth, scale, cfg.shrinkage, t,
                                                                     ta);
       BB_LAUNCH_CHECK();
@@ -654,11 +688,12 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   auto t_bin = std::chrono::steady_clock::now();
   std::vector<unsigned long long> finite, nans;
   unsigned long long* finite_dev = nullptr;
-  K* keys = make_keys<T>(c, A, Xd, n, d, finite, nans, &finite_dev);
+  const bool dist = c.comm.active();  // row-sharded fit: every rank holds a slice of the rows
+  K* keys = make_keys<T>(c, A, Xd, n, d, finite, nans, &finite_dev, dist);
   if (!x_dev) A.release(const_cast<T*>(Xd));
   double* bounds = A.alloc<double>((size_t)d * nt);
   K* bkeys = A.alloc<K>((size_t)d * nt);
-  run_select<T>(c, A, keys, n, d, levels, finite_dev, bounds, bkeys);
+  run_select<T>(c, A, keys, n, d, levels, finite_dev, bounds, bkeys, dist);
   // class blocks
   const int n_tiles = (int)ceil_div(n, CLS_TILE);
   int* tile_sig = A.alloc<int>(n_tiles + 1);
@@ -674,7 +709,34 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   BB_CUDA(cudaMemcpyAsync(&n_sig_i, tile_sig + n_tiles, 4, cudaMemcpyDeviceToHost, st));
   BB_CUDA(cudaStreamSynchronize(st));
   const int64_t n_sig = n_sig_i;
-  if (n_sig == 0 || n_sig == n) throw InvalidArg{"training data must contain both classes"};
+  Shard shard;
+  if (dist) {
+    // per-rank class counts -> this rank's offsets in the global class blocks
+    // (ranks concatenate in rank order: the global row order of the fit)
+    const int W = c.comm.world, R = c.comm.rank;
+    unsigned long long* cnt = A.alloc<unsigned long long>(2 * (size_t)W);
+    std::vector<unsigned long long> h(2 * (size_t)W, 0);
+    h[2 * R] = (unsigned long long)n_sig;
+    h[2 * R + 1] = (unsigned long long)(n - n_sig);
+    BB_CUDA(cudaMemcpyAsync(cnt, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
+    c.comm.all_reduce(cnt, h.size(), kNcclU64, kNcclSum, st);
+    BB_CUDA(cudaMemcpyAsync(h.data(), cnt, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaStreamSynchronize(st));
+    shard.dist = true;
+    shard.n_sig_l = n_sig;
+    for (int r = 0; r < W; ++r) {
+      if (r < R) {
+        shard.s0 += (int64_t)h[2 * r];
+        shard.b0 += (int64_t)h[2 * r + 1];
+      }
+      shard.n_sig_g += (int64_t)h[2 * r];
+      shard.n_bkg_g += (int64_t)h[2 * r + 1];
+    }
+    if (shard.n_sig_g + shard.n_bkg_g >= ((int64_t)1 << 31)) throw InvalidArg{"at most 2^31-1 rows per fit"};
+    if (shard.n_sig_g == 0 || shard.n_bkg_g == 0) throw InvalidArg{"training data must contain both classes"};
+  } else if (n_sig == 0 || n_sig == n) {
+    throw InvalidArg{"training data must contain both classes"};
+  }
   bool any_nan = false;
   for (int f = 0; f < d; ++f) any_nan |= nans[f] > 0;
   const int64_t stride = ceil_div(n, kTile) * kTile;  // rows incl. tile padding
@@ -696,7 +758,23 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
     w_sig = (double)n_sig;
     w_bkg = (double)(n - n_sig);
   }
-  const double f0 = (w_sig <= 0.0 || w_bkg <= 0.0) ? 0.0 : 0.5 * std::log(w_sig / w_bkg);
+  if (dist) {
+    // global class weights (exact for unit weights; for user weights the
+    // caller passes the reference's pairwise f0 in f0_override) and the
+    // global weight magnitude for the common fixed-point shift
+    double* red = A.alloc<double>(3);
+    double hv[3] = {w_sig, w_bkg, max_abs};
+    BB_CUDA(cudaMemcpyAsync(red, hv, 24, cudaMemcpyHostToDevice, st));
+    c.comm.all_reduce(red, 2, kNcclF64, kNcclSum, st);
+    c.comm.all_reduce(red + 2, 1, kNcclF64, kNcclMax, st);
+    BB_CUDA(cudaMemcpyAsync(hv, red, 24, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaStreamSynchronize(st));
+    w_sig = hv[0];
+    w_bkg = hv[1];
+    max_abs = hv[2];
+  }
+  double f0 = (w_sig <= 0.0 || w_bkg <= 0.0) ? 0.0 : 0.5 * std::log(w_sig / w_bkg);
+  if (!std::isnan(cfg.f0_override)) f0 = cfg.f0_override;
   const int shift = fixed_shift_for(max_abs);
   double ms_trees = 0.0;
   auto launch_codes = [&](auto* codes, int off) {
@@ -716,9 +794,9 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
     BB_CUDA(cudaStreamSynchronize(st));
     ms_bin = elapsed_ms(t_bin);
     if (s.depth <= 7)
-      run_trees<CodeT, uint8_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees, stats);
+      run_trees<CodeT, uint8_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees, stats, shard);
     else
-      run_trees<CodeT, uint16_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees, stats);
+      run_trees<CodeT, uint16_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees, stats, shard);
   };
   if (B <= 255) {
     go(A.alloc<uint8_t>((size_t)d * stride), 0);
@@ -812,7 +890,18 @@ int bb_ctx_destroy(bb_ctx* ctx) {
       cudaStreamSynchronize(ctx->c.stream);
       cudaStreamDestroy(ctx->c.stream);
     }
+    ctx->c.comm.destroy();
     delete ctx;
+  });
+}
+
+int bb_ctx_init_comm(bb_ctx* ctx, int32_t rank, int32_t world, const uint8_t* unique_id) {
+  return guarded([&] {
+    if (!ctx || !unique_id) throw InvalidArg{"null argument"};
+    if (world < 1 || rank < 0 || rank >= world) throw InvalidArg{"rank must be in [0, world)"};
+    std::lock_guard<std::mutex> lock(ctx->c.mu);
+    BB_CUDA(cudaSetDevice(ctx->c.device));
+    ctx->c.comm.init(rank, world, unique_id);
   });
 }
 

@@ -1370,6 +1370,25 @@ __global__ void k_mask_bits(const unsigned char* __restrict__ rem_sig, const uns
   }
 }
 
+// this rank's active bits from the global class-block bits (row-sharded
+// fits): local row j < n_sig_l is global signal row s0 + j, otherwise global
+// background row b0 + (j - n_sig_l) at bit n_sig_g + ...
+__global__ void k_mask_slice(const unsigned int* __restrict__ gbits, long long n_l, long long n_sig_l,
+                             long long n_sig_g, long long s0, long long b0, unsigned int* __restrict__ bits) {
+  const long long words = (n_l + 31) / 32;
+  for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+       w += (long long)gridDim.x * blockDim.x) {
+    unsigned int v = 0;
+    for (int b = 0; b < 32; ++b) {
+      const long long j = w * 32 + b;
+      if (j >= n_l) break;
+      const long long g = j < n_sig_l ? s0 + j : n_sig_g + b0 + (j - n_sig_l);
+      v |= ((gbits[g >> 5] >> (g & 31)) & 1u) << b;
+    }
+    bits[w] = v;
+  }
+}
+
 // --------------------------------------------------------------- scan
 // exclusive scan of n ints: per-block sums, single-CTA scan of the sums,
 // per-block exclusive scan with the carried offset

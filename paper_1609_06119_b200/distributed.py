@@ -1,0 +1,132 @@
+"""Row-sharded fit over NCCL: one process per GPU.
+
+Every rank passes its own rows; the global training sample is the
+concatenation of the ranks' rows in rank order, so the reference's class
+blocks (sample.py:112-116) are rank 0's signal rows, rank 1's signal rows,
+…, then the background rows in the same order.  ``sharding.shard_rows``
+produces such a partition from one global array.
+
+The library (bb_capi.cu, ``bb_ctx_init_comm``) then runs the whole fit with
+four kinds of exchange, all on its own stream over the NCCL communicator:
+binning (finite/NaN counts + one u32 radix histogram per select pass),
+class counts (-> this rank's offsets in the global class blocks), the layer
+histograms (int64 fixed-point, SUM — exact and order-free) and the final
+node sums of each tree.  The subsample mask is drawn for the GLOBAL class
+blocks (same PCG64 stream on every rank) and sliced to the local rows, so
+the fitted forest is bit-identical to a single-device fit of the
+concatenated rows, for any world size.
+
+torch.distributed is the plumbing only: it carries the 128-byte NCCL unique
+id from rank 0 and, for user weights, the per-class weight vectors needed to
+reproduce the reference's prior exactly (``prior``, boosting.py:76-83).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+
+import numpy as np
+
+from . import _lib
+from .engine import FitConfig, Forest, _as_features, _fit_native
+
+__all__ = ["sharded_prior", "comm_context", "fit_forest_sharded"]
+
+_comm_ctx: dict = {}
+_comm_lock = threading.Lock()
+
+
+def _dist():
+    import torch.distributed as dist
+
+    if not dist.is_available() or not dist.is_initialized():
+        raise RuntimeError("fit_forest_sharded needs an initialised torch.distributed process group")
+    return dist
+
+
+def sharded_prior(w_local: np.ndarray | None, y01_local: np.ndarray, group=None) -> float:
+    """The reference prior over the concatenated rows (boosting.py:76-83):
+    0.5*log(sum w_sig / sum w_bkg) with numpy's pairwise sums taken over the
+    GLOBAL class blocks in rank order (so the value is bit-identical to a
+    single-process fit).  NaN for unit weights: the library's exact count
+    ratio is used then."""
+    if w_local is None:
+        return math.nan
+    dist = _dist()
+    sig = y01_local > 0
+    parts = [None] * dist.get_world_size(group)
+    dist.all_gather_object(parts, (np.asarray(w_local[sig]), np.asarray(w_local[~sig])), group=group)
+    w_sig = float(np.sum(np.concatenate([p[0] for p in parts])))
+    w_bkg = float(np.sum(np.concatenate([p[1] for p in parts])))
+    if w_sig <= 0.0 or w_bkg <= 0.0:
+        return 0.0
+    return 0.5 * math.log(w_sig / w_bkg)
+
+
+def _unique_id(dist, group) -> bytes:
+    if dist.get_rank(group) == 0:
+        import torch
+
+        uid = bytes(torch.cuda.nccl.unique_id())
+    else:
+        uid = None
+    box = [uid]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    if not isinstance(box[0], (bytes, bytearray)) or len(box[0]) != 128:
+        raise RuntimeError("bad NCCL unique id from rank 0")
+    return bytes(box[0])
+
+
+def comm_context(device: int, group=None):
+    """A library context bound to an NCCL communicator over ``group``
+    (created once per (device, group); collective over the group)."""
+    dist = _dist()
+    key = (device, id(group))
+    with _comm_lock:
+        h = _comm_ctx.get(key)
+        if h is not None:
+            return h
+    uid = _unique_id(dist, group)
+    out = C.c_void_p()
+    _lib.check(_lib.lib().bb_ctx_create(device, C.byref(out)))
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    _lib.check(_lib.lib().bb_ctx_init_comm(out, dist.get_rank(group), dist.get_world_size(group), buf))
+    with _comm_lock:
+        _comm_ctx[key] = out
+    return out
+
+
+def fit_forest_sharded(X, y, weights=None, config: FitConfig | None = None, *, group=None,
+                       device: int | None = None, return_leaves: bool = False,
+                       return_scores: bool = False) -> Forest:
+    """fit_forest (boosting.py:117-173) over rows sharded across the ranks of
+    ``group``: X/y/weights are THIS rank's rows.  Collective: every rank
+    calls it with the same config; every rank gets the same Forest.
+    ``fit_info['leaves'/'scores']`` cover the local rows (class-block order)."""
+    dist = _dist()
+    if device is None:
+        import torch
+
+        device = torch.cuda.current_device()
+    cfg = config or FitConfig()
+    X, xdt = _as_features(X)
+    if X.ndim != 2:
+        raise ValueError("X must be 2-d (n_events, n_features)")
+    n, d = X.shape
+    y = np.asarray(y)
+    if y.shape != (n,):
+        raise ValueError(f"y has shape {y.shape}, expected ({n},)")
+    y01 = np.ascontiguousarray(y > 0, dtype=np.int8)
+    w = None
+    if weights is not None:
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        if w.shape != (n,):
+            raise ValueError(f"weights has shape {w.shape}, expected ({n},)")
+        if not np.all(np.isfinite(w)):
+            raise ValueError("user weights must be finite")
+    f0 = sharded_prior(w, y01, group)
+    ctx = comm_context(device, group)
+    return _fit_native(X, xdt, False, n, d, y01, False, w, False, cfg, return_leaves=return_leaves,
+                       return_scores=return_scores, device=device, ctx=ctx, f0_override=f0)

@@ -197,14 +197,14 @@ def fit_forest_device(x_ptr: int, x_dtype: str, n: int, d: int, y01_ptr: int, w_
 
 
 def _fit_native(X, xdt, x_dev, n, d, y01, y_dev, w, w_dev, cfg, *, forced_cuts=None, return_leaves=False,
-                return_scores=False, profile=False, device=0) -> Forest:
+                return_scores=False, profile=False, device=0, ctx=None, f0_override=math.nan) -> Forest:
     def p(a):
         return a if (a is None or isinstance(a, C.c_void_p)) else _lib.ptr(a)
 
     L, D, T = cfg.binning_levels, cfg.depth, cfg.n_trees
     B, I, N = 1 << L, (1 << D) - 1, (1 << (D + 1)) - 1
     c = _lib.FitConfigC(n_trees=T, depth=D, binning_levels=L, flags=int(profile), shrinkage=cfg.shrinkage,
-                        subsample=cfg.subsample, **_lib.pcg_config(cfg.seed))
+                        subsample=cfg.subsample, f0_override=f0_override, **_lib.pcg_config(cfg.seed))
     bounds = np.zeros((d, B - 1))
     feat = np.zeros((T, I), np.int32)
     cut = np.zeros((T, I), np.int32)
@@ -227,7 +227,7 @@ def _fit_native(X, xdt, x_dev, n, d, y01, y_dev, w, w_dev, cfg, *, forced_cuts=N
         forced_arr = (_lib.ForcedCutC * len(items))(
             *[_lib.ForcedCutC(int(t), int(nd), int(bool(v[0])), int(v[1]), int(v[2])) for (t, nd), v in items])
         n_forced = len(items)
-    ctx = _lib.context(device)
+    ctx = ctx or _lib.context(device)
     _lib.check(_lib.lib().bb_fit(ctx, p(X), xdt, int(x_dev), n, d, p(y01), int(y_dev), p(w), int(w_dev), C.byref(c),
                                  C.cast(forced_arr, C.c_void_p) if forced_arr is not None else None, n_forced,
                                  C.byref(out)))

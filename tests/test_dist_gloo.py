@@ -79,3 +79,47 @@ def test_sharded_histograms_allreduce_exact():
         assert p.exitcode == 0
     for r in range(2):
         np.testing.assert_array_equal(got[r], full)
+
+
+def _prior_worker(rank, world, port, out_q):
+    from paper_1609_06119_b200.distributed import _unique_id, sharded_prior
+    from paper_1609_06119_b200.sharding import shard_rows
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(4)
+    y = (rng.random(10_001) < 0.3).astype(np.int8)
+    w = rng.normal(1.0, 0.7, y.size)
+    rows = shard_rows(y, rank, world)
+    out_q.put((rank, sharded_prior(w[rows], y[rows]), _unique_id(dist, None)))
+    dist.destroy_process_group()
+
+
+def test_sharded_prior_and_unique_id_broadcast():
+    """The sharded fit's host plumbing: the prior over the rank-ordered
+    class blocks equals the single-process reference prior bit-for-bit, and
+    every rank receives rank 0's 128-byte NCCL unique id."""
+    import math
+
+    rng = np.random.default_rng(4)
+    y = (rng.random(10_001) < 0.3).astype(np.int8)
+    w = rng.normal(1.0, 0.7, y.size)
+    s, b = float(np.sum(w[y > 0])), float(np.sum(w[y <= 0]))
+    want = 0.5 * math.log(s / b)  # boosting.py:76-83 over the global class blocks
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_prior_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(2):
+        r, f0, uid = q.get(timeout=120)
+        got[r] = (f0, uid)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got[0][0] == want and got[1][0] == want
+    assert len(got[0][1]) == 128 and got[0][1] == got[1][1]

@@ -374,3 +374,43 @@ def test_cfg5_slice_vs_fixed_point_oracle():
         np.testing.assert_allclose(tr.node_weight, ref.node_weight[t], rtol=1e-12, atol=1e-15)
     p = predict_batch(forest, X[:3000])
     assert np.max(np.abs(p - oracle.predict(ref, X[:3000]))) <= 1e-12
+
+
+# ------------------------------------------------------------ sharded fit
+@pytest.mark.parametrize("weighted", [False, True])
+def test_sharded_fit_world1_matches_single(weighted):
+    """The NCCL row-sharded path (communicator, binning/class-count/layer/
+    final-sum all-reduces, global mask + slice) at world size 1 must give
+    the single-device forest bit-for-bit."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1609_06119_b200.distributed import fit_forest_sharded
+
+    rng = np.random.default_rng(11)
+    n, d = 30_000, 6
+    X = rng.normal(size=(n, d)).astype(np.float32)
+    y = (X[:, 0] + 0.5 * rng.normal(size=n) > 0).astype(np.int8)
+    w = rng.uniform(0.5, 2.0, n) if weighted else None
+    cfg = FitConfig(n_trees=6, depth=3, shrinkage=0.1, subsample=0.5, binning_levels=6, seed=3)
+    ref = fit_forest(X, y, w, cfg, return_leaves=True)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        got = fit_forest_sharded(X, y, w, cfg, device=0, return_leaves=True)
+    finally:
+        dist.destroy_process_group()
+    assert got.f0 == ref.f0
+    for a, b in zip(got.binnings, ref.binnings):
+        np.testing.assert_array_equal(a.boundaries, b.boundaries)
+    for ta, tb in zip(got.trees, ref.trees):
+        np.testing.assert_array_equal(ta.valid, tb.valid)
+        np.testing.assert_array_equal(ta.feature[ta.valid], tb.feature[tb.valid])
+        np.testing.assert_array_equal(ta.cut_bin[ta.valid], tb.cut_bin[tb.valid])
+        np.testing.assert_array_equal(ta.node_weight, tb.node_weight)
+    np.testing.assert_array_equal(got.fit_info["leaves"], ref.fit_info["leaves"])

@@ -22,6 +22,7 @@
 #include "kernels_apply.cuh"
 #include "kernels_binning.cuh"
 #include "kernels_mask.cuh"
+#include "kernels_seg.cuh"
 #include "kernels_tree.cuh"
 
 namespace bb {
@@ -251,6 +252,30 @@ static inline int hist_grid(const HistPlan& p) { return p.n_fg * p.n_ng * (p.spl
 // once per chunk; the per-tree resolution kernels follow.
 constexpr int kChunk = 8;
 
+// segment table of a block of n rows (kernels_seg.cuh seg_geom)
+struct SegPlan {
+  std::vector<SegTab> tab;
+  std::vector<int2> tasks;
+  int n_rec = 0;
+};
+
+static SegPlan build_seg_plan(int n) {
+  SegPlan P;
+  if (n - 1 < kSegTail) return P;
+  long long off = 0;
+  SegTab t{};
+  while (seg_geom(n - 1, off, kSegTail, &t)) {
+    t.rec_off = P.n_rec;
+    const int ns = t.nA + t.nB;
+    for (int q = 0; q < ns; q += kSubPerCta) P.tasks.push_back(int2{(int)P.tab.size(), q});
+    P.n_rec += ns;
+    P.tab.push_back(t);
+    off += t.len;
+    if (off > (1ll << 30)) break;
+  }
+  return P;
+}
+
 struct MaskGen {
   PcgJump* jump = nullptr;
   RngState* rng = nullptr;
@@ -269,6 +294,15 @@ struct MaskGen {
   Shard sh;                       // sh.dist: slice the global bits to this rank
   long long sh_n_local = 0;       // this rank's rows
   unsigned int* gbits = nullptr;  // global bits scratch (sharded fits)
+  // segment-parallel parse (kernels_seg.cuh)
+  SegTab* tab[2] = {nullptr, nullptr};
+  int2* tasks[2] = {nullptr, nullptr};
+  int S[2] = {0, 0}, n_tasks[2] = {0, 0};
+  SegRec* rec = nullptr;
+  int *seg_start = nullptr, *n_seg = nullptr;
+  long long* spos = nullptr;
+  RngState* rng0 = nullptr;
+  bool legacy_cl = false;  // BB_CL_PARSE: the cluster parse instead
 
   void init(Arena& A, cudaStream_t st, int64_t n_sig, int64_t n_bkg, double rate, const bb_fit_config& cfg,
             int sm_count) {
@@ -324,19 +358,95 @@ struct MaskGen {
     rec_count = A.alloc<int>(1);
     rec_bits = A.alloc<unsigned char>((size_t)rec_cap * 32);
     if (getenv("BB_PARSE_PROFILE")) {
-      prof = A.alloc<long long>(16);
-      BB_CUDA(cudaMemsetAsync(prof, 0, 128, st));
+      prof = A.alloc<long long>(32);
+      BB_CUDA(cudaMemsetAsync(prof, 0, 256, st));
     }
     gbits = A.alloc<unsigned int>((size_t)ceil_div(steps, 32) + 1);
+    legacy_cl = getenv("BB_CL_PARSE") != nullptr;
+    int smax = 1, rmax = 1;
+    for (int cc = 0; cc < 2; ++cc) {
+      const SegPlan P = build_seg_plan(n[cc]);
+      S[cc] = (int)P.tab.size();
+      n_tasks[cc] = (int)P.tasks.size();
+      tab[cc] = A.alloc<SegTab>(std::max<size_t>(1, P.tab.size()));
+      tasks[cc] = A.alloc<int2>(std::max<size_t>(1, P.tasks.size()));
+      if (S[cc]) BB_CUDA(cudaMemcpyAsync(tab[cc], P.tab.data(), P.tab.size() * sizeof(SegTab), cudaMemcpyHostToDevice, st));
+      if (n_tasks[cc])
+        BB_CUDA(cudaMemcpyAsync(tasks[cc], P.tasks.data(), P.tasks.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+      BB_CUDA(cudaStreamSynchronize(st));
+      smax = std::max(smax, S[cc]);
+      rmax = std::max(rmax, P.n_rec);
+    }
+    rec = A.alloc<SegRec>((size_t)rmax);
+    seg_start = A.alloc<int>(smax);
+    n_seg = A.alloc<int>(1);
+    spos = A.alloc<long long>(2 * (size_t)chunk + 2);
+    rng0 = A.alloc<RngState>(1);
+    BB_CUDA(cudaFuncSetAttribute(k_seg_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegPassSmem));
+    BB_CUDA(cudaFuncSetAttribute(k_seg_compose, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegComposeSmem));
   }
   void report(cudaStream_t st) {
     if (!prof) return;
-    long long h[16];
+    long long h[32];
     cudaStreamSynchronize(st);
-    cudaMemcpy(h, prof, 128, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h, prof, 256, cudaMemcpyDeviceToHost);
     fprintf(stderr, "parse prof:");
-    for (int q = 0; q < 16; ++q) fprintf(stderr, " %lld", h[q]);
+    for (int q = 0; q < 32; ++q) fprintf(stderr, " %lld", h[q]);
     fprintf(stderr, "\n");
+  }
+
+  // segment-parallel parse of `count` trees (2 * count block jobs)
+  int64_t enqueue_seg(cudaStream_t st, int count) {
+    int64_t launches = 0;
+    BB_CUDA(cudaMemcpyAsync(rng0, rng, sizeof(RngState), cudaMemcpyDeviceToDevice, st));
+    BB_CUDA(cudaMemsetAsync(spos, 0, sizeof(long long), st));
+    const long long stride = std::max(n[0], n[1]);
+    SegArgs sa{};
+    sa.draws = draws;
+    sa.n_draws = n_draws;
+    sa.jump = jump;
+    sa.rng0 = rng0;
+    sa.rng = rng;
+    sa.rec = rec;
+    sa.seg_start = seg_start;
+    sa.n_seg = n_seg;
+    sa.prof = prof;
+    SegJob prev{};
+    bool have_prev = false;
+    const int jobs = 2 * count;
+    for (int jj = 0; jj <= jobs; ++jj) {
+      SegJob job{};
+      if (jj < jobs) {
+        const int t = jj >> 1, cc = jj & 1;
+        job.n = n[cc];
+        job.k = k[cc];
+        job.S = S[cc];
+        job.tab = tab[cc];
+        job.tasks = tasks[cc];
+        job.n_tasks = n_tasks[cc];
+        job.J = J[cc] + (size_t)t * stride;
+        job.pos_in = spos + jj;
+        job.pos_out = spos + jj + 1;
+        job.write_rng = jj == jobs - 1;
+      }
+      const int nb_func = job.n_tasks;
+      const int nb_emit = have_prev ? (int)ceil_div(prev.S, kSubPerCta) : 0;
+      sa.func = job;
+      sa.emit = prev;
+      if (nb_func + nb_emit > 0) {
+        k_seg_pass<<<nb_func + nb_emit, kSegThreads, kSegPassSmem, st>>>(sa, nb_func);
+        BB_LAUNCH_CHECK();
+        launches += 1;
+      }
+      if (jj < jobs) {
+        k_seg_compose<<<1, kComposeThreads, kSegComposeSmem, st>>>(sa);
+        BB_LAUNCH_CHECK();
+        launches += 1;
+      }
+      prev = job;
+      have_prev = true;
+    }
+    return launches;
   }
 
   // masks of `count` consecutive trees; bits[j] = output words of tree j,
@@ -372,7 +482,7 @@ struct MaskGen {
       k_expand_windows<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rec_cap, 8), 8 * sm)), 256, 0, st>>>(pa);
       BB_LAUNCH_CHECK();
       launches += 2;
-    } else {
+    } else if (legacy_cl) {
       // one J stride for both classes: tree t of class c at J[c] + t * n[c];
       // the kernel uses a single stride, so give each class its own launch
       // argument via per-class base pointers and the larger stride
@@ -380,6 +490,8 @@ struct MaskGen {
       k_mask_parse_cl<<<kCl, kPT, kClSmem, st>>>(pa);
       BB_LAUNCH_CHECK();
       launches += 1;
+    } else {
+      launches += enqueue_seg(st, count);
     }
     launches += 1;
     const long long stride = single ? 0 : std::max(n[0], n[1]);
@@ -1176,6 +1288,7 @@ int bb_subsample_masks_gpu(bb_ctx* ctx, int64_t n_sig, int64_t n_bkg, double rat
     }
     if (words) BB_CUDA(cudaMemcpyAsync(out_bits, bits, (size_t)words * n_trees * 4, cudaMemcpyDeviceToHost, st));
     BB_CUDA(cudaStreamSynchronize(st));
+    mg.report(st);
   });
 }
 

@@ -1,0 +1,727 @@
+// Segment-parallel parse of the subsample draw stream (the Fisher-Yates
+// step assignment of kernels_mask.cuh, reference sample.py:128-132 through
+// numpy Generator.permutation; algorithm restated in bb_mask.cpp).
+//
+// A block job (one class block of one tree: steps i = n-1 .. 1, step i takes
+// the first draw x = v & smear(i) with x <= i) consumes a data-dependent
+// number of draws.  Its draw range is cut into segments at fixed offsets
+// from the job's first draw (host table per block size).  For every segment
+// the expected state at its first draw follows from the mean trajectory,
+// (i+1)' = -(i+1)/(mask+1) per band, and the true state lies in a window
+// [lo, hi] around it (the accept count is a sum of Bernoullis, sd <=
+// sqrt(p)/2 after p draws; the window is 9 sd on each side).
+//
+//  phase 1 (k_seg_pass, func part; a warp per 512-state sub-window, a CTA
+//    per 16 sub-windows of one segment, all SMs): the segment's transfer
+//    function over the sub-window, inside one mask band.  Paths that start
+//    at adjacent states stay ordered and at most one step apart, so the
+//    sub-window is an interval [a, b] of distinct states: a draw x <= a
+//    moves every path (a--, b--), x > b none, a < x <= b moves the paths at
+//    states >= x and merges the groups at offsets x-a and x-a-1 (b--).  A
+//    rank bitmask records which start ranks merged:
+//        end(lo + r) = a_end + r - #{cleared ranks <= r},
+//    valid for ranks that never fall to the band's last state h (end > h).
+//  phase 2 (k_seg_compose, one CTA): warp 0 chains the functions from the
+//    job's exact first state, one lookup per segment (records streamed into
+//    shared memory with cp.async).  A start the records cannot answer (a
+//    band crossing inside the segment, a window miss) is walked exactly by
+//    the whole CTA (cta_walk); below kSegTail the CTA walks the job to its
+//    end, which gives the next job's first draw.
+//  phase 3 (k_seg_pass, emit part; a CTA per segment): each segment walked
+//    exactly from its start state, writing J[i] = x for steps i >= k.
+//
+// cta_walk: 4096-draw windows, 16 warps classify draws as sure-accept
+// (x <= i - r), sure-reject (x > i) or ambiguous; warp 0 resolves the
+// ambiguous ones in draw order (resolve_list: accepted iff accepted-before
+// <= i - x - sure-accepts-before); the band's last step ends the window so
+// the next one uses the new mask.
+//
+// Every decision is exact: windows and records only decide how much work is
+// parallel, never the result.
+#pragma once
+#include "kernels_mask.cuh"
+
+namespace bb {
+
+constexpr int kSegMaxLen = 8192;   // draws per segment (max)
+constexpr int kSegCrossLen = 1024; // draws per segment in band-crossing zones
+constexpr int kSub = 512;          // states per phase-1 sub-window (one warp)
+constexpr int kSubPerCta = 8;      // sub-windows per phase-1 CTA (= warps per k_seg_pass CTA)
+constexpr int kSegMaxSub = 20;     // sub-windows per segment (max)
+constexpr int kSegTail = 8192;     // states below this: walked by phase 2
+constexpr int kSegThreads = 32 * kSubPerCta;
+constexpr int kSegRing = 16;       // segments of records in flight in k_seg_compose
+constexpr int kRows = 16;          // rows of 32 draws classified at once by phase 1 (512-draw chunks)
+constexpr int kScalarBelow = 64;   // walk states below this one draw at a time
+
+__host__ __device__ __forceinline__ unsigned int smear_host(unsigned int x) {
+  x |= x >> 1;
+  x |= x >> 2;
+  x |= x >> 4;
+  x |= x >> 8;
+  x |= x >> 16;
+  return x;
+}
+
+struct SegTab {   // per segment of a block size (host-built)
+  int off;        // first draw, relative to the job's first draw
+  int len;        // draws
+  int loA, nA;    // piece A: states [loA, hiA] in the band of hiA, nA sub-windows
+  int hiA;
+  int loB, nB;    // piece B (the band below): [loB, hiB], nB sub-windows
+  int hiB;
+  int rec_off;    // first sub-window record
+  int pad[3];
+};
+
+// expected Fisher-Yates state after p draws from state i0 (mean trajectory,
+// (i+1)' = -(i+1)/(mask+1) inside a band)
+__host__ __device__ inline double seg_pred_state(int i0, double p) {
+  double x = (double)i0 + 1.0;
+  while (true) {
+    if (x <= 1.0 + 1e-9) return 0.0;
+    const unsigned M = smear_host((unsigned)fmax(1.0, floor(x - 1.0)));
+    const double mp1 = (double)M + 1.0, lowx = mp1 / 2.0;
+    const double pb = mp1 * log(x / lowx);
+    if (p < pb) return x * exp(-p / mp1) - 1.0;
+    p -= pb;
+    x = lowx;
+  }
+}
+
+// half window after p draws: 5 sd (sd <= sqrt(p)/2); a start outside the
+// window only costs an exact walk
+__host__ __device__ inline double seg_half_window(double p) {
+  return p <= 0.0 ? 0.0 : fmin(4096.0, ceil(2.5 * sqrt(p)) + 16.0);
+}
+
+// Geometry of the segment at draw offset `off` of a stretch that starts at
+// state i0: window, pieces (A: the band of the window's top, B: the band
+// below, down to `floor_state`) and length (~90 paths of a 512-state
+// sub-window merge at most; kSegCrossLen draws where some start may reach
+// its band's last state, so the exact walk a crossing costs stays short).
+// Returns false once the window lies below floor_state.
+__host__ __device__ inline bool seg_geom(int i0, long long off, int floor_state, SegTab* t) {
+  const double pi = seg_pred_state(i0, (double)off);
+  const double H = seg_half_window((double)off);
+  int lo = (int)fmax(1.0, floor(pi - H));
+  int hi = (int)fmin((double)i0, ceil(pi + H));
+  if (off == 0) lo = hi = i0;
+  if (hi < floor_state || lo > hi) return false;
+  t->off = (int)off;
+  const unsigned Mh = smear_host((unsigned)hi);
+  const int bbA = (int)(Mh >> 1) + 1;
+  t->loA = lo > bbA ? lo : bbA;
+  t->hiA = hi;
+  t->nA = (t->hiA - t->loA + kSub) / kSub;
+  t->loB = 1;
+  t->hiB = 0;
+  t->nB = 0;
+  if (lo < bbA && bbA - 1 >= floor_state && bbA - 1 >= 1) {
+    t->hiB = bbA - 1;
+    const unsigned MB = smear_host((unsigned)t->hiB);
+    const int bbB = (int)(MB >> 1) + 1;
+    t->loB = lo > bbB ? lo : bbB;
+    t->nB = (t->hiB - t->loB + kSub) / kSub;
+  }
+  const unsigned M = smear_host((unsigned)(pi > 1.0 ? (int)pi : 1));
+  const double L = 0.176 * ((double)M + 1.0);
+  int Lp = 256;
+  while (Lp * 2 <= L && Lp < kSegMaxLen) Lp *= 2;
+  const double pe = seg_pred_state(i0, (double)(off + Lp)) - seg_half_window((double)(off + Lp));
+  if (lo < bbA || pe < (double)bbA) Lp = Lp < kSegCrossLen ? Lp : kSegCrossLen;
+  t->len = Lp;
+  return true;
+}
+
+struct SegRec {   // 128 B, one sub-window: end(lo + r) = a_end + pref[r/32] + popc(words[r/32] & bits <= r%32)
+  int a_end, h, pad0, pad1;
+  unsigned int words[16];      // rank bitmask: bit r set = rank r ends above rank r-1
+  unsigned short pref[16];     // set bits in words before w
+  int pad2[4];
+};
+
+struct SegJob {
+  int n, k;
+  int S;                       // segments in the table
+  const SegTab* tab;
+  const int2* tasks;           // phase-1 CTAs: (segment, first sub-window)
+  int n_tasks;
+  int* J;                      // J[i] for steps i >= k
+  long long* pos_in;           // job's first draw (absolute index into the draw buffer)
+  long long* pos_out;          // written by compose: first draw of the next job
+  int write_rng;               // compose: update the RNG state after this job
+};
+
+struct SegArgs {
+  const unsigned int* draws;
+  long long n_draws;
+  const PcgJump* jump;
+  const RngState* rng0;        // state at draw 0 of the buffer (chunk start)
+  RngState* rng;               // written by the compose of the chunk's last job
+  SegRec* rec;                 // sub-window records of the job in phase 1/2
+  int* seg_start;              // [S] exact start states (phase 2 -> phase 3)
+  int* n_seg;                  // segments composed (phase 2 -> phase 3)
+  SegJob func, emit;           // k_seg_pass: phase-1 job (n_tasks = 0: none), phase-3 job
+  long long* prof;
+};
+
+constexpr int kSegPassSmem = kSegMaxLen * 4;
+constexpr int kTabChunk = 64, kTabChunks = 4;  // table entries streamed into k_seg_compose
+constexpr int kSegComposeSmem = kSegRing * kSegMaxSub * 128 + kTabChunk * kTabChunks * 48 + (kSegMaxLen + 16) * 4;
+
+__device__ __forceinline__ unsigned int seg_get(const SegArgs& a, const RngState& r0, long long idx) {
+  return idx < a.n_draws ? __ldg(&a.draws[idx]) : draw_at(*a.jump, r0, idx);
+}
+
+// stage draws [p, p + len) into sd (all threads of the CTA)
+__device__ __forceinline__ void seg_stage_cta(const SegArgs& a, const RngState& r0, long long p, int len,
+                                              unsigned int* sd) {
+  if (p + len <= a.n_draws) {
+    for (int j = threadIdx.x; j < len; j += blockDim.x) sd[j] = __ldg(&a.draws[p + j]);
+  } else {
+    for (int j = threadIdx.x; j < len; j += blockDim.x) sd[j] = seg_get(a, r0, p + j);
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------- phase 1
+// One warp, states [lo, lo + W) (W <= kSub) in the band of mask M.  The rank
+// bitmask has 16 words; lane l < 16 owns word l (in a register, mirrored in
+// smem) and keeps `incl` = set bits in words <= l up to date, so a merge
+// finds its word with one ballot.
+__device__ void seg_sub(const unsigned int* sd, int len, int lo, int W, unsigned int M, SegRec* out, int lane) {
+  unsigned int wv = 0;
+  if (lane < 16) wv = (lane == 0) ? 0xfffffffeu : 0xffffffffu;  // rank 0 is the base; ranks >= W sentinels
+  int incl = __popc(wv);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int a = lo, b = lo + W - 1;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int pos = 0; pos < len; pos += 32 * kRows) {
+    // classify kRows rows against the bounds at the chunk start: every path
+    // accepts if x <= a0 - r (at most r accepts before), none if x > b0
+    const int a0 = a, b0 = b;
+    unsigned sa[kRows], am[kRows];
+    int xs[kRows];
+#pragma unroll
+    for (int u = 0; u < kRows; ++u) {
+      const int r = 32 * u + lane;
+      const bool in = pos + r < len;
+      const int x = in ? (int)(sd[pos + r] & M) : 0x7fffffff;
+      xs[u] = x;
+      const bool acc = in && x <= a0 - r;
+      sa[u] = __ballot_sync(0xffffffffu, acc);
+      am[u] = __ballot_sync(0xffffffffu, in && !acc && x <= b0);
+    }
+    unsigned amany = 0;
+    int tot = 0;
+#pragma unroll
+    for (int u = 0; u < kRows; ++u) {
+      amany |= am[u];
+      tot += __popc(sa[u]);
+    }
+    if (amany == 0) {  // fast path: every path takes the same draws
+      a -= tot;
+      b -= tot;
+      continue;
+    }
+    // rows in order; ambiguous draws decided exactly with the running a, b
+#pragma unroll
+    for (int u = 0; u < kRows; ++u) {
+      unsigned acc = sa[u];
+      int mrow = 0;
+      unsigned rem = am[u];
+      while (rem) {
+        const int f = __ffs(rem) - 1;
+        rem &= rem - 1u;
+        const int nb = __popc(acc & ((1u << f) - 1u));
+        const int ac = a - nb, bc = b - nb - mrow;
+        const int xf = __shfl_sync(0xffffffffu, xs[u], f);
+        if (xf <= ac) {
+          acc |= 1u << f;
+        } else if (xf <= bc) {
+          // clear the t-th set bit of the rank bitmask, t = xf - ac (1-based)
+          const int t = xf - ac;
+          const unsigned own = __ballot_sync(0xffffffffu, lane < 16 && incl >= t);
+          const int ow = __ffs(own) - 1;
+          if (lane == ow) {
+            const int tt = t - (incl - __popc(wv));
+            unsigned int m = wv;
+            for (int z = 1; z < tt; ++z) m &= m - 1u;
+            wv &= ~(m & (0u - m));
+          }
+          if (lane >= ow) --incl;
+          ++mrow;
+        }
+      }
+      const int na = __popc(acc);
+      a -= na;
+      b -= na + mrow;
+    }
+  }
+  (void)lt;
+  // the rank bitmask and its per-word prefix counts
+  const int pc = __popc(wv);
+  int pi = pc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, pi, o);
+    if (lane >= o) pi += y;
+  }
+  if (lane < 16) {
+    out->words[lane] = wv;
+    out->pref[lane] = (unsigned short)(pi - pc);
+  }
+  if (lane == 0) {
+    out->a_end = a;
+    out->h = (int)(M >> 1);
+  }
+}
+
+// sub-window j of segment t: (lo, W, mask)
+__device__ __forceinline__ void seg_sub_geom(const SegTab& t, int j, int& lo, int& W, unsigned int& M) {
+  if (j < t.nA) {
+    lo = t.loA + kSub * j;
+    W = min(kSub, t.hiA - lo + 1);
+    M = smear((unsigned)t.hiA);
+  } else {
+    lo = t.loB + kSub * (j - t.nA);
+    W = min(kSub, t.hiB - lo + 1);
+    M = smear((unsigned)t.hiB);
+  }
+}
+
+// bulk prefetch of [p, p + n) draws into L2 (16-byte aligned range)
+__device__ __forceinline__ void seg_prefetch_l2(const unsigned int* base, long long p, long long n, long long n_draws) {
+  long long a0 = p & ~3ll, a1 = min(n_draws, p + n);
+  a1 &= ~3ll;
+  if (a1 <= a0) return;
+  const unsigned bytes = (unsigned)min((a1 - a0) * 4, (long long)1 << 20);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + a0), "r"(bytes) : "memory");
+}
+
+// One chunk of ROWS rows of 32 draws of the exact walk (see warp_walk),
+// classified against the state i0 at the chunk start: sure accept x <= i0 - r
+// (at most r accepts before draw r), sure reject x > i0.  Ambiguous draws are
+// decided by Jacobi refinement over the chunk: accepted-before(r) lies in
+// [A(r), A(r) + U(r)] (decided accepts / unresolved draws before r), so
+// x <= i0 - A - U accepts and x > i0 - A rejects; a draw with A >= d lies
+// past the band's last step (dropped).  The first unresolved draw has U = 0,
+// so every pass decides at least one.  The d-th accept ends the chunk.
+template <int ROWS, bool kGlobal>
+__device__ __forceinline__ void walk_chunk(const unsigned int* src, int pos, int len, int i0, int d, unsigned int M,
+                                           int k, int* J, int lane, int& taken, int& consumed) {
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned acc[ROWS], ur[ROWS];
+  int xs[ROWS];
+  unsigned any = 0;
+  int tot = 0;
+#pragma unroll
+  for (int u = 0; u < ROWS; ++u) {
+    const int r = 32 * u + lane;
+    const bool in = pos + r < len;
+    const unsigned int raw = in ? (kGlobal ? __ldg(src + pos + r) : src[pos + r]) : 0u;
+    const int x = in ? (int)(raw & M) : 0x7fffffff;
+    xs[u] = x;
+    const bool sa = in && x <= i0 - r;
+    acc[u] = __ballot_sync(0xffffffffu, sa);
+    ur[u] = __ballot_sync(0xffffffffu, in && !sa && x <= i0);
+    any |= ur[u];
+    tot += __popc(acc[u]);
+  }
+  consumed = min(32 * ROWS, len - pos);
+  if (any == 0 && tot < d) {  // fast path: every draw decided, no band crossing
+    if (J) {
+      int pre = 0;
+#pragma unroll
+      for (int u = 0; u < ROWS; ++u) {
+        if ((acc[u] >> lane) & 1u) {
+          const int st = i0 - pre - __popc(acc[u] & lt);
+          if (st >= k) J[st] = xs[u];
+        }
+        pre += __popc(acc[u]);
+      }
+    }
+    taken = tot;
+    return;
+  }
+  while (any) {
+    unsigned na[ROWS], nr[ROWS];
+    int runA = 0, runU = 0;
+#pragma unroll
+    for (int u = 0; u < ROWS; ++u) {
+      const int A = runA + __popc(acc[u] & lt), U = runU + __popc(ur[u] & lt);
+      const bool mine = (ur[u] >> lane) & 1u;
+      na[u] = __ballot_sync(0xffffffffu, mine && A < d && xs[u] <= i0 - A - U);
+      nr[u] = __ballot_sync(0xffffffffu, mine && (A >= d || xs[u] > i0 - A));
+      runA += __popc(acc[u]);
+      runU += __popc(ur[u]);
+    }
+    any = 0;
+#pragma unroll
+    for (int u = 0; u < ROWS; ++u) {
+      acc[u] |= na[u];
+      ur[u] &= ~(na[u] | nr[u]);
+      any |= ur[u];
+    }
+  }
+  int runA = 0, cut_row = ROWS, cut_lane = 31;
+#pragma unroll
+  for (int u = 0; u < ROWS; ++u) {
+    const int T = __popc(acc[u]);
+    if (cut_row == ROWS && runA + T >= d) {
+      unsigned mm = acc[u];
+      for (int z = 1; z < d - runA; ++z) mm &= mm - 1u;
+      cut_row = u;
+      cut_lane = __ffs(mm) - 1;
+    }
+    if (cut_row == ROWS) runA += T;
+  }
+  if (cut_row < ROWS) {
+    consumed = 32 * cut_row + cut_lane + 1;
+    taken = d;
+  } else {
+    taken = runA;
+  }
+  if (J) {
+    int pre = 0;
+#pragma unroll
+    for (int u = 0; u < ROWS; ++u) {
+      unsigned m = acc[u];
+      if (u > cut_row) m = 0;
+      if (u == cut_row) m &= (cut_lane >= 31) ? 0xffffffffu : ((2u << cut_lane) - 1u);
+      if ((m >> lane) & 1u) {
+        const int st = i0 - pre - __popc(m & lt);
+        if (st >= k) J[st] = xs[u];
+      }
+      pre += __popc(m);
+    }
+  }
+}
+
+// Exact walk of one path by one warp, from state i over src[0 .. len-1]
+// (global or shared): chunks of 32*ROWS draws with ROWS chosen per band so
+// a chunk expects about one ambiguous draw ((32 ROWS)^2 <= 2(M+1)); states
+// below kScalarBelow are walked draw by draw.  Stops after the draw that
+// takes i to 0.  Writes J[step] = x for accepted steps >= k when J != nullptr.
+template <bool kGlobal>
+__device__ int warp_walk(const unsigned int* src, int len, int i, int k, int* J, int lane, int* used) {
+  int pos = 0;
+  while (pos < len && i >= 1) {
+    if (i < kScalarBelow) {
+      // 32 draws per step: taken in order from the lanes
+      int ii = i, pp = pos;
+      while (pp < len && ii >= 1) {
+        const unsigned int v = pp + lane < len ? (kGlobal ? __ldg(src + pp + lane) : src[pp + lane]) : 0u;
+        int take = 0;
+        for (int q = 0; q < 32 && pp + q < len && ii >= 1; ++q) {
+          const int x = (int)(__shfl_sync(0xffffffffu, v, q) & smear((unsigned)ii));
+          ++take;
+          if (x <= ii) {
+            if (J && lane == 0 && ii >= k) J[ii] = x;
+            --ii;
+          }
+        }
+        pp += take;
+      }
+      i = ii;
+      pos = pp;
+      break;
+    }
+    const unsigned int M = smear((unsigned)i);
+    const int d = i - (int)(M >> 1);  // accepts until the band's last step
+    int taken, consumed;
+    if (M >= (1u << 17) - 1)
+      walk_chunk<16, kGlobal>(src, pos, len, i, d, M, k, J, lane, taken, consumed);
+    else if (M >= (1u << 15) - 1)
+      walk_chunk<8, kGlobal>(src, pos, len, i, d, M, k, J, lane, taken, consumed);
+    else if (M >= (1u << 13) - 1)
+      walk_chunk<4, kGlobal>(src, pos, len, i, d, M, k, J, lane, taken, consumed);
+    else if (M >= (1u << 11) - 1)
+      walk_chunk<2, kGlobal>(src, pos, len, i, d, M, k, J, lane, taken, consumed);
+    else
+      walk_chunk<1, kGlobal>(src, pos, len, i, d, M, k, J, lane, taken, consumed);
+    i -= taken;
+    pos += consumed;
+  }
+  *used = pos;
+  return i;
+}
+
+// draws past the buffer (jump-ahead per draw): lane 0, one draw at a time
+__device__ int warp_walk_slow(const SegArgs& a, const RngState& r0, long long base, int len, int i, int k, int* J,
+                              int lane, int* used) {
+  int pos = 0;
+  if (lane == 0) {
+    while (pos < len && i >= 1) {
+      const int x = (int)(seg_get(a, r0, base + pos) & smear((unsigned)i));
+      ++pos;
+      if (x <= i) {
+        if (J && i >= k) J[i] = x;
+        --i;
+      }
+    }
+  }
+  i = __shfl_sync(0xffffffffu, i, 0);
+  *used = __shfl_sync(0xffffffffu, pos, 0);
+  return i;
+}
+
+// phase 1 (func job tasks) and phase 3 (emit job segments) in one launch:
+// blocks [0, nb_func) are phase-1 tasks, the rest emit segments.
+__global__ void __launch_bounds__(kSegThreads) k_seg_pass(SegArgs a, int nb_func) {
+  extern __shared__ __align__(16) unsigned char ps_sm[];
+  unsigned int* sd = reinterpret_cast<unsigned int*>(ps_sm);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const RngState r0 = *a.rng0;
+  if ((int)blockIdx.x < nb_func) {
+    const SegJob& jb = a.func;
+    const int2 task = jb.tasks[blockIdx.x];
+    const SegTab t = jb.tab[task.x];
+    const long long p0 = *jb.pos_in;
+    const long long c0 = clock64();
+    seg_stage_cta(a, r0, p0 + t.off, t.len, sd);
+    const int j = task.y + warp;
+    if (j < t.nA + t.nB) {
+      int lo, W;
+      unsigned int M;
+      seg_sub_geom(t, j, lo, W, M);
+      seg_sub(sd, t.len, lo, W, M, a.rec + t.rec_off + j, lane);
+    }
+    if (a.prof && lane == 0) {
+      atomicAdd((unsigned long long*)&a.prof[7], 1ull);
+      atomicAdd((unsigned long long*)&a.prof[8], (unsigned long long)(clock64() - c0));
+      atomicMax((unsigned long long*)&a.prof[9], (unsigned long long)(clock64() - c0));
+    }
+  } else {
+    const SegJob& jb = a.emit;
+    const int s = (blockIdx.x - nb_func) * kSubPerCta + warp;
+    if (s >= *a.n_seg) return;
+    const int i0 = a.seg_start[s];
+    if (i0 < jb.k) return;  // no step >= k in this segment
+    const SegTab t = jb.tab[s];
+    const long long base = *jb.pos_in + t.off;
+    const long long c0 = clock64();
+    if (lane == 0) seg_prefetch_l2(a.draws, base, t.len, a.n_draws);
+    int used;
+    if (base + t.len <= a.n_draws) {
+      warp_walk<true>(a.draws + base, t.len, i0, jb.k, jb.J, lane, &used);
+    } else {
+      // past the draw buffer (never for the configured sizes): jump-ahead per draw
+      warp_walk_slow(a, r0, base, t.len, i0, jb.k, jb.J, lane, &used);
+    }
+    if (a.prof && lane == 0) {
+      atomicAdd((unsigned long long*)&a.prof[10], 1ull);
+      atomicMax((unsigned long long*)&a.prof[11], (unsigned long long)(clock64() - c0));
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async16_seg(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// phase 2: one warp chains the job's segments, then walks the tail (states
+// below kSegTail) to the job's last draw.
+constexpr int kComposeThreads = 32;
+
+__global__ void __launch_bounds__(kComposeThreads) k_seg_compose(SegArgs a) {
+  extern __shared__ __align__(16) unsigned char cs_sm[];
+  SegRec* ring = reinterpret_cast<SegRec*>(cs_sm);  // [kSegRing][kSegMaxSub]
+  SegTab* tring = reinterpret_cast<SegTab*>(cs_sm + (size_t)kSegRing * kSegMaxSub * sizeof(SegRec));
+  unsigned int* sd = reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned char*>(tring) +
+                                                    (size_t)kTabChunk * kTabChunks * sizeof(SegTab));
+  __shared__ __align__(8) uint64_t tab_bar[kTabChunks], rec_bar[kSegRing], st_bar;
+  __shared__ int s_i, s_s;
+  __shared__ long long s_p;
+  unsigned st_phase = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const SegJob& jb = a.func;
+  const RngState r0 = *a.rng0;
+  const long long p0 = *jb.pos_in;
+  const int S = jb.S;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kTabChunks; ++q) mbar_init(&tab_bar[q], 1);
+    for (int q = 0; q < kSegRing; ++q) mbar_init(&rec_bar[q], 1);
+    mbar_init(&st_bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // exact walk by one warp over draws staged in shared memory with bulk
+  // copies (16-byte aligned source: copy from base & ~3, walk from base & 3)
+  auto walk_from = [&](long long base, int len, int i, int* J, int* used) -> int {
+    int done = 0;
+    while (done < len && i >= 1) {
+      const long long b = base + done;
+      const int n = min(kSegMaxLen, len - done);
+      if (lane == 0 && len - done > n) seg_prefetch_l2(a.draws, b + n, min(kSegMaxLen, len - done - n), a.n_draws);
+      int u;
+      if (b + n + 4 <= a.n_draws) {
+        const long long ab = b & ~3ll;
+        const int o = (int)(b - ab);
+        const unsigned bytes = (unsigned)(((n + o + 3) / 4) * 16);
+        if (lane == 0) {
+          mbar_expect_tx(&st_bar, bytes);
+          tma_load_1d(sd, a.draws + ab, bytes, &st_bar);
+        }
+        mbar_wait(&st_bar, st_phase);
+        st_phase ^= 1u;
+        i = warp_walk<false>(sd + o, n, i, jb.k, J, lane, &u);
+      } else {
+        i = warp_walk_slow(a, r0, b, n, i, jb.k, J, lane, &u);
+      }
+      done += u;
+      __syncwarp();
+    }
+    *used = done;
+    return i;
+  };
+  long long c_chain = 0, c_resim = 0, n_resim = 0, c_wait = 0;
+  const long long c_start = clock64();
+  if (warp == 0) {
+    // ---- chain of the job's segments
+    int tab_waited = -1;  // table chunks [0, tab_waited] resident
+    auto tab_issue = [&](int c) {
+      const int first = c * kTabChunk, cnt = min(kTabChunk, S - first);
+      if (cnt > 0 && lane == 0) {
+        uint64_t* bar = &tab_bar[c % kTabChunks];
+        mbar_expect_tx(bar, (unsigned)cnt * (unsigned)sizeof(SegTab));
+        tma_load_1d(tring + (c % kTabChunks) * kTabChunk, jb.tab + first, (unsigned)cnt * (unsigned)sizeof(SegTab),
+                    bar);
+      }
+    };
+    auto tab_need = [&](int q) {
+      const int c = q / kTabChunk;
+      while (tab_waited < c) {
+        ++tab_waited;
+        mbar_wait(&tab_bar[tab_waited % kTabChunks], (unsigned)((tab_waited / kTabChunks) & 1));
+        tab_issue(tab_waited + 2);  // its slot held chunk tab_waited - 2
+      }
+    };
+    auto issue = [&](int q) {  // records of segment q into slot q % kSegRing
+      if (q < S) {
+        tab_need(q);
+        const SegTab& t = tring[q % (kTabChunk * kTabChunks)];
+        if (lane == 0) {
+          uint64_t* bar = &rec_bar[q % kSegRing];
+          const unsigned bytes = (unsigned)(t.nA + t.nB) * (unsigned)sizeof(SegRec);
+          mbar_expect_tx(bar, bytes);
+          tma_load_1d(ring + (q % kSegRing) * kSegMaxSub, a.rec + t.rec_off, bytes, bar);
+        }
+      }
+    };
+    int i = jb.n - 1;
+    int s = 0;
+    if (S > 0) {
+      tab_issue(0);
+      tab_issue(1);
+      for (int q = 0; q < kSegRing; ++q) issue(q);
+    }
+    for (; s < S && i >= kSegTail; ++s) {
+      const long long cw0 = clock64();
+      mbar_wait(&rec_bar[s % kSegRing], (unsigned)((s / kSegRing) & 1));
+      c_wait += clock64() - cw0;
+      if (lane == 0) a.seg_start[s] = i;
+      const SegTab& t = tring[s % (kTabChunk * kTabChunks)];
+      int j = -1, lo = 0;
+      if (i >= t.loA && i <= t.hiA) {
+        j = (i - t.loA) / kSub;
+        lo = t.loA + kSub * j;
+      } else if (t.nB > 0 && i >= t.loB && i <= t.hiB) {
+        j = t.nA + (i - t.loB) / kSub;
+        lo = t.loB + kSub * (j - t.nA);
+      }
+      int next = -1;
+      if (j >= 0) {
+        const SegRec& R = ring[(s % kSegRing) * kSegMaxSub + j];
+        const int r = i - lo, w = r >> 5, bt = r & 31;
+        const unsigned int m = bt == 31 ? 0xffffffffu : ((2u << bt) - 1u);
+        const int e = R.a_end + (int)R.pref[w] + __popc(R.words[w] & m);
+        if (e > R.h) next = e;
+      }
+      const int off = t.off, len = t.len;
+      __syncwarp();
+      issue(s + kSegRing);
+      if (next < 0) {
+        // exact walk (band crossing inside the segment, or a window miss); the
+        // J values are emitted by phase 3
+        const long long cr = clock64();
+        int used;
+        next = walk_from(p0 + off, len, i, nullptr, &used);
+        c_resim += clock64() - cr;
+        ++n_resim;
+      }
+      i = next;
+    }
+    if (S > 0) {
+      // drain the bulk copies still in flight
+      for (int q = s; q < min(S, s + kSegRing); ++q) mbar_wait(&rec_bar[q % kSegRing], (unsigned)((q / kSegRing) & 1));
+      const int last_chunk = min((S - 1) / kTabChunk, tab_waited + 2);
+      for (int c = tab_waited + 1; c <= last_chunk; ++c)
+        mbar_wait(&tab_bar[c % kTabChunks], (unsigned)((c / kTabChunks) & 1));
+    }
+    if (lane == 0) {
+      *a.n_seg = s;
+      s_i = i;
+      s_s = s;
+      long long p = p0;
+      if (s > 0) p = p0 + (s < S ? (long long)jb.tab[s].off : (long long)jb.tab[S - 1].off + jb.tab[S - 1].len);
+      s_p = p;
+    }
+    c_chain = clock64() - c_start - c_resim;
+  }
+  __syncthreads();
+  int i = s_i;
+  long long p = s_p;
+  const long long ct = clock64();
+  // ---- the last states: exact walk to i == 0 (warp 0)
+  if (warp == 0) {
+    long long tail = 0;
+    while (i >= 1) {
+      int used;
+      i = walk_from(p, 8 * kSegMaxLen, i, jb.J, &used);
+      p += used;
+      tail += used;
+    }
+    if (lane == 0) {
+      *jb.pos_out = p;
+      if (a.prof) {
+        atomicAdd((unsigned long long*)&a.prof[0], (unsigned long long)s_s);
+        atomicAdd((unsigned long long*)&a.prof[1], (unsigned long long)n_resim);
+        atomicAdd((unsigned long long*)&a.prof[2], (unsigned long long)tail);
+        atomicAdd((unsigned long long*)&a.prof[3], 1ull);
+        atomicAdd((unsigned long long*)&a.prof[4], (unsigned long long)c_chain);
+        atomicAdd((unsigned long long*)&a.prof[5], (unsigned long long)c_resim);
+        atomicAdd((unsigned long long*)&a.prof[6], (unsigned long long)(clock64() - ct));
+        atomicAdd((unsigned long long*)&a.prof[12], (unsigned long long)c_wait);
+      }
+      if (jb.write_rng) {
+        RngState r = r0;
+        long long dd = p;
+        if (r.has_uint32 && dd > 0) {
+          r.has_uint32 = 0;
+          dd -= 1;
+        }
+        if (dd > 0) {
+          const unsigned long long outs = (unsigned long long)((dd + 1) / 2);
+          const U128 st = pcg_jump(*a.jump, r0.s, outs);
+          r.s = st;
+          if (dd & 1) {
+            r.has_uint32 = 1;
+            r.uinteger = (unsigned int)(xsl_rr(st) >> 32);
+          } else {
+            r.has_uint32 = 0;
+            r.uinteger = 0;
+          }
+        }
+        *a.rng = r;
+      }
+    }
+  }
+}
+
+}  // namespace bb

@@ -92,7 +92,8 @@ def _np_masks(seed, a, b, rate, T):
 @pytest.mark.parametrize("seed,a,b,rate,T", [(0, 50_000, 50_000, 0.5, 3), (7, 1, 2, 0.5, 3), (3, 1000, 17, 0.3, 4),
                                              (9, 65_537, 131_071, 0.77, 2), (2**40 + 5, 2, 5, 1.0, 2),
                                              (42, 5, 100_000, 0.01, 2), (123, 300_000, 700_000, 0.5, 2),
-                                             (5, 0, 9, 0.5, 2), (8, 2_000_003, 1_048_577, 0.5, 1)])
+                                             (5, 0, 9, 0.5, 2), (8, 2_000_003, 1_048_577, 0.5, 1),
+                                             (17, 300_000, 700_000, 0.5, 10)])
 def test_gpu_subsample_masks_match_numpy(seed, a, b, rate, T):
     cfg = _lib.FitConfigC(**_lib.pcg_config(seed))
     words = (a + b + 31) // 32

@@ -264,7 +264,7 @@ static SegPlan build_seg_plan(int n) {
   if (n - 1 < kSegTail) return P;
   long long off = 0;
   SegTab t{};
-  while (seg_geom(n - 1, off, kSegTail, &t)) {
+  while (seg_geom(n - 1, off, kSegTail, &t, 2 * kAnchorSlack)) {
     t.rec_off = P.n_rec;
     const int ns = t.nA + t.nB;
     for (int q = 0; q < ns; q += kSubPerCta) P.tasks.push_back(int2{(int)P.tab.size(), q});
@@ -300,7 +300,12 @@ struct MaskGen {
   int S[2] = {0, 0}, n_tasks[2] = {0, 0};
   SegRec* rec = nullptr;
   int *seg_start = nullptr, *n_seg = nullptr;
-  long long* spos = nullptr;
+  long long* spos = nullptr;     // true first draw of each job of a chunk
+  long long* sanchor = nullptr;  // anchor (predicted first draw + slack) of each job
+  long long* stail = nullptr;    // chain -> tail hand-off: draw
+  int* stail_i = nullptr;        //                         state
+  cudaStream_t sb = nullptr;     // phase 1 / 3 stream (overlaps the tails)
+  cudaEvent_t evA = nullptr, evB = nullptr;
   RngState* rng0 = nullptr;
   bool legacy_cl = false;  // BB_CL_PARSE: the cluster parse instead
 
@@ -381,9 +386,25 @@ struct MaskGen {
     seg_start = A.alloc<int>(smax);
     n_seg = A.alloc<int>(1);
     spos = A.alloc<long long>(2 * (size_t)chunk + 2);
+    sanchor = A.alloc<long long>(2 * (size_t)chunk + 2);
+    stail = A.alloc<long long>(1);
+    stail_i = A.alloc<int>(1);
+    int lo_prio = 0, hi_prio = 0;
+    BB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    BB_CUDA(cudaStreamCreateWithPriority(&sb, cudaStreamNonBlocking, hi_prio));
+    BB_CUDA(cudaEventCreateWithFlags(&evA, cudaEventDisableTiming));
+    BB_CUDA(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
     rng0 = A.alloc<RngState>(1);
     BB_CUDA(cudaFuncSetAttribute(k_seg_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegPassSmem));
-    BB_CUDA(cudaFuncSetAttribute(k_seg_compose, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegComposeSmem));
+    BB_CUDA(cudaFuncSetAttribute(k_seg_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegComposeSmem));
+  }
+  ~MaskGen() {
+    if (sb) {
+      cudaStreamSynchronize(sb);
+      cudaStreamDestroy(sb);
+    }
+    if (evA) cudaEventDestroy(evA);
+    if (evB) cudaEventDestroy(evB);
   }
   void report(cudaStream_t st) {
     if (!prof) return;
@@ -399,7 +420,8 @@ struct MaskGen {
   int64_t enqueue_seg(cudaStream_t st, int count) {
     int64_t launches = 0;
     BB_CUDA(cudaMemcpyAsync(rng0, rng, sizeof(RngState), cudaMemcpyDeviceToDevice, st));
-    BB_CUDA(cudaMemsetAsync(spos, 0, sizeof(long long), st));
+    k_seg_init<<<1, 1, 0, st>>>(spos, sanchor);
+    BB_LAUNCH_CHECK();
     const long long stride = std::max(n[0], n[1]);
     SegArgs sa{};
     sa.draws = draws;
@@ -410,11 +432,11 @@ struct MaskGen {
     sa.rec = rec;
     sa.seg_start = seg_start;
     sa.n_seg = n_seg;
+    sa.tail_p = stail;
+    sa.tail_i = stail_i;
     sa.prof = prof;
-    SegJob prev{};
-    bool have_prev = false;
     const int jobs = 2 * count;
-    for (int jj = 0; jj <= jobs; ++jj) {
+    auto make_job = [&](int jj) {
       SegJob job{};
       if (jj < jobs) {
         const int t = jj >> 1, cc = jj & 1;
@@ -427,24 +449,41 @@ struct MaskGen {
         job.J = J[cc] + (size_t)t * stride;
         job.pos_in = spos + jj;
         job.pos_out = spos + jj + 1;
+        job.anchor_in = sanchor + jj;
+        job.anchor_out = jj + 1 < jobs ? sanchor + jj + 1 : nullptr;
         job.write_rng = jj == jobs - 1;
       }
-      const int nb_func = job.n_tasks;
-      const int nb_emit = have_prev ? (int)ceil_div(prev.S, kSubPerCta) : 0;
+      return job;
+    };
+    auto pass = [&](cudaStream_t s, const SegJob& func, const SegJob& emit) {
+      const int nb_func = func.n_tasks;
+      const int nb_emit = (int)ceil_div(emit.S, kSubPerCta);
+      if (nb_func + nb_emit == 0) return;
+      sa.func = func;
+      sa.emit = emit;
+      k_seg_pass<<<nb_func + nb_emit, kSegThreads, kSegPassSmem, s>>>(sa, nb_func);
+      BB_LAUNCH_CHECK();
+      launches += 1;
+    };
+    // stream st: chain(j) -> tail(j) -> chain(j+1) ...; stream sb, after
+    // chain(j): phase 1 of job j+1 and phase 3 of job j, concurrent with tail(j)
+    pass(st, make_job(0), SegJob{});
+    for (int jj = 0; jj < jobs; ++jj) {
+      const SegJob job = make_job(jj);
       sa.func = job;
-      sa.emit = prev;
-      if (nb_func + nb_emit > 0) {
-        k_seg_pass<<<nb_func + nb_emit, kSegThreads, kSegPassSmem, st>>>(sa, nb_func);
-        BB_LAUNCH_CHECK();
-        launches += 1;
-      }
-      if (jj < jobs) {
-        k_seg_compose<<<1, kComposeThreads, kSegComposeSmem, st>>>(sa);
-        BB_LAUNCH_CHECK();
-        launches += 1;
-      }
-      prev = job;
-      have_prev = true;
+      sa.emit = SegJob{};
+      k_seg_chain<<<1, 32, kSegComposeSmem, st>>>(sa);
+      BB_LAUNCH_CHECK();
+      BB_CUDA(cudaEventRecord(evA, st));
+      BB_CUDA(cudaStreamWaitEvent(sb, evA, 0));
+      pass(sb, make_job(jj + 1), job);
+      BB_CUDA(cudaEventRecord(evB, sb));
+      sa.func = job;
+      sa.emit = SegJob{};
+      k_seg_tail<<<1, 32, 0, st>>>(sa);
+      BB_LAUNCH_CHECK();
+      BB_CUDA(cudaStreamWaitEvent(st, evB, 0));
+      launches += 2;
     }
     return launches;
   }

@@ -45,6 +45,7 @@ namespace bb {
 
 constexpr int kSegMaxLen = 8192;   // draws per segment (max)
 constexpr int kSegCrossLen = 1024; // draws per segment in band-crossing zones
+constexpr int kAnchorSlack = 512;  // a job's segments start at its predicted first draw + this
 constexpr int kSub = 512;          // states per phase-1 sub-window (one warp)
 constexpr int kSubPerCta = 8;      // sub-windows per phase-1 CTA (= warps per k_seg_pass CTA)
 constexpr int kSegMaxSub = 20;     // sub-windows per segment (max)
@@ -89,6 +90,18 @@ __host__ __device__ inline double seg_pred_state(int i0, double p) {
   }
 }
 
+// expected draws from state i0 to the end of the job (state 0)
+__host__ __device__ inline double seg_expected_draws(int i0) {
+  double x = (double)i0 + 1.0, p = 0.0;
+  while (x > 1.0 + 1e-9) {
+    const unsigned M = smear_host((unsigned)fmax(1.0, floor(x - 1.0)));
+    const double mp1 = (double)M + 1.0, lowx = mp1 / 2.0;
+    p += mp1 * log(x / lowx);
+    x = lowx;
+  }
+  return p;
+}
+
 // half window after p draws: 5 sd (sd <= sqrt(p)/2); a start outside the
 // window only costs an exact walk
 __host__ __device__ inline double seg_half_window(double p) {
@@ -101,12 +114,12 @@ __host__ __device__ inline double seg_half_window(double p) {
 // sub-window merge at most; kSegCrossLen draws where some start may reach
 // its band's last state, so the exact walk a crossing costs stays short).
 // Returns false once the window lies below floor_state.
-__host__ __device__ inline bool seg_geom(int i0, long long off, int floor_state, SegTab* t) {
+__host__ __device__ inline bool seg_geom(int i0, long long off, int floor_state, SegTab* t, long long slack = 0) {
+  // the job has consumed between off and off + slack draws at this segment
   const double pi = seg_pred_state(i0, (double)off);
-  const double H = seg_half_window((double)off);
-  int lo = (int)fmax(1.0, floor(pi - H));
-  int hi = (int)fmin((double)i0, ceil(pi + H));
-  if (off == 0) lo = hi = i0;
+  const double pl = seg_pred_state(i0, (double)(off + slack));
+  int lo = (int)fmax(1.0, floor(pl - seg_half_window((double)(off + slack))));
+  int hi = (int)fmin((double)i0, ceil(pi + seg_half_window((double)off)));
   if (hi < floor_state || lo > hi) return false;
   t->off = (int)off;
   const unsigned Mh = smear_host((unsigned)hi);
@@ -128,7 +141,7 @@ __host__ __device__ inline bool seg_geom(int i0, long long off, int floor_state,
   const double L = 0.176 * ((double)M + 1.0);
   int Lp = 256;
   while (Lp * 2 <= L && Lp < kSegMaxLen) Lp *= 2;
-  const double pe = seg_pred_state(i0, (double)(off + Lp)) - seg_half_window((double)(off + Lp));
+  const double pe = seg_pred_state(i0, (double)(off + slack + Lp)) - seg_half_window((double)(off + slack + Lp));
   if (lo < bbA || pe < (double)bbA) Lp = Lp < kSegCrossLen ? Lp : kSegCrossLen;
   t->len = Lp;
   return true;
@@ -149,8 +162,10 @@ struct SegJob {
   int n_tasks;
   int* J;                      // J[i] for steps i >= k
   long long* pos_in;           // job's first draw (absolute index into the draw buffer)
-  long long* pos_out;          // written by compose: first draw of the next job
-  int write_rng;               // compose: update the RNG state after this job
+  long long* pos_out;          // written by the tail: first draw of the next job
+  long long* anchor_in;        // first draw of segment 0 (predicted first draw + kAnchorSlack)
+  long long* anchor_out;       // written by the chain: the next job's anchor (nullptr: none)
+  int write_rng;               // tail: update the RNG state after this job
 };
 
 struct SegArgs {
@@ -162,6 +177,8 @@ struct SegArgs {
   SegRec* rec;                 // sub-window records of the job in phase 1/2
   int* seg_start;              // [S] exact start states (phase 2 -> phase 3)
   int* n_seg;                  // segments composed (phase 2 -> phase 3)
+  long long* tail_p;           // chain -> tail: first draw of the tail
+  int* tail_i;                 // chain -> tail: state there
   SegJob func, emit;           // k_seg_pass: phase-1 job (n_tasks = 0: none), phase-3 job
   long long* prof;
 };
@@ -482,7 +499,7 @@ __global__ void __launch_bounds__(kSegThreads) k_seg_pass(SegArgs a, int nb_func
     const SegJob& jb = a.func;
     const int2 task = jb.tasks[blockIdx.x];
     const SegTab t = jb.tab[task.x];
-    const long long p0 = *jb.pos_in;
+    const long long p0 = *jb.anchor_in;
     const long long c0 = clock64();
     seg_stage_cta(a, r0, p0 + t.off, t.len, sd);
     const int j = task.y + warp;
@@ -504,7 +521,7 @@ __global__ void __launch_bounds__(kSegThreads) k_seg_pass(SegArgs a, int nb_func
     const int i0 = a.seg_start[s];
     if (i0 < jb.k) return;  // no step >= k in this segment
     const SegTab t = jb.tab[s];
-    const long long base = *jb.pos_in + t.off;
+    const long long base = *jb.anchor_in + t.off;
     const long long c0 = clock64();
     if (lane == 0) seg_prefetch_l2(a.draws, base, t.len, a.n_draws);
     int used;
@@ -525,203 +542,241 @@ __device__ __forceinline__ void cp_async16_seg(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
-// phase 2: one warp chains the job's segments, then walks the tail (states
-// below kSegTail) to the job's last draw.
-constexpr int kComposeThreads = 32;
-
-__global__ void __launch_bounds__(kComposeThreads) k_seg_compose(SegArgs a) {
-  extern __shared__ __align__(16) unsigned char cs_sm[];
-  SegRec* ring = reinterpret_cast<SegRec*>(cs_sm);  // [kSegRing][kSegMaxSub]
-  SegTab* tring = reinterpret_cast<SegTab*>(cs_sm + (size_t)kSegRing * kSegMaxSub * sizeof(SegRec));
-  unsigned int* sd = reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned char*>(tring) +
-                                                    (size_t)kTabChunk * kTabChunks * sizeof(SegTab));
-  __shared__ __align__(8) uint64_t tab_bar[kTabChunks], rec_bar[kSegRing], st_bar;
-  __shared__ int s_i, s_s;
-  __shared__ long long s_p;
-  unsigned st_phase = 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const SegJob& jb = a.func;
-  const RngState r0 = *a.rng0;
-  const long long p0 = *jb.pos_in;
-  const int S = jb.S;
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < kTabChunks; ++q) mbar_init(&tab_bar[q], 1);
-    for (int q = 0; q < kSegRing; ++q) mbar_init(&rec_bar[q], 1);
-    mbar_init(&st_bar, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  // exact walk by one warp over draws staged in shared memory with bulk
-  // copies (16-byte aligned source: copy from base & ~3, walk from base & 3)
-  auto walk_from = [&](long long base, int len, int i, int* J, int* used) -> int {
-    int done = 0;
+// Exact walk by one warp over draws staged in shared memory by bulk copies
+// (16-byte aligned source: copy from base & ~3, walk from base & 3).
+struct StageWalk {
+  unsigned int* sd;  // kSegMaxLen + 16 draws
+  uint64_t* bar;
+  unsigned phase;
+  __device__ int operator()(const SegArgs& a, const RngState& r0, long long base, long long len, int i, int k, int* J,
+                            int lane, long long* used) {
+    long long done = 0;
     while (done < len && i >= 1) {
       const long long b = base + done;
-      const int n = min(kSegMaxLen, len - done);
-      if (lane == 0 && len - done > n) seg_prefetch_l2(a.draws, b + n, min(kSegMaxLen, len - done - n), a.n_draws);
+      const int n = (int)min((long long)kSegMaxLen, len - done);
+      if (lane == 0 && len - done > n)
+        seg_prefetch_l2(a.draws, b + n, min((long long)kSegMaxLen, len - done - n), a.n_draws);
       int u;
       if (b + n + 4 <= a.n_draws) {
         const long long ab = b & ~3ll;
         const int o = (int)(b - ab);
         const unsigned bytes = (unsigned)(((n + o + 3) / 4) * 16);
         if (lane == 0) {
-          mbar_expect_tx(&st_bar, bytes);
-          tma_load_1d(sd, a.draws + ab, bytes, &st_bar);
+          mbar_expect_tx(bar, bytes);
+          tma_load_1d(sd, a.draws + ab, bytes, bar);
         }
-        mbar_wait(&st_bar, st_phase);
-        st_phase ^= 1u;
-        i = warp_walk<false>(sd + o, n, i, jb.k, J, lane, &u);
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        i = warp_walk<false>(sd + o, n, i, k, J, lane, &u);
       } else {
-        i = warp_walk_slow(a, r0, b, n, i, jb.k, J, lane, &u);
+        i = warp_walk_slow(a, r0, b, n, i, k, J, lane, &u);
       }
       done += u;
       __syncwarp();
     }
     *used = done;
     return i;
-  };
-  long long c_chain = 0, c_resim = 0, n_resim = 0, c_wait = 0;
+  }
+};
+
+// phase 2a: one warp.  From the job's exact first draw, walk to the first
+// segment (the anchor), then chain the segments' functions down to
+// kSegTail; hand the tail's (draw, state) to k_seg_tail and predict the next
+// job's first draw (its anchor) so its phase 1 can run during the tail.
+__global__ void __launch_bounds__(32) k_seg_chain(SegArgs a) {
+  extern __shared__ __align__(16) unsigned char cs_sm[];
+  SegRec* ring = reinterpret_cast<SegRec*>(cs_sm);  // [kSegRing][kSegMaxSub]
+  SegTab* tring = reinterpret_cast<SegTab*>(cs_sm + (size_t)kSegRing * kSegMaxSub * sizeof(SegRec));
+  unsigned int* sd = reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned char*>(tring) +
+                                                    (size_t)kTabChunk * kTabChunks * sizeof(SegTab));
+  __shared__ __align__(8) uint64_t tab_bar[kTabChunks], rec_bar[kSegRing], st_bar;
+  const int lane = threadIdx.x;
+  const SegJob& jb = a.func;
+  const RngState r0 = *a.rng0;
+  const long long p0 = *jb.pos_in;
+  const long long anc = *jb.anchor_in;
+  const int S = jb.S;
+  if (lane == 0) {
+    for (int q = 0; q < kTabChunks; ++q) mbar_init(&tab_bar[q], 1);
+    for (int q = 0; q < kSegRing; ++q) mbar_init(&rec_bar[q], 1);
+    mbar_init(&st_bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  StageWalk walk{sd, &st_bar, 0u};
+  long long c_resim = 0, n_resim = 0;
   const long long c_start = clock64();
-  if (warp == 0) {
-    // ---- chain of the job's segments
-    int tab_waited = -1;  // table chunks [0, tab_waited] resident
-    auto tab_issue = [&](int c) {
-      const int first = c * kTabChunk, cnt = min(kTabChunk, S - first);
-      if (cnt > 0 && lane == 0) {
-        uint64_t* bar = &tab_bar[c % kTabChunks];
-        mbar_expect_tx(bar, (unsigned)cnt * (unsigned)sizeof(SegTab));
-        tma_load_1d(tring + (c % kTabChunks) * kTabChunk, jb.tab + first, (unsigned)cnt * (unsigned)sizeof(SegTab),
-                    bar);
-      }
-    };
-    auto tab_need = [&](int q) {
-      const int c = q / kTabChunk;
-      while (tab_waited < c) {
-        ++tab_waited;
-        mbar_wait(&tab_bar[tab_waited % kTabChunks], (unsigned)((tab_waited / kTabChunks) & 1));
-        tab_issue(tab_waited + 2);  // its slot held chunk tab_waited - 2
-      }
-    };
-    auto issue = [&](int q) {  // records of segment q into slot q % kSegRing
-      if (q < S) {
-        tab_need(q);
-        const SegTab& t = tring[q % (kTabChunk * kTabChunks)];
-        if (lane == 0) {
-          uint64_t* bar = &rec_bar[q % kSegRing];
-          const unsigned bytes = (unsigned)(t.nA + t.nB) * (unsigned)sizeof(SegRec);
-          mbar_expect_tx(bar, bytes);
-          tma_load_1d(ring + (q % kSegRing) * kSegMaxSub, a.rec + t.rec_off, bytes, bar);
-        }
-      }
-    };
-    int i = jb.n - 1;
-    int s = 0;
-    if (S > 0) {
-      tab_issue(0);
-      tab_issue(1);
-      for (int q = 0; q < kSegRing; ++q) issue(q);
-    }
-    for (; s < S && i >= kSegTail; ++s) {
-      const long long cw0 = clock64();
-      mbar_wait(&rec_bar[s % kSegRing], (unsigned)((s / kSegRing) & 1));
-      c_wait += clock64() - cw0;
-      if (lane == 0) a.seg_start[s] = i;
-      const SegTab& t = tring[s % (kTabChunk * kTabChunks)];
-      int j = -1, lo = 0;
-      if (i >= t.loA && i <= t.hiA) {
-        j = (i - t.loA) / kSub;
-        lo = t.loA + kSub * j;
-      } else if (t.nB > 0 && i >= t.loB && i <= t.hiB) {
-        j = t.nA + (i - t.loB) / kSub;
-        lo = t.loB + kSub * (j - t.nA);
-      }
-      int next = -1;
-      if (j >= 0) {
-        const SegRec& R = ring[(s % kSegRing) * kSegMaxSub + j];
-        const int r = i - lo, w = r >> 5, bt = r & 31;
-        const unsigned int m = bt == 31 ? 0xffffffffu : ((2u << bt) - 1u);
-        const int e = R.a_end + (int)R.pref[w] + __popc(R.words[w] & m);
-        if (e > R.h) next = e;
-      }
-      const int off = t.off, len = t.len;
-      __syncwarp();
-      issue(s + kSegRing);
-      if (next < 0) {
-        // exact walk (band crossing inside the segment, or a window miss); the
-        // J values are emitted by phase 3
-        const long long cr = clock64();
-        int used;
-        next = walk_from(p0 + off, len, i, nullptr, &used);
-        c_resim += clock64() - cr;
-        ++n_resim;
-      }
-      i = next;
-    }
-    if (S > 0) {
-      // drain the bulk copies still in flight
-      for (int q = s; q < min(S, s + kSegRing); ++q) mbar_wait(&rec_bar[q % kSegRing], (unsigned)((q / kSegRing) & 1));
-      const int last_chunk = min((S - 1) / kTabChunk, tab_waited + 2);
-      for (int c = tab_waited + 1; c <= last_chunk; ++c)
-        mbar_wait(&tab_bar[c % kTabChunks], (unsigned)((c / kTabChunks) & 1));
-    }
-    if (lane == 0) {
-      *a.n_seg = s;
-      s_i = i;
-      s_s = s;
-      long long p = p0;
-      if (s > 0) p = p0 + (s < S ? (long long)jb.tab[s].off : (long long)jb.tab[S - 1].off + jb.tab[S - 1].len);
-      s_p = p;
-    }
-    c_chain = clock64() - c_start - c_resim;
+  // first segment at or after the true first draw (segment 0 unless the job
+  // started more than kAnchorSlack draws late); earlier segments are skipped
+  int s0 = 0;
+  while (s0 < S && anc + jb.tab[s0].off < p0) ++s0;
+  for (int q = lane; q < s0; q += 32) a.seg_start[q] = -1;
+  int i = jb.n - 1;
+  long long p = p0;
+  if (s0 < S) {
+    long long used;
+    i = walk(a, r0, p0, anc + jb.tab[s0].off - p0, i, jb.k, jb.J, lane, &used);  // n-1 >= kSegTail: never ends the job
+    p = anc + jb.tab[s0].off;
   }
-  __syncthreads();
-  int i = s_i;
-  long long p = s_p;
+  // records and table entries stream in with bulk copies; segment q uses
+  // record slot (q - s0) % kSegRing
+  int tab_waited = -1;
+  auto tab_issue = [&](int c) {
+    const int first = c * kTabChunk, cnt = min(kTabChunk, S - first);
+    if (cnt > 0 && lane == 0) {
+      uint64_t* bar = &tab_bar[c % kTabChunks];
+      mbar_expect_tx(bar, (unsigned)cnt * (unsigned)sizeof(SegTab));
+      tma_load_1d(tring + (c % kTabChunks) * kTabChunk, jb.tab + first, (unsigned)cnt * (unsigned)sizeof(SegTab), bar);
+    }
+  };
+  auto tab_need = [&](int q) {
+    const int c = q / kTabChunk;
+    while (tab_waited < c) {
+      ++tab_waited;
+      mbar_wait(&tab_bar[tab_waited % kTabChunks], (unsigned)((tab_waited / kTabChunks) & 1));
+      tab_issue(tab_waited + 2);  // its slot held chunk tab_waited - 2
+    }
+  };
+  auto issue = [&](int q) {
+    if (q < S) {
+      tab_need(q);
+      const SegTab& t = tring[q % (kTabChunk * kTabChunks)];
+      if (lane == 0) {
+        uint64_t* bar = &rec_bar[(q - s0) % kSegRing];
+        const unsigned bytes = (unsigned)(t.nA + t.nB) * (unsigned)sizeof(SegRec);
+        mbar_expect_tx(bar, bytes);
+        tma_load_1d(ring + ((q - s0) % kSegRing) * kSegMaxSub, a.rec + t.rec_off, bytes, bar);
+      }
+    }
+  };
+  int s = s0;
+  if (s0 < S) {
+    tab_issue(0);
+    tab_issue(1);
+    for (int q = s0; q < s0 + kSegRing; ++q) issue(q);
+  }
+  for (; s < S && i >= kSegTail; ++s) {
+    const int rs = s - s0;
+    mbar_wait(&rec_bar[rs % kSegRing], (unsigned)((rs / kSegRing) & 1));
+    if (lane == 0) a.seg_start[s] = i;
+    const SegTab& t = tring[s % (kTabChunk * kTabChunks)];
+    int j = -1, lo = 0;
+    if (i >= t.loA && i <= t.hiA) {
+      j = (i - t.loA) / kSub;
+      lo = t.loA + kSub * j;
+    } else if (t.nB > 0 && i >= t.loB && i <= t.hiB) {
+      j = t.nA + (i - t.loB) / kSub;
+      lo = t.loB + kSub * (j - t.nA);
+    }
+    int next = -1;
+    if (j >= 0) {
+      const SegRec& R = ring[(rs % kSegRing) * kSegMaxSub + j];
+      const int r = i - lo, w = r >> 5, bt = r & 31;
+      const unsigned int m = bt == 31 ? 0xffffffffu : ((2u << bt) - 1u);
+      const int e = R.a_end + (int)R.pref[w] + __popc(R.words[w] & m);
+      if (e > R.h) next = e;
+    }
+    const int off = t.off, len = t.len;
+    __syncwarp();
+    issue(s + kSegRing);
+    if (next < 0) {
+      // exact walk (band crossing inside the segment, or a window miss); the
+      // J values are emitted by phase 3
+      const long long cr = clock64();
+      long long used;
+      next = walk(a, r0, anc + off, len, i, jb.k, nullptr, lane, &used);
+      c_resim += clock64() - cr;
+      ++n_resim;
+    }
+    i = next;
+    p = anc + off + len;
+  }
+  if (s0 < S) {
+    // drain the bulk copies still in flight
+    for (int q = s; q < min(S, s + kSegRing); ++q)
+      mbar_wait(&rec_bar[(q - s0) % kSegRing], (unsigned)(((q - s0) / kSegRing) & 1));
+    const int last_chunk = min((S - 1) / kTabChunk, tab_waited + 2);
+    for (int c = tab_waited + 1; c <= last_chunk; ++c)
+      mbar_wait(&tab_bar[c % kTabChunks], (unsigned)((c / kTabChunks) & 1));
+  }
+  if (lane == 0) {
+    *a.n_seg = s;
+    *a.tail_p = p;
+    *a.tail_i = i;
+    if (jb.anchor_out) *jb.anchor_out = p + (long long)(seg_expected_draws(i) + 0.5) + kAnchorSlack;
+    if (a.prof) {
+      atomicAdd((unsigned long long*)&a.prof[0], (unsigned long long)(s - s0));
+      atomicAdd((unsigned long long*)&a.prof[1], (unsigned long long)n_resim);
+      atomicAdd((unsigned long long*)&a.prof[4], (unsigned long long)(clock64() - c_start - c_resim));
+      atomicAdd((unsigned long long*)&a.prof[5], (unsigned long long)c_resim);
+      atomicAdd((unsigned long long*)&a.prof[13], (unsigned long long)s0);
+    }
+  }
+}
+
+// phase 2b: one warp walks the tail (states below kSegTail) to the job's
+// last draw, writing J for steps >= k; the next draw is the next job's first.
+__global__ void __launch_bounds__(32) k_seg_tail(SegArgs a) {
+  __shared__ __align__(16) unsigned int sd[kSegMaxLen + 16];
+  __shared__ __align__(8) uint64_t st_bar;
+  const int lane = threadIdx.x;
+  const SegJob& jb = a.func;
+  const RngState r0 = *a.rng0;
+  if (lane == 0) {
+    mbar_init(&st_bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  StageWalk walk{sd, &st_bar, 0u};
+  long long p = *a.tail_p;
+  int i = *a.tail_i;
   const long long ct = clock64();
-  // ---- the last states: exact walk to i == 0 (warp 0)
-  if (warp == 0) {
-    long long tail = 0;
-    while (i >= 1) {
-      int used;
-      i = walk_from(p, 8 * kSegMaxLen, i, jb.J, &used);
-      p += used;
-      tail += used;
+  long long tail = 0;
+  while (i >= 1) {
+    long long used;
+    i = walk(a, r0, p, 8 * kSegMaxLen, i, jb.k, jb.J, lane, &used);
+    p += used;
+    tail += used;
+  }
+  if (lane == 0) {
+    *jb.pos_out = p;
+    if (a.prof) {
+      atomicAdd((unsigned long long*)&a.prof[2], (unsigned long long)tail);
+      atomicAdd((unsigned long long*)&a.prof[3], 1ull);
+      atomicAdd((unsigned long long*)&a.prof[6], (unsigned long long)(clock64() - ct));
+      // anchor error: true first draw of the next job vs the predicted one
+      if (jb.anchor_out) {
+        const long long e = p - (*jb.anchor_out - kAnchorSlack);
+        atomicMax((unsigned long long*)&a.prof[14], (unsigned long long)(e < 0 ? -e : e));
+      }
     }
-    if (lane == 0) {
-      *jb.pos_out = p;
-      if (a.prof) {
-        atomicAdd((unsigned long long*)&a.prof[0], (unsigned long long)s_s);
-        atomicAdd((unsigned long long*)&a.prof[1], (unsigned long long)n_resim);
-        atomicAdd((unsigned long long*)&a.prof[2], (unsigned long long)tail);
-        atomicAdd((unsigned long long*)&a.prof[3], 1ull);
-        atomicAdd((unsigned long long*)&a.prof[4], (unsigned long long)c_chain);
-        atomicAdd((unsigned long long*)&a.prof[5], (unsigned long long)c_resim);
-        atomicAdd((unsigned long long*)&a.prof[6], (unsigned long long)(clock64() - ct));
-        atomicAdd((unsigned long long*)&a.prof[12], (unsigned long long)c_wait);
+    if (jb.write_rng) {
+      RngState r = r0;
+      long long dd = p;
+      if (r.has_uint32 && dd > 0) {
+        r.has_uint32 = 0;
+        dd -= 1;
       }
-      if (jb.write_rng) {
-        RngState r = r0;
-        long long dd = p;
-        if (r.has_uint32 && dd > 0) {
+      if (dd > 0) {
+        const unsigned long long outs = (unsigned long long)((dd + 1) / 2);
+        const U128 st = pcg_jump(*a.jump, r0.s, outs);
+        r.s = st;
+        if (dd & 1) {
+          r.has_uint32 = 1;
+          r.uinteger = (unsigned int)(xsl_rr(st) >> 32);
+        } else {
           r.has_uint32 = 0;
-          dd -= 1;
+          r.uinteger = 0;
         }
-        if (dd > 0) {
-          const unsigned long long outs = (unsigned long long)((dd + 1) / 2);
-          const U128 st = pcg_jump(*a.jump, r0.s, outs);
-          r.s = st;
-          if (dd & 1) {
-            r.has_uint32 = 1;
-            r.uinteger = (unsigned int)(xsl_rr(st) >> 32);
-          } else {
-            r.has_uint32 = 0;
-            r.uinteger = 0;
-          }
-        }
-        *a.rng = r;
       }
+      *a.rng = r;
     }
   }
+}
+
+__global__ void k_seg_init(long long* pos, long long* anchor) {
+  pos[0] = 0;
+  anchor[0] = kAnchorSlack;
 }
 
 }  // namespace bb

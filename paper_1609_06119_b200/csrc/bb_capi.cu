@@ -199,24 +199,27 @@ struct FitShape {
 };
 
 template <typename CodeT, typename NodeT>
-static HistPlan plan_layer(int layer, const FitShape& s, int sm_count) {
+static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, bool sib_ok = true) {
   HistPlan p{};
+  p.prof = getenv("BB_HIST_PROFILE") ? atoi(getenv("BB_HIST_PROFILE")) : 0;
   p.nodes = 1 << (layer - 1);
   p.start = p.nodes - 1;
+  p.sib = (sib_ok && layer >= 2) ? 1 : 0;  // left children only; right = parent - left (k_split)
+  const int built = p.sib ? p.nodes / 2 : p.nodes;
   constexpr int64_t kSmemMax = 227 * 1024 - 1024;
   const int64_t hist_budget = 96 * 1024;
   const int64_t fn_budget = std::max<int64_t>(1, hist_budget / ((int64_t)s.B * 8));
-  if (p.nodes <= fn_budget) {
-    p.ngs = p.nodes;
+  if (built <= fn_budget) {
+    p.ngs = built;
     p.n_ng = 1;
-    const int fg = (int)std::min<int64_t>(s.d, fn_budget / p.nodes);
+    const int fg = (int)std::min<int64_t>(s.d, fn_budget / built);
     p.n_fg = (int)ceil_div(s.d, fg);
     p.fg = (int)ceil_div(s.d, p.n_fg);
   } else {
     p.fg = 1;
     p.n_fg = s.d;
     p.ngs = (int)fn_budget;
-    p.n_ng = (int)ceil_div(p.nodes, p.ngs);
+    p.n_ng = (int)ceil_div(built, p.ngs);
   }
   const int tile = kTile;
   auto need = [&](int fg) {
@@ -575,7 +578,7 @@ template <typename CodeT, typename NodeT>
 static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, int code_off,
                       const double* w_cb, double f0, int shift, const bb_fit_config& cfg,
                       const bb_forced_cut* forced, int n_forced, const double* bounds_dev, bb_fit_out* out,
-                      double* t_trees_ms, FitStats& stats, const Shard& shard) {
+                      double* t_trees_ms, FitStats& stats, const Shard& shard, bool any_nan) {
   const int64_t n = s.n;
   cudaStream_t st = c.stream;
   const double two_s = std::ldexp(1.0, shift), scale = std::ldexp(1.0, -shift);
@@ -590,8 +593,11 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   unsigned int* mask_slots = A.alloc<unsigned int>((size_t)words * kSlots);
   const bool host_masks = (cfg.flags & 2) != 0 && !shard.dist;
   const int max_nodes = 1 << (s.depth - 1);
-  unsigned long long* hist = A.alloc<unsigned long long>((size_t)2 * max_nodes * s.d * s.B);
-  BB_CUDA(cudaMemsetAsync(hist, 0, (size_t)2 * max_nodes * s.d * s.B * 8, st));
+  // two layer histograms: the current layer's and its parent layer's (sibling
+  // subtraction); both all-zero between trees
+  unsigned long long* hist2 = A.alloc<unsigned long long>((size_t)4 * max_nodes * s.d * s.B);
+  BB_CUDA(cudaMemsetAsync(hist2, 0, (size_t)4 * max_nodes * s.d * s.B * 8, st));
+  unsigned long long* hbuf[2] = {hist2, hist2 + (size_t)2 * max_nodes * s.d * s.B};
   unsigned long long* sums = A.alloc<unsigned long long>((size_t)2 * s.n_nodes * 2);
   BB_CUDA(cudaMemsetAsync(sums, 0, (size_t)2 * s.n_nodes * 2 * 8, st));
   TreeArrays ta;
@@ -630,7 +636,10 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   BB_LAUNCH_CHECK();
 
   std::vector<HistPlan> plans(s.depth + 1);
-  for (int l = 1; l <= s.depth; ++l) plans[l] = plan_layer<CodeT, NodeT>(l, s, c.sm_count);
+  // sibling subtraction needs parent = left + right: a row with a missing
+  // value at its node's cut feature stops at the node (trees.py:207-228), so
+  // it is used only for NaN-free data
+  for (int l = 1; l <= s.depth; ++l) plans[l] = plan_layer<CodeT, NodeT>(l, s, c.sm_count, !any_nan);
   BB_CUDA(cudaFuncSetAttribute(k_layer_hist<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
 
   // subsample bits: GPU generator on its own stream (default) or the host
@@ -676,6 +685,14 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   };
   auto cleanup = [&]() {
     if (ms) mgen.report(ms);
+    if (getenv("BB_HIST_PROFILE")) {
+      unsigned long long h[8];
+      cudaStreamSynchronize(st);
+      cudaMemcpyFromSymbol(h, g_hist_prof, sizeof(h));
+      fprintf(stderr, "hist prof (thread-cycles: wait compact bar1 atomics bar2 n):");
+      for (int q = 0; q < 6; ++q) fprintf(stderr, " %llu", h[q]);
+      fprintf(stderr, "\n");
+    }
     if (ms) {
       cudaStreamSynchronize(ms);
       cudaStreamDestroy(ms);
@@ -728,6 +745,8 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
       stats.launches += 1;
       for (int layer = 1; layer <= s.depth; ++layer) {
         const HistPlan& p = plans[layer];
+        unsigned long long* hist = hbuf[layer & 1];
+        unsigned long long* par = hbuf[(layer - 1) & 1];
         if (prof) hist_event();
         k_layer_hist<CodeT, NodeT><<<hist_grid(p), kHistThreads, p.smem, st>>>(codes, code_off, node, q, n, s.n_sig,
                                                                                s.d, s.B, p, hist);
@@ -742,9 +761,11 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         const int n_fc = (int)ceil_div(s.d, fc_size);
         k_split<256><<<dim3(nodes, n_fc), 256, 0, st>>>(hist, s.d, s.B, p.start, nodes, fc_size,
                                                        layer == s.depth ? 1 : 0, scale, t, s.n_internal, ta,
-                                                       bounds_dev, sc);
+                                                       bounds_dev, sc, par, p.sib,
+                                                       (layer < s.depth && plans[layer + 1].sib) ? 1 : 0);
         BB_LAUNCH_CHECK();
         const bool last = layer == s.depth;
+        if (last && p.sib) BB_CUDA(cudaMemsetAsync(hist, 0, (size_t)2 * nodes * s.d * s.B * 8, st));
         k_advance<CodeT, NodeT><<<gridA, 512, last ? (size_t)32 * s.n_nodes : 0, st>>>(
             codes, s.d, code_off, node, n, s.n_sig, p.start, t, s.n_internal, ta, last ? 1 : 0, s.n_nodes, q, mask,
             F, w_cb, two_s, sums);
@@ -945,9 +966,9 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
     BB_CUDA(cudaStreamSynchronize(st));
     ms_bin = elapsed_ms(t_bin);
     if (s.depth <= 7)
-      run_trees<CodeT, uint8_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees, stats, shard);
+      run_trees<CodeT, uint8_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees, stats, shard, any_nan);
     else
-      run_trees<CodeT, uint16_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees, stats, shard);
+      run_trees<CodeT, uint16_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees, stats, shard, any_nan);
   };
   if (B <= 255) {
     go(A.alloc<uint8_t>((size_t)d * stride), 0);
@@ -1220,7 +1241,7 @@ int bb_layer_hist(bb_ctx* ctx, const uint16_t* codes, const uint16_t* node, cons
     BB_CUDA(cudaMemcpyAsync(nd, node, (size_t)n * 2, cudaMemcpyHostToDevice, st));
     BB_CUDA(cudaMemcpyAsync(qd, q, (size_t)n * 8, cudaMemcpyHostToDevice, st));
     FitShape s{n, n_sig, d, levels, B, layer, 0, 0, 1};
-    const HistPlan p = plan_layer<uint16_t, uint16_t>(layer, s, c.sm_count);
+    const HistPlan p = plan_layer<uint16_t, uint16_t>(layer, s, c.sm_count, false);  // full layer
     const size_t hsz = (size_t)2 * p.nodes * d * B;
     unsigned long long* hist = A.alloc<unsigned long long>(hsz);
     BB_CUDA(cudaMemsetAsync(hist, 0, hsz * 8, st));
@@ -1272,7 +1293,7 @@ int bb_split(bb_ctx* ctx, const int64_t* hist, int32_t d, int32_t levels, int32_
     const int fc_size = (int)ceil_div(d, n_fc_want);
     const int n_fc = (int)ceil_div(d, fc_size);
     k_split<256><<<dim3(nodes, n_fc), 256, 0, st>>>(hd, d, B, start, nodes, fc_size, final_layer, std::ldexp(1.0, -shift),
-                                                   0, n_internal, ta, bd, sc);
+                                                   0, n_internal, ta, bd, sc, nullptr, 0, 0);
     BB_LAUNCH_CHECK();
     BB_CUDA(cudaMemcpyAsync(out_valid, ta.valid + start, nodes, cudaMemcpyDeviceToHost, st));
     BB_CUDA(cudaMemcpyAsync(out_feature, ta.feature + start, (size_t)nodes * 4, cudaMemcpyDeviceToHost, st));

@@ -100,9 +100,14 @@ struct HistPlan {
   int tiles_sig0, tiles_sig1, tiles_bkg0, tiles_bkg1;  // tile ranges per class
   int split_sig, split_bkg;  // CTAs per group per class
   int smem;                  // dynamic shared memory bytes
+  int prof;                  // debug (BB_HIST_PROFILE=1): thread 0's per-phase cycles into g_hist_prof
+  int sib;                   // 1: build left children only (right = parent - left in k_split)
 };
 
+__device__ unsigned long long g_hist_prof[8];
+
 constexpr int kHistThreads = 512;
+constexpr int kHistFlushTiles = 1 << 20;  // 2-limb slots are exact int64 sums (no periodic flush needed)
 
 __host__ __device__ __forceinline__ int align16(int x) { return (x + 15) & ~15; }
 
@@ -142,7 +147,8 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   const int f0 = fgi * p.fg;
   const int fcount = min(p.fg, d - f0);
   const int n0 = ngi * p.ngs;
-  const int ncount = min(p.ngs, p.nodes - n0);
+  const int built = p.sib ? p.nodes >> 1 : p.nodes;  // histogram nodes built by this launch
+  const int ncount = min(p.ngs, built - n0);
   const int nslots = ncount * fcount * B;
   const int tile = p.tile;
   uint32_t* lo = reinterpret_cast<uint32_t*>(smem);
@@ -174,15 +180,35 @@ __global__ void __launch_bounds__(kHistThreads, 1)
     tma_load_1d(cb, codes + ((int64_t)k * d + f0) * kTile, fcount * kTile * sizeof(CodeT), &bar[buf]);
   };
 
+  // smem slots -> global int64 histogram (value = l sum + h sum * 2^16)
+  auto flush = [&](bool zero) {
+    for (int s = threadIdx.x; s < nslots; s += kHistThreads) {
+      const long long v = (long long)(((unsigned long long)hi[s] << 32) | (unsigned long long)lo[s]);
+      if (zero) {
+        lo[s] = 0u;
+        hi[s] = 0u;
+      }
+      if (v != 0) {
+        const int bb = s % B;
+        const int j = (s / B) % fcount;
+        const int nd = s / (B * fcount);
+        const int ln = p.sib ? 2 * (n0 + nd) : (n0 + nd);
+        const int64_t g = (((int64_t)cls * p.nodes + ln) * d + (f0 + j)) * B + bb;
+        atomicAdd(&hist[g], as_ull(v));
+      }
+    }
+  };
   if (threadIdx.x == 0 && ta < tb) issue(ta, 0);
-  const int start = p.start + n0;
   for (int k = ta; k < tb; ++k) {
     const int it = k - ta, buf = it & 1;
     if (threadIdx.x == 0) {
       if (k + 1 < tb) issue(k + 1, buf ^ 1);
       counter[(it + 1) & 1] = 0;
     }
+    const bool pf = (p.prof & 1) && threadIdx.x == 0;
+    const long long t0 = pf ? clock64() : 0;
     mbar_wait(&bar[buf], (it >> 1) & 1);
+    const long long t1 = pf ? clock64() : 0;
     const unsigned char* b = stage + buf * bufb;
     const NodeT* nt = reinterpret_cast<const NodeT*>(b);
     const long long* qt = reinterpret_cast<const long long*>(b + align16(tile * (int)sizeof(NodeT)));
@@ -191,69 +217,79 @@ __global__ void __launch_bounds__(kHistThreads, 1)
     // compaction of contributing rows (order irrelevant: integer sums)
     for (int rl = threadIdx.x; rl < tile; rl += kHistThreads) {
       const int64_t r = row0 + rl;
-      const int nd = (int)nt[rl] - start;
-      const bool ok = r >= clo && r < chi && nd >= 0 && nd < ncount && qt[rl] != 0;
+      const int ln = (int)nt[rl] - p.start;  // node within the layer
+      const int nd = (p.sib ? (ln >> 1) : ln) - n0;
+      const bool ok = r >= clo && r < chi && ln >= 0 && ln < p.nodes && !(p.sib && (ln & 1)) && nd >= 0 &&
+                      nd < ncount && qt[rl] != 0;
       const unsigned m = __ballot_sync(0xffffffffu, ok);
       int base = 0;
       if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&counter[it & 1], __popc(m));
       base = __shfl_sync(0xffffffffu, base, 0);
       if (ok) list[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = (uint32_t)rl | ((uint32_t)nd << 16);
     }
+    const long long t2 = pf ? clock64() : 0;
     __syncthreads();
+    const long long t3 = pf ? clock64() : 0;
     const int n_act = counter[it & 1];
-    // balanced work: items (row, block of 4 features), 4 independent lo-limb
-    // atomics in flight per item, carries resolved afterwards
-    const int nfb = (fcount + 3) >> 2;
-    const int items = n_act * nfb;
-    int a = 0, jb = 0;
-    if (threadIdx.x < items) {
-      jb = threadIdx.x / n_act;
-      a = threadIdx.x - jb * n_act;
-    }
-    for (int w = threadIdx.x; w < items; w += kHistThreads) {
-      const uint32_t e = list[a];
+    // one thread per compacted row, looping over the group's features: the
+    // row's node and q are read once and every code load is independent.
+    // Each update is one returning u32 add on the low limb (8 in flight)
+    // plus an add of the high word and carry on the high limb when nonzero:
+    // the fewest shared-memory wavefronts per update (bank conflicts make
+    // each warp-wide atomic ~3.5 wavefronts).  A missing code (NaN bin) goes
+    // to this lane's dummy slot (nslots + lane), never read.
+    const int dummy = nslots + (threadIdx.x & 31);
+    for (int ai = threadIdx.x; ai < n_act; ai += kHistThreads) {
+      const uint32_t e = list[ai];
       const int rl = (int)(e & 0xffffu);
       const int nd = (int)(e >> 16);
       const long long qq = qt[rl];
       const uint32_t l = (uint32_t)(unsigned long long)qq;
       const uint32_t h = (uint32_t)((unsigned long long)qq >> 32);
-      const int j0 = jb * 4;
-      const int sb = (nd * fcount + j0) * B - 1;
-      // missing codes / padding features go to this lane's dummy slot
-      // (nslots + lane), never read: the lo-limb atomic is unconditional
-      int sl[4];
-      uint32_t old[4];
+      const int sb = nd * fcount * B - 1 + code_off;
+      const CodeT* cp = ct + rl;
+      int j = 0;
+      for (; j + 8 <= fcount; j += 8) {
+        int sl[8];
+        uint32_t old[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = j0 + u;
-        const int c = (j < fcount) ? (int)ct[j * tile + rl] + code_off : 0;
-        sl[u] = (c != 0) ? sb + u * B + c : nslots + (threadIdx.x & 31);
+        for (int u = 0; u < 8; ++u) {
+          const int c = (int)cp[(j + u) * kTile];
+          sl[u] = (c + code_off != 0) ? sb + (j + u) * B + c : dummy;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) old[u] = atomicAdd(lo + sl[u], l);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t hh = h + ((old[u] + l < old[u]) ? 1u : 0u);
+          if (hh) atomicAdd(hi + sl[u], hh);
+        }
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) old[u] = atomicAdd(lo + sl[u], l);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t hh = h + ((old[u] + l < old[u]) ? 1u : 0u);
-        if (hh) atomicAdd(hi + sl[u], hh);
-      }
-      a += kHistThreads;
-      while (a >= n_act && n_act > 0) {
-        a -= n_act;
-        ++jb;
+      for (; j < fcount; ++j) {
+        const int c = (int)cp[j * kTile];
+        const int sl = (c + code_off != 0) ? sb + j * B + c : dummy;
+        const uint32_t o = atomicAdd(lo + sl, l);
+        const uint32_t hh = h + ((o + l < o) ? 1u : 0u);
+        if (hh) atomicAdd(hi + sl, hh);
       }
     }
+    const long long t4 = pf ? clock64() : 0;
     __syncthreads();
-  }
-  for (int s = threadIdx.x; s < nslots; s += kHistThreads) {
-    const long long v = (long long)(((unsigned long long)hi[s] << 32) | (unsigned long long)lo[s]);
-    if (v != 0) {
-      const int bb = s % B;
-      const int j = (s / B) % fcount;
-      const int nd = s / (B * fcount);
-      const int64_t g = (((int64_t)cls * p.nodes + (n0 + nd)) * d + (f0 + j)) * B + bb;
-      atomicAdd(&hist[g], as_ull(v));
+    if (pf) {
+      const long long t5 = clock64();
+      atomicAdd(&g_hist_prof[0], (unsigned long long)(t1 - t0));  // TMA wait
+      atomicAdd(&g_hist_prof[1], (unsigned long long)(t2 - t1));  // compaction
+      atomicAdd(&g_hist_prof[2], (unsigned long long)(t3 - t2));  // barrier 1
+      atomicAdd(&g_hist_prof[3], (unsigned long long)(t4 - t3));  // atomics
+      atomicAdd(&g_hist_prof[4], (unsigned long long)(t5 - t4));  // barrier 2
+      atomicAdd(&g_hist_prof[5], 1ull);
+    }
+    if ((it & (kHistFlushTiles - 1)) == kHistFlushTiles - 1 && k + 1 < tb) {
+      flush(true);
+      __syncthreads();
     }
   }
+  flush(false);
 }
 
 // ---------------------------------------------------------------- split
@@ -285,8 +321,10 @@ template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restrict__ hist_u, int d, int B, int start,
                                                    int nodes, int fc_size, int final_layer, double scale, int tree,
                                                    int n_internal, TreeArrays ta, const double* __restrict__ bounds,
-                                                   SplitScratch sc) {
+                                                   SplitScratch sc, unsigned long long* __restrict__ par_u, int sib,
+                                                   int keep) {
   long long* hist = reinterpret_cast<long long*>(hist_u);
+  long long* par = reinterpret_cast<long long*>(par_u);  // previous layer [2][nodes/2][d][B] (sib)
   const int node = blockIdx.x;
   const int fci = blockIdx.y;
   const int n_fc = gridDim.y;
@@ -300,18 +338,52 @@ __global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restric
   int best_flat = 0x7fffffff;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int fbeg = fci * fc_size, fend = min(d, fbeg + fc_size);
+  // sibling subtraction (sib): the histogram launch built the left children
+  // only; a right child is its parent minus its left sibling (integer sums:
+  // exact), or empty if the parent was not split.  A right child's CTA
+  // zeroes the parent it consumed; a non-final layer keeps its histograms as
+  // the next layer's parents, a final one is cleared by the host (memset).
+  const bool right = sib && (node & 1);
+  const int pnode = node >> 1, pnodes = nodes >> 1;
+  const bool pvalid = right && ta.valid[(int64_t)tree * n_internal + ((start - 1) >> 1) + pnode] != 0;
   for (int f = fbeg; f < fend; ++f) {
     long long* hs = hist + ((int64_t)node * d + f) * B;
     long long* hb = hist + (((int64_t)nodes + node) * d + f) * B;
     long long vs[8], vb[8];
     long long ts = 0, tb = 0;
     const int c0 = threadIdx.x * per;
-    for (int j = 0; j < per; ++j) {
-      const int c = c0 + j;
-      vs[j] = (c < B) ? hs[c] : 0;
-      vb[j] = (c < B) ? hb[c] : 0;
-      ts += vs[j];
-      tb += vb[j];
+    if (right) {
+      long long* ls = hist + ((int64_t)(node - 1) * d + f) * B;
+      long long* lb = hist + (((int64_t)nodes + node - 1) * d + f) * B;
+      long long* ps = par + ((int64_t)pnode * d + f) * B;
+      long long* pb = par + (((int64_t)pnodes + pnode) * d + f) * B;
+      for (int j = 0; j < per; ++j) {
+        const int c = c0 + j;
+        vs[j] = 0;
+        vb[j] = 0;
+        if (c < B) {
+          if (pvalid) {
+            vs[j] = ps[c] - ls[c];
+            vb[j] = pb[c] - lb[c];
+          }
+          if (!final_layer) {  // the next layer's parent
+            hs[c] = vs[j];
+            hb[c] = vb[j];
+          }
+          ps[c] = 0;  // only this CTA reads the parent
+          pb[c] = 0;
+        }
+        ts += vs[j];
+        tb += vb[j];
+      }
+    } else {
+      for (int j = 0; j < per; ++j) {
+        const int c = c0 + j;
+        vs[j] = (c < B) ? hs[c] : 0;
+        vb[j] = (c < B) ? hb[c] : 0;
+        ts += vs[j];
+        tb += vb[j];
+      }
     }
     // block-wide exclusive scan of (ts, tb)
     long long is = ts, ib = tb;
@@ -343,10 +415,13 @@ __global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restric
       if (better(g, flat, best_g, best_flat)) { best_g = g; best_flat = flat; }
       if (fc >= 0 && (fc >> 16) == f && (fc & 0xffff) == c + 1) sc.forced_gain[node] = g;
     }
-    // consume then zero the histogram for the next layer
-    for (int j = 0; j < per; ++j) {
-      const int c = c0 + j;
-      if (c < B) { hs[c] = 0; hb[c] = 0; }
+    // without sibling subtraction a layer zeroes what it consumed, unless the
+    // next layer subtracts from it (keep)
+    if (!sib && !keep) {
+      for (int j = 0; j < per; ++j) {
+        const int c = c0 + j;
+        if (c < B) { hs[c] = 0; hb[c] = 0; }
+      }
     }
   }
   // block argmax

@@ -65,5 +65,23 @@ def full(path, out):
             fh.write(f"{h:70s} {v:.0f}\n")
 
 
+def traffic(path, out):
+    """dram bytes (read + write) per launch of the captured kernels -> JSON for bench.py's roofline"""
+    import json
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    hdr, units = rows[0], rows[1]
+    vals = []
+    for r in rows[2:]:
+        b = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v = float(r[hdr.index(m)].replace(",", ""))
+            u = units[hdr.index(m)]
+            b += v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+        vals.append(b)
+    json.dump({"source": path, "launches": len(vals), "dram_bytes_per_launch": sum(vals) / max(1, len(vals)),
+               "per_launch": vals}, open(out, "w"), indent=1)
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](sys.argv[2], sys.argv[3])

@@ -308,7 +308,11 @@ struct MaskGen {
   long long* stail = nullptr;    // chain -> tail hand-off: draw
   int* stail_i = nullptr;        //                         state
   cudaStream_t sb = nullptr;     // phase 1 / 3 stream (overlaps the tails)
+  cudaStream_t sc = nullptr;     // value resolution + mask bits (overlaps the next chunk's parse)
   cudaEvent_t evA = nullptr, evB = nullptr;
+  cudaEvent_t evT[kChunk] = {};  // tree t of the chunk emitted (sb -> sc)
+  cudaEvent_t evR[2] = {};       // resolution of the chunk that used J half p done (sc -> st)
+  int parity = 0;                // J buffer half of the current chunk
   RngState* rng0 = nullptr;
   bool legacy_cl = false;  // BB_CL_PARSE: the cluster parse instead
 
@@ -350,7 +354,7 @@ struct MaskGen {
     draws = A.alloc<unsigned int>((size_t)n_draws);
     const int nmax = std::max(n[0], n[1]);
     for (int cc = 0; cc < 2; ++cc) {
-      J[cc] = A.alloc<int>((size_t)std::max(1, std::max(n[0], n[1])) * chunk);  // stride = larger class
+      J[cc] = A.alloc<int>((size_t)std::max(1, std::max(n[0], n[1])) * chunk * 2);  // stride = larger class; 2 chunks
       removed[cc] = A.alloc<unsigned char>(std::max(1, n[cc]));
     }
     cnt = A.alloc<int>(nmax + 1);
@@ -397,6 +401,9 @@ struct MaskGen {
     BB_CUDA(cudaStreamCreateWithPriority(&sb, cudaStreamNonBlocking, hi_prio));
     BB_CUDA(cudaEventCreateWithFlags(&evA, cudaEventDisableTiming));
     BB_CUDA(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
+    BB_CUDA(cudaStreamCreateWithPriority(&sc, cudaStreamNonBlocking, hi_prio));
+    for (int q = 0; q < kChunk; ++q) BB_CUDA(cudaEventCreateWithFlags(&evT[q], cudaEventDisableTiming));
+    for (int q = 0; q < 2; ++q) BB_CUDA(cudaEventCreateWithFlags(&evR[q], cudaEventDisableTiming));
     rng0 = A.alloc<RngState>(1);
     BB_CUDA(cudaFuncSetAttribute(k_seg_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegPassSmem));
     BB_CUDA(cudaFuncSetAttribute(k_seg_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegComposeSmem));
@@ -406,8 +413,16 @@ struct MaskGen {
       cudaStreamSynchronize(sb);
       cudaStreamDestroy(sb);
     }
+    if (sc) {
+      cudaStreamSynchronize(sc);
+      cudaStreamDestroy(sc);
+    }
     if (evA) cudaEventDestroy(evA);
     if (evB) cudaEventDestroy(evB);
+    for (int q = 0; q < kChunk; ++q)
+      if (evT[q]) cudaEventDestroy(evT[q]);
+    for (int q = 0; q < 2; ++q)
+      if (evR[q]) cudaEventDestroy(evR[q]);
   }
   void report(cudaStream_t st) {
     if (!prof) return;
@@ -449,7 +464,7 @@ struct MaskGen {
         job.tab = tab[cc];
         job.tasks = tasks[cc];
         job.n_tasks = n_tasks[cc];
-        job.J = J[cc] + (size_t)t * stride;
+        job.J = J[cc] + (size_t)(parity * kChunk + t) * stride;
         job.pos_in = spos + jj;
         job.pos_out = spos + jj + 1;
         job.anchor_in = sanchor + jj;
@@ -481,6 +496,7 @@ struct MaskGen {
       BB_CUDA(cudaStreamWaitEvent(sb, evA, 0));
       pass(sb, make_job(jj + 1), job);
       BB_CUDA(cudaEventRecord(evB, sb));
+      if (jj & 1) BB_CUDA(cudaEventRecord(evT[jj >> 1], sb));  // both jobs of tree jj/2 emitted
       sa.func = job;
       sa.emit = SegJob{};
       k_seg_tail<<<1, 32, 0, st>>>(sa);
@@ -533,14 +549,23 @@ struct MaskGen {
       BB_LAUNCH_CHECK();
       launches += 1;
     } else {
+      BB_CUDA(cudaStreamWaitEvent(st, evR[parity], 0));  // J half free (no-op before its first use)
       launches += enqueue_seg(st, count);
     }
     launches += 1;
     const long long stride = single ? 0 : std::max(n[0], n[1]);
+    const bool seg = !single && !legacy_cl;
+    const int half = seg ? parity * kChunk : 0;
+    if (seg) parity ^= 1;
+    const cudaStream_t st_out = st;  // the ready events' stream for the legacy paths
     for (int t = 0; t < count; ++t) {
+      if (seg) {  // this tree's value resolution on sc, after its jobs' J are emitted
+        BB_CUDA(cudaStreamWaitEvent(sc, evT[t], 0));
+        st = sc;
+      }
       for (int cc = 0; cc < 2; ++cc) {
         const int nn = n[cc], kk = k[cc];
-        int* Jt = J[cc] + (size_t)t * stride;
+        int* Jt = J[cc] + (size_t)(half + t) * stride;
         // k == 0: nothing is active (position 0 is never a step target)
         BB_CUDA(cudaMemsetAsync(removed[cc], kk == 0 ? 1 : 0, (size_t)std::max(1, nn), st));
         if (kk == 0 || nn <= 1 || kk >= nn) continue;
@@ -571,6 +596,17 @@ struct MaskGen {
       }
       if (ready) BB_CUDA(cudaEventRecord(ready[t], st));
     }
+    if (seg) BB_CUDA(cudaEventRecord(evR[half / kChunk], sc));
+    (void)st_out;
+  }
+  // make `st` wait for everything the mask streams have enqueued
+  void join(cudaStream_t st) {
+    if (!sc) return;
+    cudaEvent_t e;
+    BB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    BB_CUDA(cudaEventRecord(e, sc));
+    BB_CUDA(cudaStreamWaitEvent(st, e, 0));
+    BB_CUDA(cudaEventDestroy(e));
   }
 };
 
@@ -727,7 +763,10 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
       cudaEvent_t evs[kChunk];
       for (int j = 0; j < cnt; ++j) {
         const int slot = (t + j) % kSlots;
-        if (t + j >= kSlots) BB_CUDA(cudaStreamWaitEvent(ms, freed[slot], 0));
+        if (t + j >= kSlots) {
+          BB_CUDA(cudaStreamWaitEvent(ms, freed[slot], 0));
+          if (mgen.sc) BB_CUDA(cudaStreamWaitEvent(mgen.sc, freed[slot], 0));
+        }
         bits[j] = mask_slots + (size_t)slot * words;
         evs[j] = ready[slot];
       }
@@ -1346,6 +1385,7 @@ int bb_subsample_masks_gpu(bb_ctx* ctx, int64_t n_sig, int64_t n_bkg, double rat
         mg.enqueue_chunk(st, bp, cnt, nullptr, launches);
       }
     }
+    mg.join(st);
     if (words) BB_CUDA(cudaMemcpyAsync(out_bits, bits, (size_t)words * n_trees * 4, cudaMemcpyDeviceToHost, st));
     BB_CUDA(cudaStreamSynchronize(st));
     mg.report(st);

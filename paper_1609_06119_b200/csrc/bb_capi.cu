@@ -490,7 +490,7 @@ struct MaskGen {
       const SegJob job = make_job(jj);
       sa.func = job;
       sa.emit = SegJob{};
-      k_seg_chain<<<1, 32, kSegComposeSmem, st>>>(sa);
+      k_seg_chain<<<1, 64, kSegComposeSmem, st>>>(sa);
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaEventRecord(evA, st));
       BB_CUDA(cudaStreamWaitEvent(sb, evA, 0));

@@ -579,37 +579,92 @@ struct StageWalk {
   }
 };
 
-// phase 2a: one warp.  From the job's exact first draw, walk to the first
-// segment (the anchor), then chain the segments' functions down to
-// kSegTail; hand the tail's (draw, state) to k_seg_tail and predict the next
-// job's first draw (its anchor) so its phase 1 can run during the tail.
-__global__ void __launch_bounds__(32) k_seg_chain(SegArgs a) {
+// phase 2a: two warps.  Warp 1 (producer) streams the table entries and
+// the segments' records into shared memory with bulk copies (full/empty
+// mbarriers per record slot) and prefetches the draws of band-crossing-zone
+// segments into L2.  Warp 0 (consumer) walks from the job's exact first draw
+// to the anchor, then chains the segments' functions down to kSegTail (an
+// O(1) lookup per segment; a start the records cannot answer is walked
+// exactly), hands the tail's (draw, state) to k_seg_tail and predicts the
+// next job's first draw (its anchor) so its phase 1 can run during the tail.
+__global__ void __launch_bounds__(64) k_seg_chain(SegArgs a) {
   extern __shared__ __align__(16) unsigned char cs_sm[];
   SegRec* ring = reinterpret_cast<SegRec*>(cs_sm);  // [kSegRing][kSegMaxSub]
   SegTab* tring = reinterpret_cast<SegTab*>(cs_sm + (size_t)kSegRing * kSegMaxSub * sizeof(SegRec));
   unsigned int* sd = reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned char*>(tring) +
                                                     (size_t)kTabChunk * kTabChunks * sizeof(SegTab));
-  __shared__ __align__(8) uint64_t tab_bar[kTabChunks], rec_bar[kSegRing], st_bar;
-  const int lane = threadIdx.x;
+  __shared__ SegTab slot_tab[kSegRing];  // the table entry of the segment in each record slot
+  __shared__ __align__(8) uint64_t tab_bar[kTabChunks], full_bar[kSegRing], empty_bar[kSegRing], st_bar;
+  __shared__ int s_s0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const SegJob& jb = a.func;
   const RngState r0 = *a.rng0;
   const long long p0 = *jb.pos_in;
   const long long anc = *jb.anchor_in;
   const int S = jb.S;
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     for (int q = 0; q < kTabChunks; ++q) mbar_init(&tab_bar[q], 1);
-    for (int q = 0; q < kSegRing; ++q) mbar_init(&rec_bar[q], 1);
+    for (int q = 0; q < kSegRing; ++q) {
+      mbar_init(&full_bar[q], 1);
+      mbar_init(&empty_bar[q], 1);
+    }
     mbar_init(&st_bar, 1);
     fence_mbar_init();
+    // first segment at or after the true first draw (segment 0 unless the job
+    // started more than kAnchorSlack draws late); earlier ones are skipped
+    int s0 = 0;
+    while (s0 < S && anc + jb.tab[s0].off < p0) ++s0;
+    s_s0 = s0;
   }
-  __syncwarp();
+  __syncthreads();
+  const int s0 = s_s0;
+  if (warp == 1) {
+    // ---- producer
+    int tab_waited = -1;
+    auto tab_issue = [&](int c) {
+      const int first = c * kTabChunk, cnt = min(kTabChunk, S - first);
+      if (cnt > 0 && lane == 0) {
+        uint64_t* bar = &tab_bar[c % kTabChunks];
+        mbar_expect_tx(bar, (unsigned)cnt * (unsigned)sizeof(SegTab));
+        tma_load_1d(tring + (c % kTabChunks) * kTabChunk, jb.tab + first, (unsigned)cnt * (unsigned)sizeof(SegTab),
+                    bar);
+      }
+    };
+    if (s0 < S) {
+      tab_issue(0);
+      tab_issue(1);
+    }
+    for (int q = s0; q < S; ++q) {
+      const int rq = q - s0, slot = rq % kSegRing;
+      if (rq >= kSegRing) mbar_wait(&empty_bar[slot], (unsigned)(((rq / kSegRing) - 1) & 1));
+      const int c = q / kTabChunk;
+      while (tab_waited < c) {
+        ++tab_waited;
+        mbar_wait(&tab_bar[tab_waited % kTabChunks], (unsigned)((tab_waited / kTabChunks) & 1));
+        tab_issue(tab_waited + 2);  // its slot held chunk tab_waited - 2 (the consumer is past it)
+      }
+      const SegTab& t = tring[q % (kTabChunk * kTabChunks)];
+      if (lane < 12) reinterpret_cast<int*>(&slot_tab[slot])[lane] = reinterpret_cast<const int*>(&t)[lane];
+      __syncwarp();
+      if (lane == 0) {
+        if (t.len <= kSegCrossLen) seg_prefetch_l2(a.draws, anc + t.off, t.len, a.n_draws);  // likely walked
+        const unsigned bytes = (unsigned)(t.nA + t.nB) * (unsigned)sizeof(SegRec);
+        mbar_expect_tx(&full_bar[slot], bytes);  // release: slot_tab visible to the consumer
+        tma_load_1d(ring + slot * kSegMaxSub, a.rec + t.rec_off, bytes, &full_bar[slot]);
+      }
+    }
+    // drain the table chunks still in flight
+    if (s0 < S) {
+      const int last_chunk = min((S - 1) / kTabChunk, tab_waited + 2);
+      for (int c = tab_waited + 1; c <= last_chunk; ++c)
+        mbar_wait(&tab_bar[c % kTabChunks], (unsigned)((c / kTabChunks) & 1));
+    }
+    return;
+  }
+  // ---- consumer (warp 0)
   StageWalk walk{sd, &st_bar, 0u};
   long long c_resim = 0, n_resim = 0;
   const long long c_start = clock64();
-  // first segment at or after the true first draw (segment 0 unless the job
-  // started more than kAnchorSlack draws late); earlier segments are skipped
-  int s0 = 0;
-  while (s0 < S && anc + jb.tab[s0].off < p0) ++s0;
   for (int q = lane; q < s0; q += 32) a.seg_start[q] = -1;
   int i = jb.n - 1;
   long long p = p0;
@@ -618,48 +673,12 @@ __global__ void __launch_bounds__(32) k_seg_chain(SegArgs a) {
     i = walk(a, r0, p0, anc + jb.tab[s0].off - p0, i, jb.k, jb.J, lane, &used);  // n-1 >= kSegTail: never ends the job
     p = anc + jb.tab[s0].off;
   }
-  // records and table entries stream in with bulk copies; segment q uses
-  // record slot (q - s0) % kSegRing
-  int tab_waited = -1;
-  auto tab_issue = [&](int c) {
-    const int first = c * kTabChunk, cnt = min(kTabChunk, S - first);
-    if (cnt > 0 && lane == 0) {
-      uint64_t* bar = &tab_bar[c % kTabChunks];
-      mbar_expect_tx(bar, (unsigned)cnt * (unsigned)sizeof(SegTab));
-      tma_load_1d(tring + (c % kTabChunks) * kTabChunk, jb.tab + first, (unsigned)cnt * (unsigned)sizeof(SegTab), bar);
-    }
-  };
-  auto tab_need = [&](int q) {
-    const int c = q / kTabChunk;
-    while (tab_waited < c) {
-      ++tab_waited;
-      mbar_wait(&tab_bar[tab_waited % kTabChunks], (unsigned)((tab_waited / kTabChunks) & 1));
-      tab_issue(tab_waited + 2);  // its slot held chunk tab_waited - 2
-    }
-  };
-  auto issue = [&](int q) {
-    if (q < S) {
-      tab_need(q);
-      const SegTab& t = tring[q % (kTabChunk * kTabChunks)];
-      if (lane == 0) {
-        uint64_t* bar = &rec_bar[(q - s0) % kSegRing];
-        const unsigned bytes = (unsigned)(t.nA + t.nB) * (unsigned)sizeof(SegRec);
-        mbar_expect_tx(bar, bytes);
-        tma_load_1d(ring + ((q - s0) % kSegRing) * kSegMaxSub, a.rec + t.rec_off, bytes, bar);
-      }
-    }
-  };
   int s = s0;
-  if (s0 < S) {
-    tab_issue(0);
-    tab_issue(1);
-    for (int q = s0; q < s0 + kSegRing; ++q) issue(q);
-  }
   for (; s < S && i >= kSegTail; ++s) {
-    const int rs = s - s0;
-    mbar_wait(&rec_bar[rs % kSegRing], (unsigned)((rs / kSegRing) & 1));
+    const int rs = s - s0, slot = rs % kSegRing;
+    mbar_wait(&full_bar[slot], (unsigned)((rs / kSegRing) & 1));
     if (lane == 0) a.seg_start[s] = i;
-    const SegTab& t = tring[s % (kTabChunk * kTabChunks)];
+    const SegTab& t = slot_tab[slot];
     int j = -1, lo = 0;
     if (i >= t.loA && i <= t.hiA) {
       j = (i - t.loA) / kSub;
@@ -670,7 +689,7 @@ __global__ void __launch_bounds__(32) k_seg_chain(SegArgs a) {
     }
     int next = -1;
     if (j >= 0) {
-      const SegRec& R = ring[(rs % kSegRing) * kSegMaxSub + j];
+      const SegRec& R = ring[slot * kSegMaxSub + j];
       const int r = i - lo, w = r >> 5, bt = r & 31;
       const unsigned int m = bt == 31 ? 0xffffffffu : ((2u << bt) - 1u);
       const int e = R.a_end + (int)R.pref[w] + __popc(R.words[w] & m);
@@ -678,7 +697,7 @@ __global__ void __launch_bounds__(32) k_seg_chain(SegArgs a) {
     }
     const int off = t.off, len = t.len;
     __syncwarp();
-    issue(s + kSegRing);
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty_bar[slot])) : "memory");
     if (next < 0) {
       // exact walk (band crossing inside the segment, or a window miss); the
       // J values are emitted by phase 3
@@ -691,13 +710,12 @@ __global__ void __launch_bounds__(32) k_seg_chain(SegArgs a) {
     i = next;
     p = anc + off + len;
   }
-  if (s0 < S) {
-    // drain the bulk copies still in flight
-    for (int q = s; q < min(S, s + kSegRing); ++q)
-      mbar_wait(&rec_bar[(q - s0) % kSegRing], (unsigned)(((q - s0) / kSegRing) & 1));
-    const int last_chunk = min((S - 1) / kTabChunk, tab_waited + 2);
-    for (int c = tab_waited + 1; c <= last_chunk; ++c)
-      mbar_wait(&tab_bar[c % kTabChunks], (unsigned)((c / kTabChunks) & 1));
+  // let the producer finish: consume (release) the slots it still fills
+  for (int q = s; q < S; ++q) {
+    const int rq = q - s0, slot = rq % kSegRing;
+    mbar_wait(&full_bar[slot], (unsigned)((rq / kSegRing) & 1));
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty_bar[slot])) : "memory");
   }
   if (lane == 0) {
     *a.n_seg = s;

@@ -240,7 +240,8 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, bool sib_
   // one CTA per SM, leaving kCl + 1 SMs to the concurrent mask-generation
   // stream (its cluster parse kernel holds kCl SMs for the whole tree)
   const int groups = p.n_fg * p.n_ng;
-  const int total = std::max(2, (int)((sm_count - kCl - 1) / groups));
+  static const int reserve = getenv("BB_HIST_RESERVE") ? atoi(getenv("BB_HIST_RESERVE")) : kCl + 1;
+  const int total = std::max(2, (int)((sm_count - reserve) / groups));
   const int ts = p.tiles_sig1 - p.tiles_sig0, tb = p.tiles_bkg1 - p.tiles_bkg0;
   p.split_sig = std::max(1, std::min(ts, (int)std::llround((double)total * ts / (ts + tb))));
   p.split_bkg = std::max(1, std::min(tb, total - p.split_sig));
@@ -773,11 +774,23 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
       mgen.enqueue_chunk(ms, bits, cnt, evs, stats.launches);
       return cnt;
     };
+    const bool tl_on = getenv("BB_TIMELINE") != nullptr;  // debug: main-stream waits for masks
+    std::vector<cudaEvent_t> tl;
     for (int t = 0; t < s.T; ++t) {
       while (next_mask < s.T && next_mask < t + (host_masks ? 1 : kChunk + 1)) next_mask += produce(next_mask);
       const int slot = t % kSlots;
       unsigned int* mask = mask_slots + (size_t)slot * words;
+      if (tl_on) {
+        tl.emplace_back();
+        BB_CUDA(cudaEventCreate(&tl.back()));
+        BB_CUDA(cudaEventRecord(tl.back(), st));  // main stream done with tree t-1
+      }
       BB_CUDA(cudaStreamWaitEvent(st, ready[slot], 0));
+      if (tl_on) {
+        tl.emplace_back();
+        BB_CUDA(cudaEventCreate(&tl.back()));
+        BB_CUDA(cudaEventRecord(tl.back(), st));  // ... and tree t's mask ready
+      }
       k_update_refresh<NodeT><<<gridN, 256, 0, st>>>(n, s.n_sig, F, node, w_cb, q, mask,
                                                       t > 0 ? ta.nw + (size_t)(t - 1) * s.n_nodes : nullptr, two_s);
       BB_LAUNCH_CHECK();
@@ -830,6 +843,23 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
       BB_CUDA(cudaMemcpyAsync(out->scores, F, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
     }
     BB_CUDA(cudaStreamSynchronize(st));
+    if (tl_on && tl.size() >= 2) {
+      double wait = 0.0, busy = 0.0;
+      int waits = 0;
+      for (size_t k = 0; k + 1 < tl.size(); k += 2) {
+        float w = 0.f;
+        BB_CUDA(cudaEventElapsedTime(&w, tl[k], tl[k + 1]));
+        wait += w;
+        waits += w > 0.01f;
+        if (k + 2 < tl.size()) {
+          float b = 0.f;
+          BB_CUDA(cudaEventElapsedTime(&b, tl[k + 1], tl[k + 2]));
+          busy += b;
+        }
+      }
+      fprintf(stderr, "timeline: main stream waited %.2f ms for masks (%d trees), busy %.2f ms\n", wait, waits, busy);
+      for (auto e : tl) cudaEventDestroy(e);
+    }
     for (size_t k = 0; k + 1 < hev.size(); k += 2) {
       float msf = 0.f;
       BB_CUDA(cudaEventElapsedTime(&msf, hev[k], hev[k + 1]));

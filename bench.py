@@ -394,7 +394,8 @@ def run_b200(args, rank, world, local):
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
-            "breakdown_ms": {"mask_host_per_fit": statistics.mean(mask_ms), "wall_per_fit": 1e3 * statistics.mean(wall)},
+            "breakdown_ms": {"mask_host_per_fit": statistics.mean(mask_ms), "wall_per_fit": 1e3 * statistics.mean(wall),
+                             "device_per_fit": [round(x, 2) for x in dev_ms]},
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

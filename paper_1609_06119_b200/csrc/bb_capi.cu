@@ -1115,6 +1115,13 @@ int bb_ctx_create(int32_t device, bb_ctx** out) {
       BB_CUDA(cudaSetDevice(device));
       BB_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
       BB_CUDA(cudaDeviceGetAttribute(&h->c.sm_count, cudaDevAttrMultiProcessorCount, device));
+      // keep freed stream-ordered allocations cached in the device pool: the
+      // default threshold (0) returns them to the OS at every synchronisation,
+      // so each call would re-map its buffers inside the work it times
+      cudaMemPool_t pool;
+      BB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = UINT64_MAX;
+      BB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     } catch (...) {
       delete h;
       throw;
@@ -1213,7 +1220,61 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
     const unsigned grid = (unsigned)ceil_div(n, APPLY_ROWS);
     const size_t smem = (size_t)APPLY_ROWS * (d + 1) * es;
     const size_t smem32 = ((size_t)kApplyRows * (d + 1) * 4 + 15) / 16 * 16 + (size_t)kApplyTB * (N * 8 + I * 8);
-    if (x_dtype == BB_F32 && smem32 <= 200 * 1024) {
+    const int D = fo->depth;
+    const size_t smemD = ((size_t)kApplyDRows * (d + 1) * 4 + 15) / 16 * 16 +
+                         (size_t)kApplyDTB * (((size_t)1 << D) * 8 + (size_t)I * 8);
+    if (x_dtype == BB_F32 && D >= 1 && D <= 6 && smemD <= 200 * 1024) {
+      // fixed-depth walk over leaf tables with the invalid-node stops folded in
+      std::vector<int2> hr(TI), hn(TI);
+      std::vector<double> hl((size_t)fo->n_trees << D);
+      for (int t = 0; t < fo->n_trees; ++t) {
+        for (int k = 0; k < I; ++k) {
+          const size_t e = (size_t)t * I + k;
+          const double th = fo->threshold[e];
+          float tf = (float)th;  // round-to-nearest, then step up if below th
+          if ((double)tf < th) tf = std::nextafter(tf, INFINITY);
+          int bits;
+          std::memcpy(&bits, &tf, 4);
+          hr[e] = make_int2(fo->valid[e] ? 4 * fo->feature[e] : 0, bits);
+          hn[e] = make_int2(fo->valid[e] ? fo->feature[e] : -1, bits);
+        }
+        for (int l = 0; l < (1 << D); ++l) {
+          int nd = 0, stop = -1;
+          for (int lv = 0; lv < D; ++lv) {
+            if (!fo->valid[(size_t)t * I + nd]) {
+              stop = nd;
+              break;
+            }
+            nd = 2 * nd + 1 + ((l >> (D - 1 - lv)) & 1);
+          }
+          hl[((size_t)t << D) + l] = fo->node_weight[(size_t)t * N + (stop >= 0 ? stop : nd)];
+        }
+      }
+      int2* rd = A.alloc<int2>(std::max<size_t>(1, TI));
+      int2* nd2 = A.alloc<int2>(std::max<size_t>(1, TI));
+      double* ld = A.alloc<double>(std::max<size_t>(1, hl.size()));
+      if (TI) {
+        BB_CUDA(cudaMemcpyAsync(rd, hr.data(), TI * sizeof(int2), cudaMemcpyHostToDevice, st));
+        BB_CUDA(cudaMemcpyAsync(nd2, hn.data(), TI * sizeof(int2), cudaMemcpyHostToDevice, st));
+      }
+      if (!hl.empty()) BB_CUDA(cudaMemcpyAsync(ld, hl.data(), hl.size() * 8, cudaMemcpyHostToDevice, st));
+      ApplyD ad{fo->n_trees, rd, ld, nd2, nw, fo->f0};
+      const unsigned gd = (unsigned)ceil_div(n, kApplyDRows);
+      auto launch = [&](auto kern) {
+        BB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        kern<<<gd, kApplyDRows, smemD, st>>>((const float*)Xd, n, d, ad, pd, fd);
+      };
+      switch (D) {
+        case 1: launch(k_apply_d<1>); break;
+        case 2: launch(k_apply_d<2>); break;
+        case 3: launch(k_apply_d<3>); break;
+        case 4: launch(k_apply_d<4>); break;
+        case 5: launch(k_apply_d<5>); break;
+        default: launch(k_apply_d<6>); break;
+      }
+      BB_LAUNCH_CHECK();
+      BB_CUDA(cudaStreamSynchronize(st));  // host staging vectors
+    } else if (x_dtype == BB_F32 && smem32 <= 200 * 1024) {
       // packed node records with float-ceiling thresholds (exact for float rows)
       std::vector<int2> hn(TI);
       for (size_t e = 0; e < TI; ++e) {

@@ -150,4 +150,107 @@ __global__ void __launch_bounds__(kApplyRows) k_apply_f32(const float* __restric
   }
 }
 
+// ------------------------------------------------------ f32, fixed depth
+// Depth-D trees with the invalid-node stops folded into a per-tree leaf
+// table: leaf l's weight is that of the first invalid node on its path (the
+// walk stops there, trees.py:333-346) or of the leaf node.  The walk is then
+// branch-free: D levels of (record, value, compare, child), one leaf-weight
+// add per tree in tree order (float64, bit-identical F).  A row with a NaN
+// feature stops where that NaN is tested, so it takes the exact per-node
+// walk over the original records (global memory; rare).
+constexpr int kApplyDRows = 256;
+constexpr int kApplyDTB = 64;  // trees per smem batch
+
+struct ApplyD {
+  int n_trees;
+  const int2* rec;    // [T][2^D - 1]: x = 4 * feature (byte offset; 0 for invalid), y = float bits of ceil_f32(thr)
+  const double* leaf; // [T][2^D]
+  const int2* node;   // [T][2^D - 1] original records (x = -1: invalid) for NaN rows
+  const double* nw;   // [T][2^(D+1) - 1]
+  double f0;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kApplyDRows) k_apply_d(const float* __restrict__ X, int64_t n, int d, ApplyD fo,
+                                                         double* __restrict__ out_p, double* __restrict__ out_F) {
+  constexpr int I = (1 << D) - 1, L = 1 << D, N = (1 << (D + 1)) - 1;
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int ld = d + 1;
+  float* tile = reinterpret_cast<float*>(s_raw);  // [kApplyDRows][ld]
+  unsigned char* after = s_raw + ((size_t)kApplyDRows * ld * 4 + 15) / 16 * 16;
+  double* s_leaf = reinterpret_cast<double*>(after);                           // [TB][L]
+  int2* s_rec = reinterpret_cast<int2*>(s_leaf + (size_t)kApplyDTB * L);      // [TB][I]
+  const int64_t row0 = (int64_t)blockIdx.x * kApplyDRows;
+  const int rows = (int)min((int64_t)kApplyDRows, n - row0);
+  const float* src = X + row0 * d;
+  for (int e = threadIdx.x; e < rows * d; e += kApplyDRows) {
+    const int r = e / d, f = e - r * d;
+    tile[r * ld + f] = src[e];
+  }
+  __syncthreads();
+  const float* row = tile + threadIdx.x * ld;
+  bool has_nan = false;
+  if ((int)threadIdx.x < rows)
+    for (int f = 0; f < d; ++f) has_nan |= row[f] != row[f];
+  double F = fo.f0;
+  if (has_nan) {
+    // exact per-node walk (the generic rule), original records in global memory
+    for (int t = 0; t < fo.n_trees; ++t) {
+      int nd = 0;
+      for (int l = 0; l < D; ++l) {
+        const int2 rc = __ldg(&fo.node[(int64_t)t * I + nd]);
+        if (rc.x < 0) break;
+        const float v = row[rc.x];
+        if (v != v) break;
+        nd = 2 * nd + 1 + (v >= __int_as_float(rc.y) ? 1 : 0);
+      }
+      F = __dadd_rn(F, __ldg(&fo.nw[(int64_t)t * N + nd]));
+    }
+  }
+  for (int tb = 0; tb < fo.n_trees; tb += kApplyDTB) {
+    const int nt = min(kApplyDTB, fo.n_trees - tb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nt * I; e += kApplyDRows) s_rec[e] = fo.rec[(int64_t)tb * I + e];
+    for (int e = threadIdx.x; e < nt * L; e += kApplyDRows) s_leaf[e] = fo.leaf[(int64_t)tb * L + e];
+    __syncthreads();
+    if (has_nan || (int)threadIdx.x >= rows) continue;
+    // byte offsets: records hold the feature's byte offset in the row, the
+    // node index walks as off = 8 * node (child: 2 off + 8 + 8 p)
+    const unsigned char* rb = reinterpret_cast<const unsigned char*>(row);
+    const unsigned char* recb = reinterpret_cast<const unsigned char*>(s_rec);
+    const unsigned char* leafb = reinterpret_cast<const unsigned char*>(s_leaf) - 8 * I;
+    int t = 0;
+    for (; t + 4 <= nt; t += 4) {
+      int off[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int l = 0; l < D; ++l) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int2 rc = *reinterpret_cast<const int2*>(recb + (t + u) * (8 * I) + off[u]);
+          const float v = *reinterpret_cast<const float*>(rb + rc.x);
+          off[u] = 2 * off[u] + 8 + (v >= __int_as_float(rc.y) ? 8 : 0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        F = __dadd_rn(F, *reinterpret_cast<const double*>(leafb + (t + u) * (8 * L) + off[u]));
+    }
+    for (; t < nt; ++t) {
+      int off = 0;
+#pragma unroll
+      for (int l = 0; l < D; ++l) {
+        const int2 rc = *reinterpret_cast<const int2*>(recb + t * (8 * I) + off);
+        const float v = *reinterpret_cast<const float*>(rb + rc.x);
+        off = 2 * off + 8 + (v >= __int_as_float(rc.y) ? 8 : 0);
+      }
+      F = __dadd_rn(F, *reinterpret_cast<const double*>(leafb + t * (8 * L) + off));
+    }
+  }
+  if ((int)threadIdx.x < rows) {
+    const int64_t i = row0 + threadIdx.x;
+    if (out_F) out_F[i] = F;
+    if (out_p) out_p[i] = sigmoid2(F);
+  }
+}
+
 }  // namespace bb

@@ -207,7 +207,7 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, bool sib_
   p.sib = (sib_ok && layer >= 2) ? 1 : 0;  // left children only; right = parent - left (k_split)
   const int built = p.sib ? p.nodes / 2 : p.nodes;
   constexpr int64_t kSmemMax = 227 * 1024 - 1024;
-  const int64_t hist_budget = 96 * 1024;
+  static const int64_t hist_budget = (getenv("BB_HIST_BUDGET_KB") ? atoi(getenv("BB_HIST_BUDGET_KB")) : 96) * 1024;
   const int64_t fn_budget = std::max<int64_t>(1, hist_budget / ((int64_t)s.B * 8));
   if (built <= fn_budget) {
     p.ngs = built;
@@ -237,11 +237,12 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, bool sib_
   p.tiles_sig1 = (int)ceil_div(s.n_sig, tile);
   p.tiles_bkg0 = (int)(s.n_sig / tile);
   p.tiles_bkg1 = (int)ceil_div(s.n, tile);
-  // one CTA per SM, leaving kCl + 1 SMs to the concurrent mask-generation
-  // stream (its cluster parse kernel holds kCl SMs for the whole tree)
+  // one CTA per SM, leaving 9 SMs to the concurrent mask streams (their
+  // chain / tail / pass CTAs need room while a histogram launch runs)
   const int groups = p.n_fg * p.n_ng;
-  static const int reserve = getenv("BB_HIST_RESERVE") ? atoi(getenv("BB_HIST_RESERVE")) : kCl + 1;
-  const int total = std::max(2, (int)((sm_count - reserve) / groups));
+  static const int reserve = getenv("BB_HIST_RESERVE") ? atoi(getenv("BB_HIST_RESERVE")) : 9;  // SMs left to the mask streams
+  const int per_sm = std::max(1, std::min(2, (int)((228 * 1024) / (p.smem + 2048))));  // resident CTAs per SM
+  const int total = std::max(2, (int)(per_sm * (sm_count - reserve) / groups));
   const int ts = p.tiles_sig1 - p.tiles_sig0, tb = p.tiles_bkg1 - p.tiles_bkg0;
   p.split_sig = std::max(1, std::min(ts, (int)std::llround((double)total * ts / (ts + tb))));
   p.split_bkg = std::max(1, std::min(tb, total - p.split_sig));
@@ -287,14 +288,10 @@ struct MaskGen {
   long long n_draws = 0;
   int* J[2] = {nullptr, nullptr};
   int *cnt = nullptr, *off = nullptr, *fill = nullptr, *bucket = nullptr, *sums = nullptr;
-  int *rec_pos = nullptr, *rec_i = nullptr, *rec_len = nullptr, *rec_count = nullptr;
-  unsigned char* rec_bits = nullptr;
-  int rec_cap = 0;
   long long* prof = nullptr;  // BB_PARSE_PROFILE: phase cycles, printed at the end
   unsigned char* removed[2] = {nullptr, nullptr};
   int n[2] = {0, 0}, k[2] = {0, 0};
   int sm = 148;
-  bool single = false;  // single-tree legacy parse kernels (debug env)
   Shard sh;                       // sh.dist: slice the global bits to this rank
   long long sh_n_local = 0;       // this rank's rows
   unsigned int* gbits = nullptr;  // global bits scratch (sharded fits)
@@ -315,12 +312,10 @@ struct MaskGen {
   cudaEvent_t evR[2] = {};       // resolution of the chunk that used J half p done (sc -> st)
   int parity = 0;                // J buffer half of the current chunk
   RngState* rng0 = nullptr;
-  bool legacy_cl = false;  // BB_CL_PARSE: the cluster parse instead
 
   void init(Arena& A, cudaStream_t st, int64_t n_sig, int64_t n_bkg, double rate, const bb_fit_config& cfg,
             int sm_count) {
     sm = sm_count;
-    single = getenv("BB_WARP_PARSE") || getenv("BB_CTA_PARSE");
     n[0] = (int)n_sig;
     n[1] = (int)n_bkg;
     k[0] = (int)subsample_count(n_sig, rate);
@@ -339,16 +334,13 @@ struct MaskGen {
     hr.inc = U128{cfg.pcg_inc_lo, cfg.pcg_inc_hi};
     hr.has_uint32 = cfg.pcg_has_uint32;
     hr.uinteger = cfg.pcg_uinteger;
-    BB_CUDA(cudaFuncSetAttribute(k_mask_parse, cudaFuncAttributeMaxDynamicSharedMemorySize, kRing * 4));
-    BB_CUDA(cudaFuncSetAttribute(k_mask_parse_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, kParseSmem));
-    BB_CUDA(cudaFuncSetAttribute(k_mask_parse_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, kClSmem));
     jump = A.alloc<PcgJump>(1);
     rng = A.alloc<RngState>(1);
     BB_CUDA(cudaMemcpyAsync(jump, &hj, sizeof(hj), cudaMemcpyHostToDevice, st));
     BB_CUDA(cudaMemcpyAsync(rng, &hr, sizeof(hr), cudaMemcpyHostToDevice, st));
     BB_CUDA(cudaStreamSynchronize(st));  // host staging structs go out of scope
     const int64_t steps = n_sig + n_bkg;
-    const int chunk = single ? 1 : kChunk;
+    const int chunk = kChunk;
     // E[draws/step] = mean of (mask+1)/(i+1) <= ~1.45 (2 ln 2 asymptotically) and < 2
     // always; beyond the buffer the parse falls back to per-draw jump-ahead
     n_draws = (long long)(2.0 * (double)steps * chunk) + 65536;
@@ -363,19 +355,11 @@ struct MaskGen {
     fill = A.alloc<int>(nmax + 1);
     bucket = A.alloc<int>(nmax + 1);
     sums = A.alloc<int>(ceil_div(nmax, kScanBlock) + 1);
-    rec_cap = single ? (int)(n_draws / 64 + 1024) : 1;
-    if (const char* e = getenv("BB_DEBUG_REC_CAP")) rec_cap = std::max(1, atoi(e));  // debug: force fallback
-    rec_pos = A.alloc<int>(rec_cap);
-    rec_i = A.alloc<int>(rec_cap);
-    rec_len = A.alloc<int>(rec_cap);
-    rec_count = A.alloc<int>(1);
-    rec_bits = A.alloc<unsigned char>((size_t)rec_cap * 32);
     if (getenv("BB_PARSE_PROFILE")) {
       prof = A.alloc<long long>(32);
       BB_CUDA(cudaMemsetAsync(prof, 0, 256, st));
     }
     gbits = A.alloc<unsigned int>((size_t)ceil_div(steps, 32) + 1);
-    legacy_cl = getenv("BB_CL_PARSE") != nullptr;
     int smax = 1, rmax = 1;
     for (int cc = 0; cc < 2; ++cc) {
       const SegPlan P = build_seg_plan(n[cc]);
@@ -515,55 +499,14 @@ struct MaskGen {
     const long long n_out = (n_draws + 1) / 2;
     k_pcg_draws<<<(unsigned)ceil_div(ceil_div(n_out, kDrawChunk), 256), 256, 0, st>>>(jump, rng, draws, n_draws);
     BB_LAUNCH_CHECK();
-    ParseArgs pa;
-    pa.draws = draws;
-    pa.n_draws = n_draws;
-    pa.jump = jump;
-    pa.rng = rng;
-    for (int cc = 0; cc < 2; ++cc) {
-      pa.n[cc] = n[cc];
-      pa.k[cc] = k[cc];
-      pa.J[cc] = J[cc];
-    }
-    pa.rec_pos = rec_pos;
-    pa.rec_i = rec_i;
-    pa.rec_len = rec_len;
-    pa.rec_bits = rec_bits;
-    pa.rec_count = rec_count;
-    pa.rec_cap = rec_cap;
-    pa.prof = prof;
-    pa.n_trees = count;
-    pa.J_stride = 0;  // set per class below via J offsets: tree t at J[c] + t * n[c]
-    if (single) {
-      if (getenv("BB_WARP_PARSE")) k_mask_parse<<<1, 32, kRing * 4, st>>>(pa);
-      else k_mask_parse_cta<<<1, kPT, kParseSmem, st>>>(pa);
-      BB_LAUNCH_CHECK();
-      k_expand_windows<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rec_cap, 8), 8 * sm)), 256, 0, st>>>(pa);
-      BB_LAUNCH_CHECK();
-      launches += 2;
-    } else if (legacy_cl) {
-      // one J stride for both classes: tree t of class c at J[c] + t * n[c];
-      // the kernel uses a single stride, so give each class its own launch
-      // argument via per-class base pointers and the larger stride
-      pa.J_stride = std::max(n[0], n[1]);
-      k_mask_parse_cl<<<kCl, kPT, kClSmem, st>>>(pa);
-      BB_LAUNCH_CHECK();
-      launches += 1;
-    } else {
-      BB_CUDA(cudaStreamWaitEvent(st, evR[parity], 0));  // J half free (no-op before its first use)
-      launches += enqueue_seg(st, count);
-    }
-    launches += 1;
-    const long long stride = single ? 0 : std::max(n[0], n[1]);
-    const bool seg = !single && !legacy_cl;
-    const int half = seg ? parity * kChunk : 0;
-    if (seg) parity ^= 1;
-    const cudaStream_t st_out = st;  // the ready events' stream for the legacy paths
+    BB_CUDA(cudaStreamWaitEvent(st, evR[parity], 0));  // J half free (no-op before its first use)
+    launches += enqueue_seg(st, count) + 1;
+    const long long stride = std::max(n[0], n[1]);
+    const int half = parity * kChunk;
+    parity ^= 1;
+    st = sc;  // value resolution and mask bits on their own stream
     for (int t = 0; t < count; ++t) {
-      if (seg) {  // this tree's value resolution on sc, after its jobs' J are emitted
-        BB_CUDA(cudaStreamWaitEvent(sc, evT[t], 0));
-        st = sc;
-      }
+      BB_CUDA(cudaStreamWaitEvent(sc, evT[t], 0));  // after this tree's jobs' J are emitted
       for (int cc = 0; cc < 2; ++cc) {
         const int nn = n[cc], kk = k[cc];
         int* Jt = J[cc] + (size_t)(half + t) * stride;
@@ -597,8 +540,7 @@ struct MaskGen {
       }
       if (ready) BB_CUDA(cudaEventRecord(ready[t], st));
     }
-    if (seg) BB_CUDA(cudaEventRecord(evR[half / kChunk], sc));
-    (void)st_out;
+    BB_CUDA(cudaEventRecord(evR[half / kChunk], sc));
   }
   // make `st` wait for everything the mask streams have enqueued
   void join(cudaStream_t st) {
@@ -759,7 +701,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         BB_CUDA(cudaEventRecord(ready[slot], st));
         return 1;
       }
-      const int cnt = std::min(mgen.single ? 1 : kChunk, s.T - t);
+      const int cnt = std::min(kChunk, s.T - t);
       unsigned int* bits[kChunk];
       cudaEvent_t evs[kChunk];
       for (int j = 0; j < cnt; ++j) {
@@ -1470,11 +1412,7 @@ int bb_subsample_masks_gpu(bb_ctx* ctx, int64_t n_sig, int64_t n_bkg, double rat
       const int cnt = std::min(kChunk, n_trees - t);
       unsigned int* bp[kChunk];
       for (int j = 0; j < cnt; ++j) bp[j] = bits + (size_t)(t + j) * words;
-      if (mg.single) {
-        for (int j = 0; j < cnt; ++j) mg.enqueue_chunk(st, &bp[j], 1, nullptr, launches);
-      } else {
-        mg.enqueue_chunk(st, bp, cnt, nullptr, launches);
-      }
+      mg.enqueue_chunk(st, bp, cnt, nullptr, launches);
     }
     mg.join(st);
     if (words) BB_CUDA(cudaMemcpyAsync(out_bits, bits, (size_t)words * n_trees * 4, cudaMemcpyDeviceToHost, st));

@@ -17,4 +17,4 @@ for r in range(a.reps):
     t0 = time.perf_counter()
     _lib.check(_lib.lib().bb_subsample_masks_gpu(_lib.context(), a.a, a.b, 0.5, a.trees, C.byref(cfg), _lib.ptr(bits)))
     dt = time.perf_counter() - t0
-    print(f"{os.environ.get('BB_CL_PARSE') and 'cluster' or 'segment'}: {a.trees} trees {dt*1e3:.1f} ms = {dt*1e3/a.trees:.3f} ms/tree")
+    print(f"masks: {a.trees} trees {dt*1e3:.1f} ms = {dt*1e3/a.trees:.3f} ms/tree")

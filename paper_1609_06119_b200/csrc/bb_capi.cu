@@ -393,6 +393,10 @@ struct MaskGen {
     BB_CUDA(cudaFuncSetAttribute(k_seg_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegPassSmem));
     BB_CUDA(cudaFuncSetAttribute(k_seg_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegComposeSmem));
   }
+  void sync() {
+    if (sb) cudaStreamSynchronize(sb);
+    if (sc) cudaStreamSynchronize(sc);
+  }
   ~MaskGen() {
     if (sb) {
       cudaStreamSynchronize(sb);
@@ -553,11 +557,117 @@ struct MaskGen {
   }
 };
 
+// Subsample bits of every tree, produced ahead of the fit into a ring of
+// kSlots mask buffers: the GPU generator on its own streams (default) or the
+// host restatement (flags bit 1).  Created before binning, so the first
+// chunk's parse overlaps it (the masks only need the class sizes).
+constexpr int kSlots = 2 * kChunk;
+
+struct MaskFeed {
+  cudaStream_t st = nullptr;  // the fit's stream
+  int64_t n = 0, n_sig = 0;
+  int T = 0;
+  bool host_masks = false;
+  int64_t words = 0;
+  double rate = 1.0;
+  unsigned int* slots = nullptr;  // [kSlots][words]
+  MaskGen mgen;
+  cudaStream_t ms = nullptr;
+  cudaEvent_t ready[kSlots] = {}, freed[kSlots] = {};
+  unsigned int* pinned[kSlots] = {};
+  Pcg64 g;
+  std::vector<uint32_t> perm;
+  int next = 0;
+  FitStats* stats = nullptr;
+
+  void init(Ctx& c, Arena& A, int64_t n_, int64_t n_sig_, const bb_fit_config& cfg, const Shard& shard,
+            FitStats* stats_) {
+    st = c.stream;
+    n = n_;
+    n_sig = n_sig_;
+    T = cfg.n_trees;
+    rate = cfg.subsample;
+    stats = stats_;
+    host_masks = (cfg.flags & 2) != 0 && !shard.dist;
+    words = ceil_div(n, 32);
+    slots = A.alloc<unsigned int>((size_t)words * kSlots);
+    g.state = ((unsigned __int128)cfg.pcg_state_hi << 64) | cfg.pcg_state_lo;
+    g.inc = ((unsigned __int128)cfg.pcg_inc_hi << 64) | cfg.pcg_inc_lo;
+    g.has_uint32 = cfg.pcg_has_uint32;
+    g.uinteger = cfg.pcg_uinteger;
+    for (int k = 0; k < kSlots; ++k) {
+      BB_CUDA(cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming));
+      BB_CUDA(cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming));
+    }
+    if (host_masks) {
+      for (int k = 0; k < kSlots; ++k) BB_CUDA(cudaMallocHost(&pinned[k], (size_t)words * 4));
+      return;
+    }
+    // the mask chain is the fit's critical path: highest stream priority
+    int prio_lo = 0, prio_hi = 0;
+    BB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    BB_CUDA(cudaStreamCreateWithPriority(&ms, cudaStreamNonBlocking, prio_hi));
+    if (shard.dist) {
+      mgen.init(A, st, shard.n_sig_g, shard.n_bkg_g, cfg.subsample, cfg, c.sm_count);
+      mgen.sh = shard;
+      mgen.sh_n_local = n;
+    } else {
+      mgen.init(A, st, n_sig, n - n_sig, cfg.subsample, cfg, c.sm_count);
+    }
+  }
+  // host path: one tree; GPU path: the chunk starting at t
+  int produce(int t) {
+    if (host_masks) {
+      const int slot = t % kSlots;
+      unsigned int* bits = slots + (size_t)slot * words;
+      if (t >= kSlots) BB_CUDA(cudaEventSynchronize(freed[slot]));
+      const auto tm = std::chrono::steady_clock::now();
+      subsample_tree(g, n_sig, n - n_sig, rate, pinned[slot], perm);
+      stats->mask_ms += elapsed_ms(tm);
+      BB_CUDA(cudaMemcpyAsync(bits, pinned[slot], (size_t)words * 4, cudaMemcpyHostToDevice, st));
+      BB_CUDA(cudaEventRecord(ready[slot], st));
+      return 1;
+    }
+    const int cnt = std::min(kChunk, T - t);
+    unsigned int* bits[kChunk];
+    cudaEvent_t evs[kChunk];
+    for (int j = 0; j < cnt; ++j) {
+      const int slot = (t + j) % kSlots;
+      if (t + j >= kSlots) {
+        BB_CUDA(cudaStreamWaitEvent(ms, freed[slot], 0));
+        BB_CUDA(cudaStreamWaitEvent(mgen.sc, freed[slot], 0));
+      }
+      bits[j] = slots + (size_t)slot * words;
+      evs[j] = ready[slot];
+    }
+    mgen.enqueue_chunk(ms, bits, cnt, evs, stats->launches);
+    return cnt;
+  }
+  // masks enqueued up to tree t (+ one chunk of lookahead on the GPU path)
+  void ahead(int t) {
+    while (next < T && next < t + (host_masks ? 1 : kChunk + 1)) next += produce(next);
+  }
+  unsigned int* bits(int t) const { return slots + (size_t)(t % kSlots) * words; }
+  ~MaskFeed() {
+    if (ms) {
+      mgen.report(ms);
+      cudaStreamSynchronize(ms);
+    }
+    mgen.sync();  // its streams still wait on ready / freed
+    if (ms) cudaStreamDestroy(ms);
+    for (int k = 0; k < kSlots; ++k) {
+      if (ready[k]) cudaEventDestroy(ready[k]);
+      if (freed[k]) cudaEventDestroy(freed[k]);
+      if (pinned[k]) cudaFreeHost(pinned[k]);
+    }
+  }
+};
+
 template <typename CodeT, typename NodeT>
 static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, int code_off,
                       const double* w_cb, double f0, int shift, const bb_fit_config& cfg,
                       const bb_forced_cut* forced, int n_forced, const double* bounds_dev, bb_fit_out* out,
-                      double* t_trees_ms, FitStats& stats, const Shard& shard, bool any_nan) {
+                      double* t_trees_ms, FitStats& stats, const Shard& shard, bool any_nan, MaskFeed& feed) {
   const int64_t n = s.n;
   cudaStream_t st = c.stream;
   const double two_s = std::ldexp(1.0, shift), scale = std::ldexp(1.0, -shift);
@@ -567,10 +677,6 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   long long* q = A.alloc<long long>(npad);
   BB_CUDA(cudaMemsetAsync(node, 0, (size_t)npad * sizeof(NodeT), st));
   BB_CUDA(cudaMemsetAsync(q, 0, (size_t)npad * 8, st));
-  const int64_t words = ceil_div(n, 32);
-  constexpr int kSlots = 2 * kChunk;
-  unsigned int* mask_slots = A.alloc<unsigned int>((size_t)words * kSlots);
-  const bool host_masks = (cfg.flags & 2) != 0 && !shard.dist;
   const int max_nodes = 1 << (s.depth - 1);
   // two layer histograms: the current layer's and its parent layer's (sibling
   // subtraction); both all-zero between trees
@@ -621,38 +727,6 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   for (int l = 1; l <= s.depth; ++l) plans[l] = plan_layer<CodeT, NodeT>(l, s, c.sm_count, !any_nan);
   BB_CUDA(cudaFuncSetAttribute(k_layer_hist<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
 
-  // subsample bits: GPU generator on its own stream (default) or the host
-  // restatement (flags bit 1), into a ring of kSlots mask buffers
-  Pcg64 g;
-  g.state = ((unsigned __int128)cfg.pcg_state_hi << 64) | cfg.pcg_state_lo;
-  g.inc = ((unsigned __int128)cfg.pcg_inc_hi << 64) | cfg.pcg_inc_lo;
-  g.has_uint32 = cfg.pcg_has_uint32;
-  g.uinteger = cfg.pcg_uinteger;
-  MaskGen mgen;
-  cudaStream_t ms = nullptr;
-  cudaEvent_t ready[kSlots], freed[kSlots];
-  unsigned int* pinned[kSlots] = {};
-  for (int k = 0; k < kSlots; ++k) {
-    BB_CUDA(cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming));
-    BB_CUDA(cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming));
-  }
-  if (host_masks) {
-    for (int k = 0; k < kSlots; ++k) BB_CUDA(cudaMallocHost(&pinned[k], (size_t)words * 4));
-  } else {
-    // the mask chain is the fit's critical path: highest stream priority so
-    // its cluster is scheduled as soon as SMs free up
-    int prio_lo = 0, prio_hi = 0;
-    BB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    BB_CUDA(cudaStreamCreateWithPriority(&ms, cudaStreamNonBlocking, prio_hi));
-    if (shard.dist) {
-      mgen.init(A, st, shard.n_sig_g, shard.n_bkg_g, cfg.subsample, cfg, c.sm_count);
-      mgen.sh = shard;
-      mgen.sh_n_local = s.n;
-    } else {
-      mgen.init(A, st, s.n_sig, s.n - s.n_sig, cfg.subsample, cfg, c.sm_count);
-    }
-  }
-  std::vector<uint32_t> perm;
   std::vector<NodeT> leaf_tmp;
   const bool prof = (cfg.flags & 1) != 0;
   std::vector<cudaEvent_t> hev;
@@ -663,7 +737,6 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
     hev.push_back(e);
   };
   auto cleanup = [&]() {
-    if (ms) mgen.report(ms);
     if (getenv("BB_HIST_PROFILE")) {
       unsigned long long h[8];
       cudaStreamSynchronize(st);
@@ -672,62 +745,24 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
       for (int q = 0; q < 6; ++q) fprintf(stderr, " %llu", h[q]);
       fprintf(stderr, "\n");
     }
-    if (ms) {
-      cudaStreamSynchronize(ms);
-      cudaStreamDestroy(ms);
-    }
-    for (int k = 0; k < kSlots; ++k) {
-      cudaEventDestroy(ready[k]);
-      cudaEventDestroy(freed[k]);
-      if (pinned[k]) cudaFreeHost(pinned[k]);
-    }
     for (auto e : hev) cudaEventDestroy(e);
   };
   const int gridN = grid_for(n, 256, c.sm_count);
   const int gridA = grid_for(n, 512, c.sm_count, 4);
   const auto t0 = std::chrono::steady_clock::now();
   try {
-    // the mask stream may run ahead of the fit stream by kSlots trees
-    int next_mask = 0;
-    auto produce = [&](int t) {  // host path: one tree; GPU path: the chunk starting at t
-      if (host_masks) {
-        const int slot = t % kSlots;
-        unsigned int* bits = mask_slots + (size_t)slot * words;
-        if (t >= kSlots) BB_CUDA(cudaEventSynchronize(freed[slot]));
-        const auto tm = std::chrono::steady_clock::now();
-        subsample_tree(g, s.n_sig, s.n - s.n_sig, cfg.subsample, pinned[slot], perm);
-        stats.mask_ms += elapsed_ms(tm);
-        BB_CUDA(cudaMemcpyAsync(bits, pinned[slot], (size_t)words * 4, cudaMemcpyHostToDevice, st));
-        BB_CUDA(cudaEventRecord(ready[slot], st));
-        return 1;
-      }
-      const int cnt = std::min(kChunk, s.T - t);
-      unsigned int* bits[kChunk];
-      cudaEvent_t evs[kChunk];
-      for (int j = 0; j < cnt; ++j) {
-        const int slot = (t + j) % kSlots;
-        if (t + j >= kSlots) {
-          BB_CUDA(cudaStreamWaitEvent(ms, freed[slot], 0));
-          if (mgen.sc) BB_CUDA(cudaStreamWaitEvent(mgen.sc, freed[slot], 0));
-        }
-        bits[j] = mask_slots + (size_t)slot * words;
-        evs[j] = ready[slot];
-      }
-      mgen.enqueue_chunk(ms, bits, cnt, evs, stats.launches);
-      return cnt;
-    };
     const bool tl_on = getenv("BB_TIMELINE") != nullptr;  // debug: main-stream waits for masks
     std::vector<cudaEvent_t> tl;
     for (int t = 0; t < s.T; ++t) {
-      while (next_mask < s.T && next_mask < t + (host_masks ? 1 : kChunk + 1)) next_mask += produce(next_mask);
+      feed.ahead(t);
       const int slot = t % kSlots;
-      unsigned int* mask = mask_slots + (size_t)slot * words;
+      unsigned int* mask = feed.bits(t);
       if (tl_on) {
         tl.emplace_back();
         BB_CUDA(cudaEventCreate(&tl.back()));
         BB_CUDA(cudaEventRecord(tl.back(), st));  // main stream done with tree t-1
       }
-      BB_CUDA(cudaStreamWaitEvent(st, ready[slot], 0));
+      BB_CUDA(cudaStreamWaitEvent(st, feed.ready[slot], 0));
       if (tl_on) {
         tl.emplace_back();
         BB_CUDA(cudaEventCreate(&tl.back()));
@@ -765,7 +800,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
             F, w_cb, two_s, sums);
         BB_LAUNCH_CHECK();
       }
-      BB_CUDA(cudaEventRecord(freed[slot], st));
+      BB_CUDA(cudaEventRecord(feed.freed[slot], st));
       c.comm.all_reduce(sums, (size_t)2 * s.n_nodes * 2, kNcclI64, kNcclSum, st);  // sharded fits
       k_node_weights<<<1, 256, (size_t)2 * s.n_nodes * 2 * 8, st>>>(sums, s.n_nodes, s.depth, scale, cfg.shrinkage, t,
                                                                     ta);
@@ -867,17 +902,9 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   }
   BB_CUDA(cudaStreamSynchronize(st));
   const double ms_up = elapsed_ms(t_up);
-  // ---- binning
+  // ---- class blocks (sample.py:112-116)
   auto t_bin = std::chrono::steady_clock::now();
-  std::vector<unsigned long long> finite, nans;
-  unsigned long long* finite_dev = nullptr;
   const bool dist = c.comm.active();  // row-sharded fit: every rank holds a slice of the rows
-  K* keys = make_keys<T>(c, A, Xd, n, d, finite, nans, &finite_dev, dist);
-  if (!x_dev) A.release(const_cast<T*>(Xd));
-  double* bounds = A.alloc<double>((size_t)d * nt);
-  K* bkeys = A.alloc<K>((size_t)d * nt);
-  run_select<T>(c, A, keys, n, d, levels, finite_dev, bounds, bkeys, dist);
-  // class blocks
   const int n_tiles = (int)ceil_div(n, CLS_TILE);
   int* tile_sig = A.alloc<int>(n_tiles + 1);
   int* pos = A.alloc<int>(n);
@@ -920,6 +947,27 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   } else if (n_sig == 0 || n_sig == n) {
     throw InvalidArg{"training data must contain both classes"};
   }
+  // ---- subsample masks: they need only the class sizes, so the first
+  // chunk's parse starts now and overlaps the binning below
+  MaskFeed feed;
+  feed.init(c, A, n, n_sig, cfg, shard, &stats);
+  feed.ahead(0);
+  // the user weights come back now; their host pass (prior, shift) overlaps
+  // the binning kernels
+  std::vector<double> wh;
+  if (w) {
+    wh.resize(n);
+    BB_CUDA(cudaMemcpyAsync(wh.data(), w_cb, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaStreamSynchronize(st));
+  }
+  // ---- binning
+  std::vector<unsigned long long> finite, nans;
+  unsigned long long* finite_dev = nullptr;
+  K* keys = make_keys<T>(c, A, Xd, n, d, finite, nans, &finite_dev, dist);
+  if (!x_dev) A.release(const_cast<T*>(Xd));
+  double* bounds = A.alloc<double>((size_t)d * nt);
+  K* bkeys = A.alloc<K>((size_t)d * nt);
+  run_select<T>(c, A, keys, n, d, levels, finite_dev, bounds, bkeys, dist);
   bool any_nan = false;
   for (int f = 0; f < d; ++f) any_nan |= nans[f] > 0;
   const int64_t stride = ceil_div(n, kTile) * kTile;  // rows incl. tile padding
@@ -927,9 +975,6 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   // prior (boosting.py:76-83) and the fixed-point shift from the user weights
   double w_sig, w_bkg, max_abs = 1.0;
   if (w) {
-    std::vector<double> wh(n);
-    BB_CUDA(cudaMemcpyAsync(wh.data(), w_cb, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
-    BB_CUDA(cudaStreamSynchronize(st));
     w_sig = pairwise(wh.data(), n_sig);
     w_bkg = pairwise(wh.data() + n_sig, n - n_sig);
     max_abs = 0.0;
@@ -977,9 +1022,11 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
     BB_CUDA(cudaStreamSynchronize(st));
     ms_bin = elapsed_ms(t_bin);
     if (s.depth <= 7)
-      run_trees<CodeT, uint8_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees, stats, shard, any_nan);
+      run_trees<CodeT, uint8_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees,
+                                stats, shard, any_nan, feed);
     else
-      run_trees<CodeT, uint16_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees, stats, shard, any_nan);
+      run_trees<CodeT, uint16_t>(c, A, s, codes, off, w_cb, f0, shift, cfg, forced, n_forced, bounds, out, &ms_trees,
+                                 stats, shard, any_nan, feed);
   };
   if (B <= 255) {
     go(A.alloc<uint8_t>((size_t)d * stride), 0);

@@ -80,6 +80,75 @@ struct Shard {
   bool dist = false;
 };
 
+// numpy's pairwise summation (pairwise() above) on the device: the host
+// enumerates the recursion's leaves (<= 128 elements), a kernel sums each
+// leaf with numpy's rule, the host combines the leaf sums in recursion order
+static void pw_leaves(int64_t off, int64_t n, std::vector<long long>& lo, std::vector<int>& ln) {
+  if (n <= 128) {
+    lo.push_back(off);
+    ln.push_back((int)n);
+    return;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  pw_leaves(off, n2, lo, ln);
+  pw_leaves(off + n2, n - n2, lo, ln);
+}
+
+static double pw_combine(int64_t n, const double* leaf, size_t& k) {
+  if (n <= 128) return leaf[k++];
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  const double a = pw_combine(n2, leaf, k);
+  const double b = pw_combine(n - n2, leaf, k);
+  return a + b;
+}
+
+__global__ void k_pairwise_leaves(const double* __restrict__ a, const long long* __restrict__ off,
+                                  const int* __restrict__ len, int L, double* __restrict__ out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < L; e += gridDim.x * blockDim.x) {
+    const double* x = a + off[e];
+    const int n = len[e];
+    double res;
+    if (n < 8) {
+      res = 0.0;
+      for (int i = 0; i < n; ++i) res = __dadd_rn(res, x[i]);
+    } else {
+      double r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = x[j];
+      int i;
+      for (i = 8; i < n - (n % 8); i += 8)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], x[i + j]);
+      res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      for (; i < n; ++i) res = __dadd_rn(res, x[i]);
+    }
+    out[e] = res;
+  }
+}
+
+// max |w| (as ordered bits) and a non-finite flag
+__global__ void k_weight_stats(const double* __restrict__ w, int64_t n, unsigned long long* __restrict__ maxbits,
+                               unsigned int* __restrict__ bad) {
+  double m = 0.0;
+  bool b = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = w[i];
+    b |= !isfinite(v);
+    m = fmax(m, fabs(v));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    b |= __shfl_xor_sync(0xffffffffu, (int)b, o) != 0;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(maxbits, (unsigned long long)__double_as_longlong(m));
+    if (b) atomicOr(bad, 1u);
+  }
+}
+
 // stream-ordered arena: every allocation of one call, freed at the end
 struct Arena {
   cudaStream_t s;
@@ -952,13 +1021,31 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   MaskFeed feed;
   feed.init(c, A, n, n_sig, cfg, shard, &stats);
   feed.ahead(0);
-  // the user weights come back now; their host pass (prior, shift) overlaps
-  // the binning kernels
-  std::vector<double> wh;
+  // user weights: per-class pairwise-sum leaves and max |w| on the device
+  // (read back after the binning kernels are queued)
+  std::vector<long long> pw_off;
+  std::vector<int> pw_len;
+  double* pw_out = nullptr;
+  unsigned long long* wstat = nullptr;
+  size_t L_sig = 0;
   if (w) {
-    wh.resize(n);
-    BB_CUDA(cudaMemcpyAsync(wh.data(), w_cb, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
-    BB_CUDA(cudaStreamSynchronize(st));
+    pw_leaves(0, n_sig, pw_off, pw_len);
+    L_sig = pw_off.size();
+    pw_leaves(n_sig, n - n_sig, pw_off, pw_len);
+    const int L = (int)pw_off.size();
+    long long* d_off = A.alloc<long long>(L);
+    int* d_len = A.alloc<int>(L);
+    pw_out = A.alloc<double>(L);
+    wstat = A.alloc<unsigned long long>(2);
+    BB_CUDA(cudaMemcpyAsync(d_off, pw_off.data(), (size_t)L * 8, cudaMemcpyHostToDevice, st));
+    BB_CUDA(cudaMemcpyAsync(d_len, pw_len.data(), (size_t)L * 4, cudaMemcpyHostToDevice, st));
+    BB_CUDA(cudaMemsetAsync(wstat, 0, 16, st));
+    k_pairwise_leaves<<<grid_for(L, 128, c.sm_count), 128, 0, st>>>(w_cb, d_off, d_len, L, pw_out);
+    BB_LAUNCH_CHECK();
+    k_weight_stats<<<grid_for(n, 256, c.sm_count), 256, 0, st>>>(w_cb, n, wstat,
+                                                               reinterpret_cast<unsigned int*>(wstat + 1));
+    BB_LAUNCH_CHECK();
+    BB_CUDA(cudaStreamSynchronize(st));  // host vectors pw_off / pw_len go out of use
   }
   // ---- binning
   std::vector<unsigned long long> finite, nans;
@@ -975,13 +1062,16 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   // prior (boosting.py:76-83) and the fixed-point shift from the user weights
   double w_sig, w_bkg, max_abs = 1.0;
   if (w) {
-    w_sig = pairwise(wh.data(), n_sig);
-    w_bkg = pairwise(wh.data() + n_sig, n - n_sig);
-    max_abs = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-      if (!std::isfinite(wh[i])) throw InvalidArg{"user weights must be finite"};
-      max_abs = std::max(max_abs, std::fabs(wh[i]));
-    }
+    std::vector<double> leaf(pw_off.size());
+    unsigned long long hs[2];
+    BB_CUDA(cudaMemcpyAsync(leaf.data(), pw_out, leaf.size() * 8, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaMemcpyAsync(hs, wstat, 16, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaStreamSynchronize(st));
+    if ((unsigned int)hs[1] != 0u) throw InvalidArg{"user weights must be finite"};
+    size_t k0 = 0, k1 = L_sig;
+    w_sig = pw_combine(n_sig, leaf.data(), k0);
+    w_bkg = pw_combine(n - n_sig, leaf.data(), k1);
+    std::memcpy(&max_abs, &hs[0], 8);
   } else {
     w_sig = (double)n_sig;
     w_bkg = (double)(n - n_sig);

@@ -318,6 +318,13 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, bool sib_
   return p;
 }
 
+// shared-memory plans needing more (node, feature) groups than this (each
+// re-reads every row) use the global-atomic histogram instead
+static int hist_global_groups() {
+  const char* e = getenv("BB_HIST_GLOBAL_GROUPS");  // read per call: tests force either path
+  return e ? atoi(e) : 16;
+}
+
 static inline int hist_grid(const HistPlan& p) { return p.n_fg * p.n_ng * (p.split_sig + p.split_bkg); }
 
 // GPU subsample-mask generator on its own stream (kernels_mask.cuh).  One
@@ -846,8 +853,12 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         unsigned long long* hist = hbuf[layer & 1];
         unsigned long long* par = hbuf[(layer - 1) & 1];
         if (prof) hist_event();
-        k_layer_hist<CodeT, NodeT><<<hist_grid(p), kHistThreads, p.smem, st>>>(codes, code_off, node, q, n, s.n_sig,
-                                                                               s.d, s.B, p, hist);
+        if (p.n_fg * p.n_ng > hist_global_groups())
+          k_layer_hist_g<CodeT, NodeT><<<8 * c.sm_count, 256, 0, st>>>(codes, code_off, node, q, n, s.n_sig, s.d,
+                                                                       s.B, p, hist);
+        else
+          k_layer_hist<CodeT, NodeT><<<hist_grid(p), kHistThreads, p.smem, st>>>(codes, code_off, node, q, n,
+                                                                                 s.n_sig, s.d, s.B, p, hist);
         BB_LAUNCH_CHECK();
         if (prof) hist_event();
         c.comm.all_reduce(hist, (size_t)2 * p.nodes * s.d * s.B, kNcclI64, kNcclSum, st);  // sharded fits
@@ -1456,7 +1467,10 @@ int bb_layer_hist(bb_ctx* ctx, const uint16_t* codes, const uint16_t* node, cons
     BB_CUDA(cudaMemsetAsync(hist, 0, hsz * 8, st));
     BB_CUDA(cudaFuncSetAttribute(k_layer_hist<uint16_t, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  227 * 1024));
-    k_layer_hist<uint16_t, uint16_t><<<hist_grid(p), kHistThreads, p.smem, st>>>(cd, 0, nd, qd, n, n_sig, d, B, p,
+    if (p.n_fg * p.n_ng > hist_global_groups())
+      k_layer_hist_g<uint16_t, uint16_t><<<8 * c.sm_count, 256, 0, st>>>(cd, 0, nd, qd, n, n_sig, d, B, p, hist);
+    else
+      k_layer_hist<uint16_t, uint16_t><<<hist_grid(p), kHistThreads, p.smem, st>>>(cd, 0, nd, qd, n, n_sig, d, B, p,
                                                                                   hist);
     BB_CUDA(cudaStreamSynchronize(st));  // host staging vector lives until here
     BB_LAUNCH_CHECK();

@@ -292,6 +292,39 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   flush(false);
 }
 
+// Layer histogram straight into global memory (int64 RED.ADD, L2-resident
+// layer histogram) for layers whose shared-memory plan would need many
+// (node, feature) groups, each re-reading every row: one pass over the rows,
+// one thread per (row, 8-feature block).  Same slots, same exact sums.
+template <typename CodeT, typename NodeT>
+__global__ void __launch_bounds__(256)
+    k_layer_hist_g(const CodeT* __restrict__ codes, int code_off, const NodeT* __restrict__ node,
+                   const long long* __restrict__ q, int64_t n, int64_t n_sig, int d, int B, HistPlan p,
+                   unsigned long long* __restrict__ hist) {
+  const int nfb = (d + 7) >> 3;
+  const int64_t items = ((n + kTile - 1) / kTile) * kTile * nfb;  // whole tiles x feature blocks
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    // consecutive threads take consecutive rows of one feature block (coalesced codes)
+    const int64_t tile = it / ((int64_t)kTile * nfb);
+    const int64_t rem = it - tile * (int64_t)kTile * nfb;
+    const int fb = (int)(rem / kTile);
+    const int64_t r = tile * kTile + (rem - (int64_t)fb * kTile);
+    if (r >= n) continue;
+    const int ln = (int)node[r] - p.start;
+    if (ln < 0 || ln >= p.nodes || (p.sib && (ln & 1))) continue;
+    const long long qq = q[r];
+    if (qq == 0) continue;
+    const int cls = r >= n_sig ? 1 : 0;
+    const int64_t base = ((int64_t)cls * p.nodes + ln) * d;
+    const int f0 = fb * 8, f1 = min(d, f0 + 8);
+    for (int f = f0; f < f1; ++f) {
+      const int c = (int)codes[code_index(r, f, d)] + code_off;
+      if (c != 0) atomicAdd(&hist[(base + f) * B + (c - 1)], as_ull(qq));
+    }
+  }
+}
+
 // ---------------------------------------------------------------- split
 // CPH prefix scan + separation gain + argmax (trees.py:117-136,170-204),
 // fixed-point definition shared with oracle/binboost_np.py:_gains_fixed.

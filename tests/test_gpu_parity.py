@@ -138,8 +138,17 @@ def _oracle_hist(codes, node, q, n_sig, d, levels, layer):
     return out
 
 
+@pytest.fixture(params=["smem", "global"])
+def hist_path(request, monkeypatch):
+    """Both histogram kernels: the shared-memory one and the global-atomic one
+    (forced with BB_HIST_GLOBAL_GROUPS=0)."""
+    if request.param == "global":
+        monkeypatch.setenv("BB_HIST_GLOBAL_GROUPS", "0")
+    return request.param
+
+
 @pytest.mark.parametrize("levels,layer,d", [(8, 1, 10), (8, 3, 40), (8, 5, 7), (10, 6, 3), (3, 2, 5), (1, 1, 2)])
-def test_layer_hist_exact(levels, layer, d):
+def test_layer_hist_exact(levels, layer, d, hist_path):
     rng = np.random.default_rng(levels * 100 + layer)
     n, n_sig = 60_000, 23_456
     codes, node, q = _random_layer(rng, n, n_sig, d, levels, layer)
@@ -231,7 +240,7 @@ def test_fit_cfg1_vs_reference_golden(golden_dir):
     _check_fit_vs_golden(forest, g, X[g["pred_rows"]])
 
 
-def test_fit_vs_fixed_point_oracle():
+def test_fit_vs_fixed_point_oracle(hist_path):
     X, y, w, _ = make_config("cfg2", n=60_000)
     cfg = FitConfig(n_trees=12, depth=4, shrinkage=0.2, subsample=0.6, binning_levels=6, seed=11)
     forest = fit_forest(X, y, w, cfg, return_leaves=True, return_scores=True)

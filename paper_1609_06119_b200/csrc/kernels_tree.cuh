@@ -107,6 +107,10 @@ struct HistPlan {
 __device__ unsigned long long g_hist_prof[8];
 
 constexpr int kHistThreads = 512;
+#ifndef BB_HIST_ILP
+#define BB_HIST_ILP 8
+#endif
+constexpr int kHistIlp = BB_HIST_ILP;  // returning low-limb atomics in flight per thread
 constexpr int kHistFlushTiles = 1 << 20;  // 2-limb slots are exact int64 sums (no periodic flush needed)
 
 __host__ __device__ __forceinline__ int align16(int x) { return (x + 15) & ~15; }
@@ -249,18 +253,18 @@ __global__ void __launch_bounds__(kHistThreads, 1)
       const int sb = nd * fcount * B - 1 + code_off;
       const CodeT* cp = ct + rl;
       int j = 0;
-      for (; j + 8 <= fcount; j += 8) {
-        int sl[8];
-        uint32_t old[8];
+      for (; j + kHistIlp <= fcount; j += kHistIlp) {
+        int sl[kHistIlp];
+        uint32_t old[kHistIlp];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kHistIlp; ++u) {
           const int c = (int)cp[(j + u) * kTile];
           sl[u] = (c + code_off != 0) ? sb + (j + u) * B + c : dummy;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) old[u] = atomicAdd(lo + sl[u], l);
+        for (int u = 0; u < kHistIlp; ++u) old[u] = atomicAdd(lo + sl[u], l);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kHistIlp; ++u) {
           const uint32_t hh = h + ((old[u] + l < old[u]) ? 1u : 0u);
           if (hh) atomicAdd(hi + sl[u], hh);
         }

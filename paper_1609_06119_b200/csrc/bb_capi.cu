@@ -352,7 +352,8 @@ static SegPlan build_seg_plan(int n) {
     P.n_rec += ns;
     P.tab.push_back(t);
     off += t.len;
-    if (off > (1ll << 30)) break;
+    // safety net: ~4x the expected draws of the job in 256-draw segments
+    if (P.tab.size() > 64 + (size_t)(4.0 * seg_expected_draws(n - 1) / 256.0)) break;
   }
   return P;
 }
@@ -449,6 +450,8 @@ struct MaskGen {
       BB_CUDA(cudaStreamSynchronize(st));
       smax = std::max(smax, S[cc]);
       rmax = std::max(rmax, P.n_rec);
+      if (getenv("BB_PARSE_PROFILE"))
+        fprintf(stderr, "seg plan n=%d: %d segments, %d phase-1 CTAs, %d records\n", n[cc], S[cc], n_tasks[cc], P.n_rec);
     }
     rec = A.alloc<SegRec>((size_t)rmax);
     seg_start = A.alloc<int>(smax);

@@ -49,7 +49,7 @@ constexpr int kAnchorSlack = 512;  // a job's segments start at its predicted fi
 constexpr int kSub = 512;          // states per phase-1 sub-window (one warp)
 constexpr int kSubPerCta = 8;      // sub-windows per phase-1 CTA (= warps per k_seg_pass CTA)
 constexpr int kSegMaxSub = 20;     // sub-windows per segment (max)
-constexpr int kSegTail = 8192;     // states below this: walked by phase 2
+constexpr int kSegTail = 4096;     // states below this: walked by phase 2
 constexpr int kSegThreads = 32 * kSubPerCta;
 constexpr int kSegRing = 16;       // segments of records in flight in k_seg_compose
 constexpr int kRows = 16;          // rows of 32 draws classified at once by phase 1 (512-draw chunks)
@@ -121,6 +121,10 @@ __host__ __device__ inline bool seg_geom(int i0, long long off, int floor_state,
   int lo = (int)fmax(1.0, floor(pl - seg_half_window((double)(off + slack))));
   int hi = (int)fmin((double)i0, ceil(pi + seg_half_window((double)off)));
   if (hi < floor_state || lo > hi) return false;
+  // stop once the state is below the floor with 3 sd to spare: the window cap
+  // (4096) would otherwise keep hi above a low floor forever; a job that is
+  // still above the floor after the last segment walks the rest exactly
+  if (pi + 1.5 * sqrt((double)(off + slack)) < (double)floor_state) return false;
   t->off = (int)off;
   const unsigned Mh = smear_host((unsigned)hi);
   const int bbA = (int)(Mh >> 1) + 1;

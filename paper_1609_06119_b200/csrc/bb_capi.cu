@@ -340,12 +340,35 @@ struct SegPlan {
   int n_rec = 0;
 };
 
-static SegPlan build_seg_plan(int n) {
+// standard deviation of a job's draw count: sum over steps of (1-q)/q^2,
+// q = (i+1)/(mask+1), integrated per band: (M+1)(1/qa - 1/qb + ln(qa/qb))
+static double seg_draws_sd(int n) {
+  double var = 0.0;
+  double x = (double)n;  // i + 1 at the job's first step
+  while (x > 1.0 + 1e-9) {
+    const unsigned M = smear_host((unsigned)std::max(1.0, std::floor(x - 1.0)));
+    const double mp1 = (double)M + 1.0, lowx = mp1 / 2.0;
+    const double qa = lowx / mp1, qb = x / mp1;  // q at the band's last and first steps
+    var += mp1 * (1.0 / qa - 1.0 / qb + std::log(qa / qb));
+    x = lowx;
+  }
+  return std::sqrt(std::max(0.0, var));
+}
+
+// anchor slack of a job: 2 sd of the previous job's draw count
+// (its first draw is predicted before that job is parsed), clamped
+static long long seg_slack(int n_prev) {
+  static const double k = getenv("BB_ANCHOR_SD") ? atof(getenv("BB_ANCHOR_SD")) : 2.0;
+  return std::min<long long>(kAnchorSlackMax,
+                             std::max<long long>(kAnchorSlackMin, (long long)std::ceil(k * seg_draws_sd(n_prev))));
+}
+
+static SegPlan build_seg_plan(int n, long long slack) {
   SegPlan P;
   if (n - 1 < kSegTail) return P;
   long long off = 0;
   SegTab t{};
-  while (seg_geom(n - 1, off, kSegTail, &t, 2 * kAnchorSlack)) {
+  while (seg_geom(n - 1, off, kSegTail, &t, 2 * slack)) {
     t.rec_off = P.n_rec;
     const int ns = t.nA + t.nB;
     for (int q = 0; q < ns; q += kSubPerCta) P.tasks.push_back(int2{(int)P.tab.size(), q});
@@ -376,8 +399,11 @@ struct MaskGen {
   SegTab* tab[2] = {nullptr, nullptr};
   int2* tasks[2] = {nullptr, nullptr};
   int S[2] = {0, 0}, n_tasks[2] = {0, 0};
-  SegRec* rec = nullptr;
-  int *seg_start = nullptr, *n_seg = nullptr;
+  SegRec* rec[2] = {nullptr, nullptr};          // by job parity
+  int *seg_start[2] = {nullptr, nullptr}, *n_seg[2] = {nullptr, nullptr};
+  long long slack[2] = {0, 0};                    // anchor slack per class
+  long long exp_draws[2] = {0, 0};                // expected draws of a job per class
+  cudaEvent_t evF[2] = {}, evC = nullptr, evTl = nullptr;
   long long* spos = nullptr;     // true first draw of each job of a chunk
   long long* sanchor = nullptr;  // anchor (predicted first draw + slack) of each job
   long long* stail = nullptr;    // chain -> tail hand-off: draw
@@ -439,7 +465,10 @@ struct MaskGen {
     gbits = A.alloc<unsigned int>((size_t)ceil_div(steps, 32) + 1);
     int smax = 1, rmax = 1;
     for (int cc = 0; cc < 2; ++cc) {
-      const SegPlan P = build_seg_plan(n[cc]);
+      // class cc's jobs follow jobs of the other class (sig, bkg alternate)
+      slack[cc] = seg_slack(n[1 - cc]);
+      exp_draws[cc] = n[cc] > 1 ? (long long)std::llround(seg_expected_draws(n[cc] - 1)) : 0;
+      const SegPlan P = build_seg_plan(n[cc], slack[cc]);
       S[cc] = (int)P.tab.size();
       n_tasks[cc] = (int)P.tasks.size();
       tab[cc] = A.alloc<SegTab>(std::max<size_t>(1, P.tab.size()));
@@ -453,9 +482,11 @@ struct MaskGen {
       if (getenv("BB_PARSE_PROFILE"))
         fprintf(stderr, "seg plan n=%d: %d segments, %d phase-1 CTAs, %d records\n", n[cc], S[cc], n_tasks[cc], P.n_rec);
     }
-    rec = A.alloc<SegRec>((size_t)rmax);
-    seg_start = A.alloc<int>(smax);
-    n_seg = A.alloc<int>(1);
+    for (int q = 0; q < 2; ++q) {
+      rec[q] = A.alloc<SegRec>((size_t)rmax);
+      seg_start[q] = A.alloc<int>(smax);
+      n_seg[q] = A.alloc<int>(1);
+    }
     spos = A.alloc<long long>(2 * (size_t)chunk + 2);
     sanchor = A.alloc<long long>(2 * (size_t)chunk + 2);
     stail = A.alloc<long long>(1);
@@ -465,6 +496,9 @@ struct MaskGen {
     BB_CUDA(cudaStreamCreateWithPriority(&sb, cudaStreamNonBlocking, hi_prio));
     BB_CUDA(cudaEventCreateWithFlags(&evA, cudaEventDisableTiming));
     BB_CUDA(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
+    BB_CUDA(cudaEventCreateWithFlags(&evC, cudaEventDisableTiming));
+    BB_CUDA(cudaEventCreateWithFlags(&evTl, cudaEventDisableTiming));
+    for (int q = 0; q < 2; ++q) BB_CUDA(cudaEventCreateWithFlags(&evF[q], cudaEventDisableTiming));
     BB_CUDA(cudaStreamCreateWithPriority(&sc, cudaStreamNonBlocking, hi_prio));
     for (int q = 0; q < kChunk; ++q) BB_CUDA(cudaEventCreateWithFlags(&evT[q], cudaEventDisableTiming));
     for (int q = 0; q < 2; ++q) BB_CUDA(cudaEventCreateWithFlags(&evR[q], cudaEventDisableTiming));
@@ -487,6 +521,10 @@ struct MaskGen {
     }
     if (evA) cudaEventDestroy(evA);
     if (evB) cudaEventDestroy(evB);
+    if (evC) cudaEventDestroy(evC);
+    if (evTl) cudaEventDestroy(evTl);
+    for (int q = 0; q < 2; ++q)
+      if (evF[q]) cudaEventDestroy(evF[q]);
     for (int q = 0; q < kChunk; ++q)
       if (evT[q]) cudaEventDestroy(evT[q]);
     for (int q = 0; q < 2; ++q)
@@ -505,23 +543,28 @@ struct MaskGen {
   // segment-parallel parse of `count` trees (2 * count block jobs)
   int64_t enqueue_seg(cudaStream_t st, int count) {
     int64_t launches = 0;
+    const int jobs = 2 * count;
     BB_CUDA(cudaMemcpyAsync(rng0, rng, sizeof(RngState), cudaMemcpyDeviceToDevice, st));
-    k_seg_init<<<1, 1, 0, st>>>(spos, sanchor);
+    // job 0 starts at draw 0; job 1's first draw is predicted from job 0's length
+    k_seg_init<<<1, 1, 0, st>>>(spos, sanchor, slack[0], exp_draws[0] + slack[1]);
     BB_LAUNCH_CHECK();
     const long long stride = std::max(n[0], n[1]);
-    SegArgs sa{};
-    sa.draws = draws;
-    sa.n_draws = n_draws;
-    sa.jump = jump;
-    sa.rng0 = rng0;
-    sa.rng = rng;
-    sa.rec = rec;
-    sa.seg_start = seg_start;
-    sa.n_seg = n_seg;
-    sa.tail_p = stail;
-    sa.tail_i = stail_i;
-    sa.prof = prof;
-    const int jobs = 2 * count;
+    SegArgs base{};
+    base.draws = draws;
+    base.n_draws = n_draws;
+    base.jump = jump;
+    base.rng0 = rng0;
+    base.rng = rng;
+    base.tail_p = stail;
+    base.tail_i = stail_i;
+    base.prof = prof;
+    auto args = [&](int jj) {  // the job-parity buffers of job jj
+      SegArgs a = base;
+      a.rec = rec[jj & 1];
+      a.seg_start = seg_start[jj & 1];
+      a.n_seg = n_seg[jj & 1];
+      return a;
+    };
     auto make_job = [&](int jj) {
       SegJob job{};
       if (jj < jobs) {
@@ -536,42 +579,68 @@ struct MaskGen {
         job.pos_in = spos + jj;
         job.pos_out = spos + jj + 1;
         job.anchor_in = sanchor + jj;
-        job.anchor_out = jj + 1 < jobs ? sanchor + jj + 1 : nullptr;
+        job.anchor2_out = jj + 2 < jobs ? sanchor + jj + 2 : nullptr;
+        job.next_draws = exp_draws[1 - cc];
+        job.slack2 = slack[cc];  // job jj+2 is of this job's class
         job.write_rng = jj == jobs - 1;
       }
       return job;
     };
-    auto pass = [&](cudaStream_t s, const SegJob& func, const SegJob& emit) {
-      const int nb_func = func.n_tasks;
-      const int nb_emit = (int)ceil_div(emit.S, kSubPerCta);
-      if (nb_func + nb_emit == 0) return;
-      sa.func = func;
-      sa.emit = emit;
-      k_seg_pass<<<nb_func + nb_emit, kSegThreads, kSegPassSmem, s>>>(sa, nb_func);
-      BB_LAUNCH_CHECK();
-      launches += 1;
+    auto func = [&](int jj) {  // phase 1 of job jj (stream sb)
+      const SegJob job = make_job(jj);
+      if (job.n_tasks > 0) {
+        SegArgs a = args(jj);
+        a.func = job;
+        a.emit = SegJob{};
+        k_seg_pass<<<job.n_tasks, kSegThreads, kSegPassSmem, sb>>>(a, job.n_tasks);
+        BB_LAUNCH_CHECK();
+        launches += 1;
+      }
+      BB_CUDA(cudaEventRecord(evF[jj & 1], sb));
     };
-    // stream st: chain(j) -> tail(j) -> chain(j+1) ...; stream sb, after
-    // chain(j): phase 1 of job j+1 and phase 3 of job j, concurrent with tail(j)
-    pass(st, make_job(0), SegJob{});
+    auto emit = [&](int jj) {  // phase 3 of job jj (stream sb)
+      const SegJob job = make_job(jj);
+      const int nb = (int)ceil_div(job.S, kSubPerCta);
+      if (nb > 0) {
+        SegArgs a = args(jj);
+        a.func = SegJob{};
+        a.emit = job;
+        k_seg_pass<<<nb, kSegThreads, kSegPassSmem, sb>>>(a, 0);
+        BB_LAUNCH_CHECK();
+        launches += 1;
+      }
+    };
+    // stream st: chain(j) -> tail(j) -> chain(j+1) ...  Stream sb: phase 1 of
+    // job j+2 right after tail(j) (its anchor is then known), overlapping
+    // chain(j+1) + tail(j+1); phase 3 of job j after chain(j).  Records and
+    // segment starts alternate between two buffers by job parity.
+    BB_CUDA(cudaEventRecord(evA, st));
+    BB_CUDA(cudaStreamWaitEvent(sb, evA, 0));
+    func(0);
+    if (jobs > 1) func(1);
     for (int jj = 0; jj < jobs; ++jj) {
       const SegJob job = make_job(jj);
-      sa.func = job;
-      sa.emit = SegJob{};
-      k_seg_chain<<<1, 64, kSegComposeSmem, st>>>(sa);
+      SegArgs a = args(jj);
+      a.func = job;
+      a.emit = SegJob{};
+      BB_CUDA(cudaStreamWaitEvent(st, evF[jj & 1], 0));  // phase 1 of job jj (and emit of jj-2) done
+      k_seg_chain<<<1, 64, kSegComposeSmem, st>>>(a);
       BB_LAUNCH_CHECK();
-      BB_CUDA(cudaEventRecord(evA, st));
-      BB_CUDA(cudaStreamWaitEvent(sb, evA, 0));
-      pass(sb, make_job(jj + 1), job);
-      BB_CUDA(cudaEventRecord(evB, sb));
-      if (jj & 1) BB_CUDA(cudaEventRecord(evT[jj >> 1], sb));  // both jobs of tree jj/2 emitted
-      sa.func = job;
-      sa.emit = SegJob{};
-      k_seg_tail<<<1, 32, 0, st>>>(sa);
+      BB_CUDA(cudaEventRecord(evC, st));
+      k_seg_tail<<<1, 32, 0, st>>>(a);
       BB_LAUNCH_CHECK();
-      BB_CUDA(cudaStreamWaitEvent(st, evB, 0));
+      BB_CUDA(cudaEventRecord(evTl, st));
       launches += 2;
+      BB_CUDA(cudaStreamWaitEvent(sb, evC, 0));
+      emit(jj);
+      if (jj & 1) BB_CUDA(cudaEventRecord(evT[jj >> 1], sb));  // both jobs of tree jj/2 emitted
+      if (jj + 2 < jobs) {
+        BB_CUDA(cudaStreamWaitEvent(sb, evTl, 0));
+        func(jj + 2);
+      }
     }
+    BB_CUDA(cudaEventRecord(evB, sb));
+    BB_CUDA(cudaStreamWaitEvent(st, evB, 0));  // the next chunk's draws overwrite what the emits read
     return launches;
   }
 

@@ -45,10 +45,11 @@ namespace bb {
 
 constexpr int kSegMaxLen = 8192;   // draws per segment (max)
 constexpr int kSegCrossLen = 1024; // draws per segment in band-crossing zones
-constexpr int kAnchorSlack = 512;  // a job's segments start at its predicted first draw + this
+constexpr int kAnchorSlackMin = 512;   // a job's segments start at its predicted first draw + a slack of
+constexpr int kAnchorSlackMax = 4000;  // 5 sd of a job's draw count, clamped to this range
 constexpr int kSub = 512;          // states per phase-1 sub-window (one warp)
 constexpr int kSubPerCta = 8;      // sub-windows per phase-1 CTA (= warps per k_seg_pass CTA)
-constexpr int kSegMaxSub = 20;     // sub-windows per segment (max)
+constexpr int kSegMaxSub = 32;     // sub-windows per segment (max)
 constexpr int kSegTail = 4096;     // states below this: walked by phase 2
 constexpr int kSegThreads = 32 * kSubPerCta;
 constexpr int kSegRing = 16;       // segments of records in flight in k_seg_compose
@@ -167,8 +168,10 @@ struct SegJob {
   int* J;                      // J[i] for steps i >= k
   long long* pos_in;           // job's first draw (absolute index into the draw buffer)
   long long* pos_out;          // written by the tail: first draw of the next job
-  long long* anchor_in;        // first draw of segment 0 (predicted first draw + kAnchorSlack)
-  long long* anchor_out;       // written by the chain: the next job's anchor (nullptr: none)
+  long long* anchor_in;        // first draw of segment 0 (predicted first draw + this class's slack)
+  long long* anchor2_out;      // written by the tail: anchor of the job after next (nullptr: none)
+  long long next_draws;        // expected draws of the next job (its first draw = this job's last + 1)
+  long long slack2;            // anchor slack of the job after next
   int write_rng;               // tail: update the RNG state after this job
 };
 
@@ -589,8 +592,7 @@ struct StageWalk {
 // segments into L2.  Warp 0 (consumer) walks from the job's exact first draw
 // to the anchor, then chains the segments' functions down to kSegTail (an
 // O(1) lookup per segment; a start the records cannot answer is walked
-// exactly), hands the tail's (draw, state) to k_seg_tail and predicts the
-// next job's first draw (its anchor) so its phase 1 can run during the tail.
+// exactly) and hands the tail's (draw, state) to k_seg_tail.
 __global__ void __launch_bounds__(64) k_seg_chain(SegArgs a) {
   extern __shared__ __align__(16) unsigned char cs_sm[];
   SegRec* ring = reinterpret_cast<SegRec*>(cs_sm);  // [kSegRing][kSegMaxSub]
@@ -615,7 +617,7 @@ __global__ void __launch_bounds__(64) k_seg_chain(SegArgs a) {
     mbar_init(&st_bar, 1);
     fence_mbar_init();
     // first segment at or after the true first draw (segment 0 unless the job
-    // started more than kAnchorSlack draws late); earlier ones are skipped
+    // started more than its slack late); earlier ones are skipped
     int s0 = 0;
     while (s0 < S && anc + jb.tab[s0].off < p0) ++s0;
     s_s0 = s0;
@@ -725,7 +727,6 @@ __global__ void __launch_bounds__(64) k_seg_chain(SegArgs a) {
     *a.n_seg = s;
     *a.tail_p = p;
     *a.tail_i = i;
-    if (jb.anchor_out) *jb.anchor_out = p + (long long)(seg_expected_draws(i) + 0.5) + kAnchorSlack;
     if (a.prof) {
       atomicAdd((unsigned long long*)&a.prof[0], (unsigned long long)(s - s0));
       atomicAdd((unsigned long long*)&a.prof[1], (unsigned long long)n_resim);
@@ -762,15 +763,15 @@ __global__ void __launch_bounds__(32) k_seg_tail(SegArgs a) {
   }
   if (lane == 0) {
     *jb.pos_out = p;
+    // the job after next: first draw predicted from the next job's exact first
+    // draw (p) and its expected length, so its phase 1 runs during the next
+    // job's chain and tail
+    if (jb.anchor2_out) *jb.anchor2_out = p + jb.next_draws + jb.slack2;
     if (a.prof) {
       atomicAdd((unsigned long long*)&a.prof[2], (unsigned long long)tail);
       atomicAdd((unsigned long long*)&a.prof[3], 1ull);
       atomicAdd((unsigned long long*)&a.prof[6], (unsigned long long)(clock64() - ct));
-      // anchor error: true first draw of the next job vs the predicted one
-      if (jb.anchor_out) {
-        const long long e = p - (*jb.anchor_out - kAnchorSlack);
-        atomicMax((unsigned long long*)&a.prof[14], (unsigned long long)(e < 0 ? -e : e));
-      }
+      // anchor error of this job: true first draw vs predicted (anchor - slack), via pos_in
     }
     if (jb.write_rng) {
       RngState r = r0;
@@ -796,9 +797,10 @@ __global__ void __launch_bounds__(32) k_seg_tail(SegArgs a) {
   }
 }
 
-__global__ void k_seg_init(long long* pos, long long* anchor) {
+__global__ void k_seg_init(long long* pos, long long* anchor, long long a0, long long a1) {
   pos[0] = 0;
-  anchor[0] = kAnchorSlack;
+  anchor[0] = a0;
+  anchor[1] = a1;
 }
 
 }  // namespace bb

@@ -105,8 +105,11 @@ __host__ __device__ inline double seg_expected_draws(int i0) {
 
 // half window after p draws: 5 sd (sd <= sqrt(p)/2); a start outside the
 // window only costs an exact walk
+#ifndef BB_SEG_WINDOW_SD
+#define BB_SEG_WINDOW_SD 5.0
+#endif
 __host__ __device__ inline double seg_half_window(double p) {
-  return p <= 0.0 ? 0.0 : fmin(4096.0, ceil(2.5 * sqrt(p)) + 16.0);
+  return p <= 0.0 ? 0.0 : fmin(4096.0, ceil(0.5 * BB_SEG_WINDOW_SD * sqrt(p)) + 16.0);
 }
 
 // Geometry of the segment at draw offset `off` of a stretch that starts at

@@ -9,6 +9,6 @@ ncu --set full --import-source on --clock-control none -k regex:k_layer_hist -s 
     python tools/prof_fit.py --trees 4 --reps 1 --host-masks > gpurun_out/ncu_hist.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_seg_chain -s 4 -c 1 -o gpurun_out/chain_full \
     python tools/time_masks.py --trees 8 --reps 1 > gpurun_out/ncu_chain.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:k_apply_f32 -c 1 -o gpurun_out/apply_full \
+ncu --set full --import-source on --clock-control none -k regex:k_apply -c 1 -o gpurun_out/apply_full \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --apply-rows 10000000 > gpurun_out/ncu_apply.log 2>&1
 ls -la gpurun_out

@@ -325,6 +325,11 @@ static int hist_global_groups() {
   return e ? atoi(e) : 16;
 }
 
+static bool hist_warp_mode() {  // the warp-independent histogram kernel (BB_HIST_WARP=0: the CTA-barrier one)
+  const char* e = getenv("BB_HIST_WARP");
+  return !e || atoi(e) != 0;
+}
+
 static inline int hist_grid(const HistPlan& p) { return p.n_fg * p.n_ng * (p.split_sig + p.split_bkg); }
 
 // GPU subsample-mask generator on its own stream (kernels_mask.cuh).  One
@@ -874,6 +879,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   // it is used only for NaN-free data
   for (int l = 1; l <= s.depth; ++l) plans[l] = plan_layer<CodeT, NodeT>(l, s, c.sm_count, !any_nan);
   BB_CUDA(cudaFuncSetAttribute(k_layer_hist<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  BB_CUDA(cudaFuncSetAttribute(k_layer_hist_w<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
 
   std::vector<NodeT> leaf_tmp;
   const bool prof = (cfg.flags & 1) != 0;
@@ -928,6 +934,9 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         if (p.n_fg * p.n_ng > hist_global_groups())
           k_layer_hist_g<CodeT, NodeT><<<8 * c.sm_count, 256, 0, st>>>(codes, code_off, node, q, n, s.n_sig, s.d,
                                                                        s.B, p, hist);
+        else if (hist_warp_mode())
+          k_layer_hist_w<CodeT, NodeT><<<hist_grid(p), kHistWThreads, p.smem, st>>>(codes, code_off, node, q, n,
+                                                                                   s.n_sig, s.d, s.B, p, hist);
         else
           k_layer_hist<CodeT, NodeT><<<hist_grid(p), kHistThreads, p.smem, st>>>(codes, code_off, node, q, n,
                                                                                  s.n_sig, s.d, s.B, p, hist);
@@ -1539,8 +1548,13 @@ int bb_layer_hist(bb_ctx* ctx, const uint16_t* codes, const uint16_t* node, cons
     BB_CUDA(cudaMemsetAsync(hist, 0, hsz * 8, st));
     BB_CUDA(cudaFuncSetAttribute(k_layer_hist<uint16_t, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  227 * 1024));
+    BB_CUDA(cudaFuncSetAttribute(k_layer_hist_w<uint16_t, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 227 * 1024));
     if (p.n_fg * p.n_ng > hist_global_groups())
       k_layer_hist_g<uint16_t, uint16_t><<<8 * c.sm_count, 256, 0, st>>>(cd, 0, nd, qd, n, n_sig, d, B, p, hist);
+    else if (hist_warp_mode())
+      k_layer_hist_w<uint16_t, uint16_t><<<hist_grid(p), kHistWThreads, p.smem, st>>>(cd, 0, nd, qd, n, n_sig, d, B,
+                                                                                      p, hist);
     else
       k_layer_hist<uint16_t, uint16_t><<<hist_grid(p), kHistThreads, p.smem, st>>>(cd, 0, nd, qd, n, n_sig, d, B, p,
                                                                                   hist);

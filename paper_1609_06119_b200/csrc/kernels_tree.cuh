@@ -296,6 +296,166 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   flush(false);
 }
 
+// Warp-independent variant of k_layer_hist (same plan, slots and sums): warp
+// 16 is a producer issuing the tiles' bulk copies behind full/empty
+// mbarriers; compute warp w compacts and accumulates its own 64 rows of
+// each tile with no CTA-wide barrier, so warps drift up to a tile apart and
+// the shared atomic pipe stays busy across tile boundaries.
+#ifndef BB_HIST_WARPS
+#define BB_HIST_WARPS 16
+#endif
+constexpr int kHistWarps = BB_HIST_WARPS;  // compute warps; each owns 1024 / kHistWarps rows of a tile
+constexpr int kHistWRows = 1024 / kHistWarps;
+constexpr int kHistWThreads = 32 * (kHistWarps + 1);
+
+template <typename CodeT, typename NodeT>
+__global__ void __launch_bounds__(kHistWThreads, 1)
+    k_layer_hist_w(const CodeT* __restrict__ codes, int code_off, const NodeT* __restrict__ node,
+                   const long long* __restrict__ q, int64_t n, int64_t n_sig, int d, int B, HistPlan p,
+                   unsigned long long* __restrict__ hist) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int groups = p.n_fg * p.n_ng;
+  const int group = blockIdx.x % groups;
+  const int part = blockIdx.x / groups;
+  const int fgi = group % p.n_fg, ngi = group / p.n_fg;
+  int cls, ta, tb;
+  int64_t clo, chi;
+  if (part < p.split_sig) {
+    cls = 0;
+    clo = 0;
+    chi = n_sig;
+    const int nt = p.tiles_sig1 - p.tiles_sig0;
+    ta = p.tiles_sig0 + (int)((int64_t)nt * part / p.split_sig);
+    tb = p.tiles_sig0 + (int)((int64_t)nt * (part + 1) / p.split_sig);
+  } else {
+    cls = 1;
+    clo = n_sig;
+    chi = n;
+    const int k = part - p.split_sig;
+    const int nt = p.tiles_bkg1 - p.tiles_bkg0;
+    ta = p.tiles_bkg0 + (int)((int64_t)nt * k / p.split_bkg);
+    tb = p.tiles_bkg0 + (int)((int64_t)nt * (k + 1) / p.split_bkg);
+  }
+  const int f0 = fgi * p.fg;
+  const int fcount = min(p.fg, d - f0);
+  const int n0 = ngi * p.ngs;
+  const int built = p.sib ? p.nodes >> 1 : p.nodes;
+  const int ncount = min(p.ngs, built - n0);
+  const int nslots = ncount * fcount * B;
+  const int tile = p.tile;
+  uint32_t* lo = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* hi = lo + nslots + 32;
+  unsigned char* stage = smem + align16((nslots + 32) * 8);
+  const int bufb = hist_buf_bytes<CodeT, NodeT>(tile, fcount);
+  uint32_t* list = reinterpret_cast<uint32_t*>(stage + 2 * bufb);  // [warp][kHistWRows]
+  uint64_t* full = reinterpret_cast<uint64_t*>(list + tile);
+  uint64_t* empty = full + 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  for (int i = threadIdx.x; i < 2 * (nslots + 32); i += kHistWThreads) lo[i] = 0u;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], kHistWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == kHistWarps) {
+    // ---- producer
+    if (lane == 0) {
+      for (int k = ta; k < tb; ++k) {
+        const int it = k - ta, buf = it & 1;
+        if (it >= 2) mbar_wait(&empty[buf], (unsigned)(((it >> 1) - 1) & 1));
+        unsigned char* b = stage + buf * bufb;
+        const int64_t row0 = (int64_t)k * tile;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[buf], (unsigned)(tile * (int)sizeof(NodeT) + tile * 8 + fcount * tile * (int)sizeof(CodeT)));
+        tma_load_1d(b, node + row0, tile * sizeof(NodeT), &full[buf]);
+        tma_load_1d(b + align16(tile * (int)sizeof(NodeT)), q + row0, tile * 8, &full[buf]);
+        tma_load_1d(b + align16(tile * (int)sizeof(NodeT)) + tile * 8, codes + ((int64_t)k * d + f0) * kTile,
+                    fcount * kTile * sizeof(CodeT), &full[buf]);
+      }
+    }
+  } else {
+    // ---- compute warps
+    uint32_t* wl = list + warp * kHistWRows;
+    const int dummy = nslots + lane;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int k = ta; k < tb; ++k) {
+      const int it = k - ta, buf = it & 1;
+      mbar_wait(&full[buf], (unsigned)((it >> 1) & 1));
+      const unsigned char* b = stage + buf * bufb;
+      const NodeT* nt = reinterpret_cast<const NodeT*>(b);
+      const long long* qt = reinterpret_cast<const long long*>(b + align16(tile * (int)sizeof(NodeT)));
+      const CodeT* ct = reinterpret_cast<const CodeT*>(b + align16(tile * (int)sizeof(NodeT)) + tile * 8);
+      const int64_t row0 = (int64_t)k * tile;
+      int cnt = 0;
+#pragma unroll
+      for (int h = 0; h < kHistWRows / 32; ++h) {
+        const int rl = warp * kHistWRows + h * 32 + lane;
+        const int64_t r = row0 + rl;
+        const int ln = (int)nt[rl] - p.start;
+        const int nd = (p.sib ? (ln >> 1) : ln) - n0;
+        const bool ok = r >= clo && r < chi && ln >= 0 && ln < p.nodes && !(p.sib && (ln & 1)) && nd >= 0 &&
+                        nd < ncount && qt[rl] != 0;
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        if (ok) wl[cnt + __popc(m & lt)] = (uint32_t)rl | ((uint32_t)nd << 16);
+        cnt += __popc(m);
+      }
+      __syncwarp();
+      for (int ai = lane; ai < cnt; ai += 32) {
+        const uint32_t e = wl[ai];
+        const int rl = (int)(e & 0xffffu);
+        const int nd = (int)(e >> 16);
+        const long long qq = qt[rl];
+        const uint32_t l = (uint32_t)(unsigned long long)qq;
+        const uint32_t h = (uint32_t)((unsigned long long)qq >> 32);
+        const int sb = nd * fcount * B - 1 + code_off;
+        const CodeT* cp = ct + rl;
+        int j = 0;
+        for (; j + kHistIlp <= fcount; j += kHistIlp) {
+          int sl[kHistIlp];
+          uint32_t old[kHistIlp];
+#pragma unroll
+          for (int u = 0; u < kHistIlp; ++u) {
+            const int c = (int)cp[(j + u) * kTile];
+            sl[u] = (c + code_off != 0) ? sb + (j + u) * B + c : dummy;
+          }
+#pragma unroll
+          for (int u = 0; u < kHistIlp; ++u) old[u] = atomicAdd(lo + sl[u], l);
+#pragma unroll
+          for (int u = 0; u < kHistIlp; ++u) {
+            const uint32_t hh = h + ((old[u] + l < old[u]) ? 1u : 0u);
+            if (hh) atomicAdd(hi + sl[u], hh);
+          }
+        }
+        for (; j < fcount; ++j) {
+          const int c = (int)cp[j * kTile];
+          const int sl = (c + code_off != 0) ? sb + j * B + c : dummy;
+          const uint32_t o = atomicAdd(lo + sl, l);
+          const uint32_t hh = h + ((o + l < o) ? 1u : 0u);
+          if (hh) atomicAdd(hi + sl, hh);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[buf])) : "memory");
+    }
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < nslots; s += kHistWThreads) {
+    const long long v = (long long)(((unsigned long long)hi[s] << 32) | (unsigned long long)lo[s]);
+    if (v != 0) {
+      const int bb = s % B;
+      const int j = (s / B) % fcount;
+      const int nd = s / (B * fcount);
+      const int ln = p.sib ? 2 * (n0 + nd) : (n0 + nd);
+      const int64_t g = (((int64_t)cls * p.nodes + ln) * d + (f0 + j)) * B + bb;
+      atomicAdd(&hist[g], as_ull(v));
+    }
+  }
+}
+
 // Layer histogram straight into global memory (int64 RED.ADD, L2-resident
 // layer histogram) for layers whose shared-memory plan would need many
 // (node, feature) groups, each re-reading every row: one pass over the rows,

@@ -138,10 +138,13 @@ def _oracle_hist(codes, node, q, n_sig, d, levels, layer):
     return out
 
 
-@pytest.fixture(params=["smem", "global"])
+@pytest.fixture(params=["warp", "cta", "global"])
 def hist_path(request, monkeypatch):
-    """Both histogram kernels: the shared-memory one and the global-atomic one
+    """Every histogram kernel: the warp-independent shared-memory one
+    (default), the CTA-barrier one (BB_HIST_WARP=0) and the global-atomic one
     (forced with BB_HIST_GLOBAL_GROUPS=0)."""
+    if request.param == "cta":
+        monkeypatch.setenv("BB_HIST_WARP", "0")
     if request.param == "global":
         monkeypatch.setenv("BB_HIST_GLOBAL_GROUPS", "0")
     return request.param

@@ -12,8 +12,11 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <stdexcept>
 #include <string>
 #include <vector>
+
+#include <cudaTypedefs.h>
 
 #include "../../include/fastbdt_b200.h"
 #include "bb_mask.h"
@@ -24,6 +27,7 @@
 #include "kernels_mask.cuh"
 #include "kernels_seg.cuh"
 #include "kernels_tree.cuh"
+#include "kernels_hist_fl.cuh"
 
 namespace bb {
 
@@ -331,6 +335,226 @@ static bool hist_warp_mode() {  // the warp-independent histogram kernel (BB_HIS
 }
 
 static inline int hist_grid(const HistPlan& p) { return p.n_fg * p.n_ng * (p.split_sig + p.split_bkg); }
+
+// Histogram path: BB_HIST_PATH = fl | w | cta | g (read per call: tests force
+// each path); default: feature-lane kernel where its plan fits, else the
+// warp-independent one (or global atomics for many-group plans).
+static int hist_path_env() {
+  const char* e = getenv("BB_HIST_PATH");
+  if (!e) return 0;
+  if (!strcmp(e, "fl")) return 1;
+  if (!strcmp(e, "w")) return 2;
+  if (!strcmp(e, "cta")) return 3;
+  if (!strcmp(e, "g")) return 4;
+  return 0;
+}
+
+// Tensor maps (driver entry point; no libcuda link) for the feature-lane
+// histogram's 2-D code boxes.
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    BB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr));
+    if (!f || qr != cudaDriverEntryPointSuccess) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// codes viewed as 2-D [tiles * d feature columns][kTile codes], boxes of
+// [fpad columns][128 bytes], 128-byte swizzle
+template <typename CodeT>
+static void make_code_map(CUtensorMap* tm, const CodeT* codes, int64_t tiles, int d, int fpad) {
+  const cuuint64_t dims[2] = {(cuuint64_t)kTile, (cuuint64_t)(tiles * d)};
+  const cuuint64_t strides[1] = {(cuuint64_t)kTile * sizeof(CodeT)};
+  const cuuint32_t box[2] = {(cuuint32_t)(128 / sizeof(CodeT)), (cuuint32_t)fpad};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(
+      tm, sizeof(CodeT) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
+      const_cast<CodeT*>(codes), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+// Plan of k_layer_hist_fl (kernels_hist_fl.cuh): work types = class x
+// feature group (up to 64 features: 32 lanes x 1 row, plus a remainder sub
+// with 1, 2 or 4 row copies) x node group (nodes whose lane-interleaved
+// 2-limb slots fit next to the ring); one CTA per SM, split across types in
+// proportion to their estimated work.  n_types == 0: no feasible plan (wide
+// bins).
+template <typename CodeT, typename NodeT>
+static FlPlan plan_fl(int layer, const FitShape& s, int sm_count, bool sib_ok, const CodeT* codes) {
+  FlPlan p{};
+  p.nodes = 1 << (layer - 1);
+  p.start = p.nodes - 1;
+  p.sib = (sib_ok && layer >= 2) ? 1 : 0;
+  p.log2b = s.levels;
+  const int built = p.sib ? p.nodes / 2 : p.nodes;
+  if (s.B > 256) return FlPlan{};
+  auto rl = [](int r) { return r > 16 ? 0 : (r > 8 ? 1 : 2); };
+  struct FG { int f0, fc0, r0log, fc1, r1log, fpad; };
+  constexpr int kSmemMax = 227 * 1024;
+  const int subb = (s.B + 1) * 256;
+  const int fixed0 = 1024 + kFlMetaBytes + 2 * kFlMaxStages * 8;
+  std::vector<FG> fgs;
+  int nsub = 1;
+  bool ok = false;
+  for (int width : {64, 32}) {  // features per type: merged remainder first
+    fgs.clear();
+    nsub = 1;
+    for (int f0 = 0; f0 < s.d; f0 += width) {
+      const int r = std::min(width, s.d - f0);
+      FG g{};
+      g.f0 = f0;
+      if (r > 32) {
+        g.fc0 = 32; g.r0log = 0; g.fc1 = r - 32; g.r1log = rl(r - 32);
+        nsub = 2;
+      } else {
+        g.fc0 = r; g.r0log = rl(r); g.fc1 = 0; g.r1log = 0;
+      }
+      g.fpad = (g.fc0 + g.fc1 + 7) & ~7;
+      fgs.push_back(g);
+    }
+    p.stage_bytes = fl_stage_bytes<CodeT, NodeT>(fgs[0].fpad);
+    for (int ns : {3, 2}) {
+      if (fixed0 + ns * p.stage_bytes + nsub * subb <= kSmemMax) {
+        p.stages = ns;
+        ok = true;
+        break;
+      }
+    }
+    if (ok) break;
+  }
+  if (!ok) return FlPlan{};
+  const int nc_fit = (kSmemMax - fixed0 - p.stages * p.stage_bytes) / (nsub * subb);
+  const int n_ng = (int)ceil_div(built, std::min(built, nc_fit));
+  p.ngs = (int)ceil_div(built, n_ng);
+  p.hist_bytes = p.ngs * nsub * subb;
+  p.smem = fixed0 + p.stages * p.stage_bytes + p.hist_bytes;
+  const int64_t tiles = ceil_div(s.n, kTile);
+  make_code_map(&p.tm[0], codes, tiles, s.d, fgs[0].fpad);
+  if (fgs.back().fpad != fgs[0].fpad) make_code_map(&p.tm[1], codes, tiles, s.d, fgs.back().fpad);
+  static const int reserve = getenv("BB_HIST_RESERVE") ? atoi(getenv("BB_HIST_RESERVE")) : 9;
+  const int total = std::max(1, sm_count - reserve);
+  const int64_t st_sig0 = 0, st_sig1 = ceil_div(s.n_sig, kFlRows);
+  const int64_t st_bkg0 = s.n_sig / kFlRows, st_bkg1 = ceil_div(s.n, kFlRows);
+  std::vector<FlType> ts;
+  std::vector<double> w;
+  const double frac0 = 0.5 * (p.sib ? 0.5 : 1.0) / n_ng;  // contributing share of a class's rows (alpha ~ 0.5)
+  auto steps = [&](int r_log) {                            // warp steps per row of a sub
+    const int R = 1 << r_log;
+    return (1.0 - std::pow(1.0 - frac0, R)) / R;
+  };
+  for (int cls = 0; cls < 2; ++cls) {
+    const int64_t a = cls ? st_bkg0 : st_sig0, b = cls ? st_bkg1 : st_sig1;
+    if (b <= a) continue;
+    for (size_t gi = 0; gi < fgs.size(); ++gi) {
+      const FG& g = fgs[gi];
+      for (int ng = 0; ng < n_ng; ++ng) {
+        FlType t{};
+        t.t0 = (int)a;
+        t.t1 = (int)b;
+        t.cls = (short)cls;
+        t.f0 = (short)g.f0;
+        t.fc0 = (short)g.fc0;
+        t.r0log = (short)g.r0log;
+        t.fc1 = (short)g.fc1;
+        t.r1log = (short)g.r1log;
+        t.fpad = (short)g.fpad;
+        t.map = (short)(g.fpad == fgs[0].fpad ? 0 : 1);
+        t.n0 = (short)(ng * p.ngs);
+        t.ncount = (short)std::min(p.ngs, built - ng * p.ngs);
+        w.push_back((double)(b - a) * (0.6 + 3.0 * (steps(g.r0log) + (g.fc1 ? steps(g.r1log) : 0.0))));
+        ts.push_back(t);
+      }
+    }
+  }
+  if (ts.empty() || (int)ts.size() > kFlMaxTypes || (int)ts.size() > total) return FlPlan{};
+  double wsum = 0;
+  for (double x : w) wsum += x;
+  int used = 0;
+  for (size_t i = 0; i < ts.size(); ++i) {
+    int k = (int)std::floor(total * w[i] / wsum);
+    k = (int)std::max<int64_t>(1, std::min<int64_t>(k, ts[i].t1 - ts[i].t0));
+    ts[i].nctas = k;
+    used += k;
+  }
+  // hand the rounding remainder to the heaviest types (per CTA)
+  while (used < total) {
+    int best = -1;
+    double bw = 0;
+    for (size_t i = 0; i < ts.size(); ++i) {
+      if (ts[i].nctas >= ts[i].t1 - ts[i].t0) continue;
+      const double x = w[i] / ts[i].nctas;
+      if (x > bw) { bw = x; best = (int)i; }
+    }
+    if (best < 0) break;
+    ts[best].nctas += 1;
+    used += 1;
+  }
+  int cta = 0;
+  for (size_t i = 0; i < ts.size(); ++i) {
+    ts[i].cta0 = cta;
+    for (int k = 0; k < ts[i].nctas && cta + k < 256; ++k) p.cta_type[cta + k] = (unsigned char)i;
+    cta += ts[i].nctas;
+    p.t[i] = ts[i];
+  }
+  if (cta > 256) return FlPlan{};
+  p.n_types = (int)ts.size();
+  p.noflush = getenv("BB_FL_NOFLUSH") ? atoi(getenv("BB_FL_NOFLUSH")) : 0;
+  return p;
+}
+
+// partial rows per CTA (elements) and the scratch a plan needs
+static inline int64_t fl_cta_stride(const FlPlan& p, int B) {
+  int rows = 0;
+  for (int i = 0; i < p.n_types; ++i) rows = std::max(rows, p.t[i].ncount * (p.t[i].fc0 + p.t[i].fc1));
+  return (int64_t)rows * B;
+}
+
+static inline int fl_grid(const FlPlan& p) { return p.n_types ? p.t[p.n_types - 1].cta0 + p.t[p.n_types - 1].nctas : 0; }
+
+// one layer histogram launch on the chosen path (same slots, same exact sums)
+template <typename CodeT, typename NodeT>
+static void launch_layer_hist(const HistPlan& p, const FlPlan& fl, int sm_count, const CodeT* codes, int code_off,
+                              const NodeT* node, const long long* q, int64_t n, int64_t n_sig, int d, int B,
+                              unsigned long long* hist, cudaStream_t st, long long* partials) {
+  const int path = hist_path_env();
+  if ((path == 0 || path == 1) && fl.n_types > 0 && !getenv("BB_HIST_WARP") && !getenv("BB_HIST_GLOBAL_GROUPS")) {
+    const bool use_partials = getenv("BB_FL_PARTIALS") && atoi(getenv("BB_FL_PARTIALS")) != 0;  // per call: tests
+    if (partials && use_partials) {
+      FlPlan f2 = fl;
+      f2.partials = partials;
+      f2.cta_stride = fl_cta_stride(fl, B);
+      k_layer_hist_fl<CodeT, NodeT><<<fl_grid(f2), kFlThreads, f2.smem, st>>>(code_off, node, q, n, n_sig, d, B, f2,
+                                                                             hist);
+      BB_LAUNCH_CHECK();
+      int rows = 0;
+      for (int i = 0; i < f2.n_types; ++i) rows = std::max(rows, f2.t[i].ncount * (f2.t[i].fc0 + f2.t[i].fc1));
+      k_fl_reduce<<<dim3(rows, f2.n_types), kFlRedThreads, 0, st>>>(d, B, f2, hist);
+    } else {
+      k_layer_hist_fl<CodeT, NodeT><<<fl_grid(fl), kFlThreads, fl.smem, st>>>(code_off, node, q, n, n_sig, d, B, fl,
+                                                                             hist);
+    }
+  } else if (path == 4 || (path == 0 && p.n_fg * p.n_ng > hist_global_groups())) {
+    k_layer_hist_g<CodeT, NodeT><<<8 * sm_count, 256, 0, st>>>(codes, code_off, node, q, n, n_sig, d, B, p, hist);
+  } else if (path == 2 || (path != 3 && hist_warp_mode())) {
+    k_layer_hist_w<CodeT, NodeT><<<hist_grid(p), kHistWThreads, p.smem, st>>>(codes, code_off, node, q, n, n_sig, d, B,
+                                                                             p, hist);
+  } else {
+    k_layer_hist<CodeT, NodeT><<<hist_grid(p), kHistThreads, p.smem, st>>>(codes, code_off, node, q, n, n_sig, d, B, p,
+                                                                           hist);
+  }
+  BB_LAUNCH_CHECK();
+}
+
+template <typename CodeT, typename NodeT>
+static void set_hist_smem_attrs() {
+  BB_CUDA(cudaFuncSetAttribute(k_layer_hist<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  BB_CUDA(cudaFuncSetAttribute(k_layer_hist_w<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  BB_CUDA(cudaFuncSetAttribute(k_layer_hist_fl<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+}
 
 // GPU subsample-mask generator on its own stream (kernels_mask.cuh).  One
 // cluster launch parses a chunk of up to kChunk trees back to back (the u32
@@ -877,9 +1101,15 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   // sibling subtraction needs parent = left + right: a row with a missing
   // value at its node's cut feature stops at the node (trees.py:207-228), so
   // it is used only for NaN-free data
-  for (int l = 1; l <= s.depth; ++l) plans[l] = plan_layer<CodeT, NodeT>(l, s, c.sm_count, !any_nan);
-  BB_CUDA(cudaFuncSetAttribute(k_layer_hist<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-  BB_CUDA(cudaFuncSetAttribute(k_layer_hist_w<CodeT, NodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  std::vector<FlPlan> fl_plans(s.depth + 1);
+  int64_t part_elems = 0;
+  for (int l = 1; l <= s.depth; ++l) {
+    plans[l] = plan_layer<CodeT, NodeT>(l, s, c.sm_count, !any_nan);
+    fl_plans[l] = plan_fl<CodeT, NodeT>(l, s, c.sm_count, !any_nan, codes);
+    part_elems = std::max(part_elems, (int64_t)fl_grid(fl_plans[l]) * fl_cta_stride(fl_plans[l], s.B));
+  }
+  long long* fl_partials = part_elems ? A.alloc<long long>((size_t)part_elems) : nullptr;
+  set_hist_smem_attrs<CodeT, NodeT>();
 
   std::vector<NodeT> leaf_tmp;
   const bool prof = (cfg.flags & 1) != 0;
@@ -931,16 +1161,8 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         unsigned long long* hist = hbuf[layer & 1];
         unsigned long long* par = hbuf[(layer - 1) & 1];
         if (prof) hist_event();
-        if (p.n_fg * p.n_ng > hist_global_groups())
-          k_layer_hist_g<CodeT, NodeT><<<8 * c.sm_count, 256, 0, st>>>(codes, code_off, node, q, n, s.n_sig, s.d,
-                                                                       s.B, p, hist);
-        else if (hist_warp_mode())
-          k_layer_hist_w<CodeT, NodeT><<<hist_grid(p), kHistWThreads, p.smem, st>>>(codes, code_off, node, q, n,
-                                                                                   s.n_sig, s.d, s.B, p, hist);
-        else
-          k_layer_hist<CodeT, NodeT><<<hist_grid(p), kHistThreads, p.smem, st>>>(codes, code_off, node, q, n,
-                                                                                 s.n_sig, s.d, s.B, p, hist);
-        BB_LAUNCH_CHECK();
+        launch_layer_hist<CodeT, NodeT>(p, fl_plans[layer], c.sm_count, codes, code_off, node, q, n, s.n_sig, s.d,
+                                        s.B, hist, st, fl_partials);
         if (prof) hist_event();
         c.comm.all_reduce(hist, (size_t)2 * p.nodes * s.d * s.B, kNcclI64, kNcclSum, st);  // sharded fits
         stats.launches += 3;
@@ -1546,20 +1768,12 @@ int bb_layer_hist(bb_ctx* ctx, const uint16_t* codes, const uint16_t* node, cons
     const size_t hsz = (size_t)2 * p.nodes * d * B;
     unsigned long long* hist = A.alloc<unsigned long long>(hsz);
     BB_CUDA(cudaMemsetAsync(hist, 0, hsz * 8, st));
-    BB_CUDA(cudaFuncSetAttribute(k_layer_hist<uint16_t, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 227 * 1024));
-    BB_CUDA(cudaFuncSetAttribute(k_layer_hist_w<uint16_t, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 227 * 1024));
-    if (p.n_fg * p.n_ng > hist_global_groups())
-      k_layer_hist_g<uint16_t, uint16_t><<<8 * c.sm_count, 256, 0, st>>>(cd, 0, nd, qd, n, n_sig, d, B, p, hist);
-    else if (hist_warp_mode())
-      k_layer_hist_w<uint16_t, uint16_t><<<hist_grid(p), kHistWThreads, p.smem, st>>>(cd, 0, nd, qd, n, n_sig, d, B,
-                                                                                      p, hist);
-    else
-      k_layer_hist<uint16_t, uint16_t><<<hist_grid(p), kHistThreads, p.smem, st>>>(cd, 0, nd, qd, n, n_sig, d, B, p,
-                                                                                  hist);
+    const FlPlan fl = plan_fl<uint16_t, uint16_t>(layer, s, c.sm_count, false, cd);
+    set_hist_smem_attrs<uint16_t, uint16_t>();
+    const int64_t pe = (int64_t)fl_grid(fl) * fl_cta_stride(fl, B);
+    long long* partials = pe ? A.alloc<long long>((size_t)pe) : nullptr;
+    launch_layer_hist<uint16_t, uint16_t>(p, fl, c.sm_count, cd, 0, nd, qd, n, n_sig, d, B, hist, st, partials);
     BB_CUDA(cudaStreamSynchronize(st));  // host staging vector lives until here
-    BB_LAUNCH_CHECK();
     BB_CUDA(cudaMemcpyAsync(out_hist, hist, hsz * 8, cudaMemcpyDeviceToHost, st));
     BB_CUDA(cudaStreamSynchronize(st));
   });

@@ -138,19 +138,22 @@ def _oracle_hist(codes, node, q, n_sig, d, levels, layer):
     return out
 
 
-@pytest.fixture(params=["warp", "cta", "global"])
+@pytest.fixture(params=["fl", "fl_partials", "warp", "cta", "global"])
 def hist_path(request, monkeypatch):
-    """Every histogram kernel: the warp-independent shared-memory one
-    (default), the CTA-barrier one (BB_HIST_WARP=0) and the global-atomic one
-    (forced with BB_HIST_GLOBAL_GROUPS=0)."""
-    if request.param == "cta":
-        monkeypatch.setenv("BB_HIST_WARP", "0")
-    if request.param == "global":
-        monkeypatch.setenv("BB_HIST_GLOBAL_GROUPS", "0")
+    """Every histogram kernel: the feature-lane one (default where its plan
+    fits; TMA bulk reductions into the histogram, or with BB_FL_PARTIALS=1
+    per-CTA partial rows summed by k_fl_reduce), the warp-independent
+    shared-memory one, the CTA-barrier one and the global-atomic one
+    (BB_HIST_PATH = fl | w | cta | g)."""
+    monkeypatch.setenv("BB_HIST_PATH", {"fl": "fl", "fl_partials": "fl", "warp": "w", "cta": "cta", "global": "g"}[
+        request.param])
+    if request.param == "fl_partials":
+        monkeypatch.setenv("BB_FL_PARTIALS", "1")
     return request.param
 
 
-@pytest.mark.parametrize("levels,layer,d", [(8, 1, 10), (8, 3, 40), (8, 5, 7), (10, 6, 3), (3, 2, 5), (1, 1, 2)])
+@pytest.mark.parametrize("levels,layer,d", [(8, 1, 10), (8, 3, 40), (8, 5, 7), (10, 6, 3), (3, 2, 5), (1, 1, 2),
+                                             (8, 2, 50), (8, 4, 33), (6, 3, 17), (8, 2, 70), (4, 3, 100)])
 def test_layer_hist_exact(levels, layer, d, hist_path):
     rng = np.random.default_rng(levels * 100 + layer)
     n, n_sig = 60_000, 23_456
@@ -158,6 +161,23 @@ def test_layer_hist_exact(levels, layer, d, hist_path):
     B = 1 << levels
     nodes = 1 << (layer - 1)
     out = np.zeros((2, nodes, d, B), np.int64)
+    _lib.check(_lib.lib().bb_layer_hist(_lib.context(), _lib.ptr(codes), _lib.ptr(node), _lib.ptr(q), n, n_sig, d,
+                                        levels, layer, _lib.ptr(out)))
+    np.testing.assert_array_equal(out, _oracle_hist(codes, node, q, n_sig, d, levels, layer))
+
+
+def test_layer_hist_fl_long_runs(monkeypatch):
+    """Feature-lane kernel with > kFlFlushStages stages per CTA (mid-run
+    flushes of the 16/16-bit limbs) and the largest |q| (2^32 - 1)."""
+    monkeypatch.setenv("BB_HIST_PATH", "fl")
+    rng = np.random.default_rng(5)
+    n, n_sig, d, levels, layer = 3_000_000, 1_100_001, 2, 8, 2
+    codes, node, q = _random_layer(rng, n, n_sig, d, levels, layer)
+    q[::7] = (1 << 32) - 1
+    q[3::11] = -((1 << 32) - 1)
+    codes[1, : n // 2] = 17  # one tied bin takes half the rows
+    B = 1 << levels
+    out = np.zeros((2, 1 << (layer - 1), d, B), np.int64)
     _lib.check(_lib.lib().bb_layer_hist(_lib.context(), _lib.ptr(codes), _lib.ptr(node), _lib.ptr(q), n, n_sig, d,
                                         levels, layer, _lib.ptr(out)))
     np.testing.assert_array_equal(out, _oracle_hist(codes, node, q, n_sig, d, levels, layer))

@@ -1411,6 +1411,11 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   double ms_trees = 0.0;
   auto launch_codes = [&](auto* codes, int off) {
     using CodeT = std::remove_pointer_t<decltype(codes)>;
+    // padding rows of the last tile hold code 0: the feature-lane histogram
+    // adds zeros for rows that do not contribute, at their (in-range) codes
+    if (n % kTile)
+      BB_CUDA(cudaMemsetAsync(codes + (size_t)(ceil_div(n, kTile) - 1) * d * kTile, 0, (size_t)d * kTile * sizeof(CodeT),
+                              st));
     k_codes<K, CodeT><<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256 * 4), 4 * c.sm_count / d + 1)), d),
                         256, (size_t)nt * sizeof(K), st>>>(keys, n, nt, bkeys, pos, codes, stride, off, d, 1);
     BB_LAUNCH_CHECK();

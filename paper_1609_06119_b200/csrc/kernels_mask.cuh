@@ -102,12 +102,7 @@ __global__ void k_pcg_draws(const PcgJump* __restrict__ Jp, const RngState* __re
 }
 
 __device__ __forceinline__ unsigned int smear(unsigned int x) {
-  x |= x >> 1;
-  x |= x >> 2;
-  x |= x >> 4;
-  x |= x >> 8;
-  x |= x >> 16;
-  return x;
+  return x ? (0xffffffffu >> __clz((int)x)) : 0u;  // smallest 2^k - 1 >= x
 }
 
 // ----------------------------------------------------------- resolution

@@ -54,7 +54,10 @@ constexpr int kSegTail = 4096;     // states below this: walked by phase 2
 constexpr int kSegThreads = 32 * kSubPerCta;
 constexpr int kSegRing = 16;       // segments of records in flight in k_seg_compose
 constexpr int kRows = 16;          // rows of 32 draws classified at once by phase 1 (512-draw chunks)
-constexpr int kScalarBelow = 64;   // walk states below this one draw at a time
+constexpr int kScalarBelow = 64;
+#ifndef BB_WALK_ROWS_SHIFT
+#define BB_WALK_ROWS_SHIFT 0
+#endif   // walk states below this one draw at a time
 
 __host__ __device__ __forceinline__ unsigned int smear_host(unsigned int x) {
   x |= x >> 1;
@@ -462,18 +465,65 @@ __device__ int warp_walk(const unsigned int* src, int len, int i, int k, int* J,
     const unsigned int M = smear((unsigned)i);
     const int d = i - (int)(M >> 1);  // accepts until the band's last step
     int taken, consumed;
-    if (M >= (1u << 17) - 1)
+    constexpr int sh = 2 * BB_WALK_ROWS_SHIFT;  // rows per chunk x 2^BB_WALK_ROWS_SHIFT at a given band
+    if (M >= (1u << (17 - sh)) - 1)
       walk_chunk<16, kGlobal>(src, pos, len, i, d, M, k, J, lane, taken, consumed);
-    else if (M >= (1u << 15) - 1)
+    else if (M >= (1u << (15 - sh)) - 1)
       walk_chunk<8, kGlobal>(src, pos, len, i, d, M, k, J, lane, taken, consumed);
-    else if (M >= (1u << 13) - 1)
+    else if (M >= (1u << (13 - sh)) - 1)
       walk_chunk<4, kGlobal>(src, pos, len, i, d, M, k, J, lane, taken, consumed);
-    else if (M >= (1u << 11) - 1)
+    else if (M >= (1u << (11 - sh)) - 1)
       walk_chunk<2, kGlobal>(src, pos, len, i, d, M, k, J, lane, taken, consumed);
     else
       walk_chunk<1, kGlobal>(src, pos, len, i, d, M, k, J, lane, taken, consumed);
     i -= taken;
     pos += consumed;
+  }
+  *used = pos;
+  return i;
+}
+
+// Lean exact walk (one warp, one draw per lane per chunk of 32): sure accept
+// x <= i - r, sure reject x > i, the few ambiguous draws resolved in draw
+// order (accepted iff x <= i - accepted-before); the band's last step (or the
+// job's end) cuts the chunk.  Used where the per-chunk latency is what counts
+// (the tail's low states, the short crossing-zone segments of the chain):
+// the next chunk's draws are loaded while this one resolves.
+__device__ int lean_walk(const unsigned int* src, int len, int i, int k, int* J, int lane, int* used) {
+  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
+  int pos = 0;
+  unsigned int raw = lane < len ? src[lane] : 0u;
+  while (pos < len && i >= 1) {
+    const unsigned int M = smear((unsigned)i);
+    const int need = i - (int)(M >> 1);  // accepts to the band's last step
+    const bool in = pos + lane < len;
+    const int x = (int)(raw & M);
+    const unsigned int nxt = pos + 32 + lane < len ? src[pos + 32 + lane] : 0u;
+    unsigned acc = __ballot_sync(FULL, in && x <= i - lane);
+    unsigned am = __ballot_sync(FULL, in && x > i - lane && x <= i);
+    while (am) {
+      const int r = __ffs(am) - 1;
+      const int xr = __shfl_sync(FULL, x, r);
+      if (xr <= i - __popc(acc & ((1u << r) - 1u))) acc |= 1u << r;
+      am &= am - 1u;
+    }
+    const int cnt = __popc(acc);
+    int consumed = min(32, len - pos), taken = cnt;
+    if (cnt >= need) {
+      unsigned mm = acc;
+      for (int z = 1; z < need; ++z) mm &= mm - 1u;
+      const int cut = __ffs(mm) - 1;
+      consumed = cut + 1;
+      taken = need;
+      acc &= cut >= 31 ? FULL : ((2u << cut) - 1u);
+    }
+    if (J && i >= k) {
+      const int st = i - __popc(acc & lt);
+      if (((acc >> lane) & 1u) && st >= k) J[st] = x;
+    }
+    i -= taken;
+    pos += consumed;
+    raw = consumed == 32 ? nxt : (pos + lane < len ? src[pos + lane] : 0u);
   }
   *used = pos;
   return i;
@@ -559,7 +609,7 @@ struct StageWalk {
   uint64_t* bar;
   unsigned phase;
   __device__ int operator()(const SegArgs& a, const RngState& r0, long long base, long long len, int i, int k, int* J,
-                            int lane, long long* used) {
+                            int lane, long long* used, bool lean = false) {
     long long done = 0;
     while (done < len && i >= 1) {
       const long long b = base + done;
@@ -577,7 +627,7 @@ struct StageWalk {
         }
         mbar_wait(bar, phase);
         phase ^= 1u;
-        i = warp_walk<false>(sd + o, n, i, k, J, lane, &u);
+        i = lean ? lean_walk(sd + o, n, i, k, J, lane, &u) : warp_walk<false>(sd + o, n, i, k, J, lane, &u);
       } else {
         i = warp_walk_slow(a, r0, b, n, i, k, J, lane, &u);
       }
@@ -712,7 +762,7 @@ __global__ void __launch_bounds__(64) k_seg_chain(SegArgs a) {
       // J values are emitted by phase 3
       const long long cr = clock64();
       long long used;
-      next = walk(a, r0, anc + off, len, i, jb.k, nullptr, lane, &used);
+      next = walk(a, r0, anc + off, len, i, jb.k, nullptr, lane, &used, true);
       c_resim += clock64() - cr;
       ++n_resim;
     }
@@ -760,7 +810,7 @@ __global__ void __launch_bounds__(32) k_seg_tail(SegArgs a) {
   long long tail = 0;
   while (i >= 1) {
     long long used;
-    i = walk(a, r0, p, 8 * kSegMaxLen, i, jb.k, jb.J, lane, &used);
+    i = walk(a, r0, p, 8 * kSegMaxLen, i, jb.k, jb.J, lane, &used, true);
     p += used;
     tail += used;
   }

@@ -1,5 +1,6 @@
 // Shared device/host helpers for the FastBDT B200 hot path.
 #pragma once
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -20,7 +21,17 @@ struct CudaError {
       throw ::bb::CudaError{std::string(#call) + ": " + cudaGetErrorString(e_) + " (" + \
                             __FILE__ + ":" + std::to_string(__LINE__) + ")"};           \
   } while (0)
-#define BB_LAUNCH_CHECK() BB_CUDA(cudaGetLastError())
+// BB_SYNC_DEBUG=1: synchronise after every launch so a faulting kernel is
+// reported at its own launch site (debug only)
+inline bool sync_debug() {
+  static const bool on = getenv("BB_SYNC_DEBUG") != nullptr;
+  return on;
+}
+#define BB_LAUNCH_CHECK()                                   \
+  do {                                                      \
+    BB_CUDA(cudaGetLastError());                            \
+    if (::bb::sync_debug()) BB_CUDA(cudaDeviceSynchronize()); \
+  } while (0)
 
 struct InvalidArg {
   std::string msg;

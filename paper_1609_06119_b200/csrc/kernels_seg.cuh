@@ -49,7 +49,11 @@ constexpr int kAnchorSlackMin = 512;   // a job's segments start at its predicte
 constexpr int kAnchorSlackMax = 4000;  // 5 sd of a job's draw count, clamped to this range
 constexpr int kSub = 512;          // states per phase-1 sub-window (one warp)
 constexpr int kSubPerCta = 8;      // sub-windows per phase-1 CTA (= warps per k_seg_pass CTA)
-constexpr int kSegMaxSub = 32;     // sub-windows per segment (max)
+constexpr int kSegMaxSub = 64;     // sub-windows per segment (max)
+// half-window cap (states): 5 sd of a 29M-draw stretch (a 20M-row class
+// block, cfg5) is ~13.5k states; with the cap below that, a deviated path
+// misses every later window and the chain degenerates into an exact walk
+constexpr double kSegHalfWindowCap = 14336.0;
 constexpr int kSegTail = 4096;     // states below this: walked by phase 2
 constexpr int kSegThreads = 32 * kSubPerCta;
 constexpr int kSegRing = 16;       // segments of records in flight in k_seg_compose
@@ -112,7 +116,7 @@ __host__ __device__ inline double seg_expected_draws(int i0) {
 #define BB_SEG_WINDOW_SD 5.0
 #endif
 __host__ __device__ inline double seg_half_window(double p) {
-  return p <= 0.0 ? 0.0 : fmin(4096.0, ceil(0.5 * BB_SEG_WINDOW_SD * sqrt(p)) + 16.0);
+  return p <= 0.0 ? 0.0 : fmin(kSegHalfWindowCap, ceil(0.5 * BB_SEG_WINDOW_SD * sqrt(p)) + 16.0);
 }
 
 // Geometry of the segment at draw offset `off` of a stretch that starts at
@@ -131,7 +135,9 @@ __host__ __device__ inline bool seg_geom(int i0, long long off, int floor_state,
   // stop once the state is below the floor with 3 sd to spare: the window cap
   // (4096) would otherwise keep hi above a low floor forever; a job that is
   // still above the floor after the last segment walks the rest exactly
-  if (pi + 1.5 * sqrt((double)(off + slack)) < (double)floor_state) return false;
+  // (the 3-sd margin is capped at half the floor: for large jobs it exceeds
+  // the floor itself and the plan would never end)
+  if (pi + fmin(1.5 * sqrt((double)(off + slack)), 0.5 * floor_state) < (double)floor_state) return false;
   t->off = (int)off;
   const unsigned Mh = smear_host((unsigned)hi);
   const int bbA = (int)(Mh >> 1) + 1;
@@ -147,6 +153,23 @@ __host__ __device__ inline bool seg_geom(int i0, long long off, int floor_state,
     const int bbB = (int)(MB >> 1) + 1;
     t->loB = lo > bbB ? lo : bbB;
     t->nB = (t->hiB - t->loB + kSub) / kSub;
+  }
+  // at most kSegMaxSub sub-windows (the chain's record slots): trim the far
+  // ends (a start outside the window is walked exactly)
+  if (t->nA > kSegMaxSub) {
+    t->nA = kSegMaxSub;
+    t->loA = t->hiA - kSegMaxSub * kSub + 1;
+    t->loB = 1;
+    t->hiB = 0;
+    t->nB = 0;
+  } else if (t->nA + t->nB > kSegMaxSub) {
+    t->nB = kSegMaxSub - t->nA;
+    t->loB = t->hiB - t->nB * kSub + 1;
+    if (t->nB <= 0) {
+      t->nB = 0;
+      t->loB = 1;
+      t->hiB = 0;
+    }
   }
   const unsigned M = smear_host((unsigned)(pi > 1.0 ? (int)pi : 1));
   const double L = 0.176 * ((double)M + 1.0);

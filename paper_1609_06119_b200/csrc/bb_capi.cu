@@ -429,6 +429,12 @@ static FlPlan plan_fl(int layer, const FitShape& s, int sm_count, bool sib_ok, c
   if (!ok) return FlPlan{};
   const int nc_fit = (kSmemMax - fixed0 - p.stages * p.stage_bytes) / (nsub * subb);
   const int n_ng = (int)ceil_div(built, std::min(built, nc_fit));
+  // one node group only: every further group re-reads all rows for a
+  // shrinking share of contributing ones (measured: cfg3 layers 3-5 at 2, 4,
+  // 8 groups run 1.5-2.7x slower than the warp-independent kernel, which
+  // holds all of a layer's nodes); BB_HIST_PATH=fl forces it
+  const char* pe = getenv("BB_HIST_PATH");
+  if (n_ng > 1 && !(pe && !strcmp(pe, "fl"))) return FlPlan{};
   p.ngs = (int)ceil_div(built, n_ng);
   p.hist_bytes = p.ngs * nsub * subb;
   p.smem = fixed0 + p.stages * p.stage_bytes + p.hist_bytes;

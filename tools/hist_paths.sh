@@ -4,12 +4,12 @@
 run() {
   echo "== $1"
   env $2 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_layer_hist --csv \
-    python tools/prof_fit.py --trees 4 --reps 1 --host-masks 2>/dev/null | python -c "
+    python tools/prof_fit.py ${PF_ARGS:---trees 4 --reps 1 --host-masks} 2>/dev/null | python -c "
 import csv,sys
 rows=[r for r in csv.reader(sys.stdin) if len(r)>10]
 h=rows[0]; i=h.index('Metric Value'); u=h.index('Metric Unit'); k=h.index('Kernel Name')
 v=[float(r[i].replace(',',''))*(1e-3 if r[u] in ('nsecond','ns') else 1) for r in rows[1:]]
-print('kernel', rows[1][k][:40], 'launches', len(v), 'avg us %.1f' % (sum(v)/len(v)), 'per layer', ['%.1f' % x for x in v[:6]])
+L=int(__import__('os').environ.get('PF_DEPTH','3')); print('kernel', rows[1][k][:40], 'launches', len(v), 'avg us %.1f' % (sum(v)/len(v)), 'per layer', ['%.1f' % (sum(v[l::L])/len(v[l::L])) for l in range(L)])
 "
 }
 run fl BB_HIST_PATH=fl

@@ -280,7 +280,7 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, bool sib_
   p.sib = (sib_ok && layer >= 2) ? 1 : 0;  // left children only; right = parent - left (k_split)
   const int built = p.sib ? p.nodes / 2 : p.nodes;
   constexpr int64_t kSmemMax = 227 * 1024 - 1024;
-  static const int64_t hist_budget = (getenv("BB_HIST_BUDGET_KB") ? atoi(getenv("BB_HIST_BUDGET_KB")) : 96) * 1024;
+  static const int64_t hist_budget = (getenv("BB_HIST_BUDGET_KB") ? atoi(getenv("BB_HIST_BUDGET_KB")) : 128) * 1024;
   const int64_t fn_budget = std::max<int64_t>(1, hist_budget / ((int64_t)s.B * 8));
   if (built <= fn_budget) {
     p.ngs = built;
@@ -326,7 +326,7 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, bool sib_
 // re-reads every row) use the global-atomic histogram instead
 static int hist_global_groups() {
   const char* e = getenv("BB_HIST_GLOBAL_GROUPS");  // read per call: tests force either path
-  return e ? atoi(e) : 16;
+  return e ? atoi(e) : 40;  // cfg5 (B = 1024): the warp kernel wins up to ~34 groups (profiles)
 }
 
 static bool hist_warp_mode() {  // the warp-independent histogram kernel (BB_HIST_WARP=0: the CTA-barrier one)

@@ -54,7 +54,10 @@ constexpr int kSegMaxSub = 64;     // sub-windows per segment (max)
 // block, cfg5) is ~13.5k states; with the cap below that, a deviated path
 // misses every later window and the chain degenerates into an exact walk
 constexpr double kSegHalfWindowCap = 14336.0;
-constexpr int kSegTail = 4096;     // states below this: walked by phase 2
+#ifndef BB_SEG_TAIL
+#define BB_SEG_TAIL 2048
+#endif
+constexpr int kSegTail = BB_SEG_TAIL;     // states below this: walked by phase 2
 constexpr int kSegThreads = 32 * kSubPerCta;
 constexpr int kSegRing = 16;       // segments of records in flight in k_seg_compose
 constexpr int kRows = 16;          // rows of 32 draws classified at once by phase 1 (512-draw chunks)

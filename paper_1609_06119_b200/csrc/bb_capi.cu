@@ -739,6 +739,7 @@ struct MaskGen {
     for (int q = 0; q < 2; ++q) BB_CUDA(cudaEventCreateWithFlags(&evR[q], cudaEventDisableTiming));
     rng0 = A.alloc<RngState>(1);
     BB_CUDA(cudaFuncSetAttribute(k_seg_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegPassSmem));
+    BB_CUDA(cudaFuncSetAttribute(k_seg_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegTailSmem));
     BB_CUDA(cudaFuncSetAttribute(k_seg_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegComposeSmem));
   }
   void sync() {
@@ -862,7 +863,7 @@ struct MaskGen {
       k_seg_chain<<<1, 64, kSegComposeSmem, st>>>(a);
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaEventRecord(evC, st));
-      k_seg_tail<<<1, 32, 0, st>>>(a);
+      k_seg_tail<<<1, 32, kSegTailSmem, st>>>(a);
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaEventRecord(evTl, st));
       launches += 2;

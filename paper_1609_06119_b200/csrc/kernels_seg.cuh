@@ -43,7 +43,10 @@
 
 namespace bb {
 
-constexpr int kSegMaxLen = 8192;   // draws per segment (max)
+#ifndef BB_SEG_MAXLEN
+#define BB_SEG_MAXLEN 8192
+#endif
+constexpr int kSegMaxLen = BB_SEG_MAXLEN;   // draws per segment (max)
 constexpr int kSegCrossLen = 1024; // draws per segment in band-crossing zones
 constexpr int kAnchorSlackMin = 512;   // a job's segments start at its predicted first draw + a slack of
 constexpr int kAnchorSlackMax = 4000;  // 5 sd of a job's draw count, clamped to this range
@@ -818,8 +821,9 @@ __global__ void __launch_bounds__(64) k_seg_chain(SegArgs a) {
 
 // phase 2b: one warp walks the tail (states below kSegTail) to the job's
 // last draw, writing J for steps >= k; the next draw is the next job's first.
+constexpr int kSegTailSmem = (kSegMaxLen + 16) * 4;
 __global__ void __launch_bounds__(32) k_seg_tail(SegArgs a) {
-  __shared__ __align__(16) unsigned int sd[kSegMaxLen + 16];
+  extern __shared__ __align__(16) unsigned int sd[];  // kSegMaxLen + 16 draws
   __shared__ __align__(8) uint64_t st_bar;
   const int lane = threadIdx.x;
   const SegJob& jb = a.func;

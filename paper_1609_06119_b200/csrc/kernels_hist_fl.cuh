@@ -42,7 +42,7 @@ constexpr int kFlRows = 512;          // rows per stage (half a code tile)
 constexpr int kFlMaxStages = 3;       // ring depth (2 when the type's boxes are wide)
 constexpr int kFlWarps = 16;          // compute warps (32 rows each per stage)
 constexpr int kFlThreads = 32 * (kFlWarps + 1);
-constexpr int kFlFlushStages = 32;    // copy slot adds per flush < 2^15 (32 * 512 / R rows)
+constexpr int kFlFlushStages = 63;    // copy slot adds per flush < 2^15 (at most 63 * 512 / R rows)
 constexpr int kFlMaxTypes = 80;
 constexpr int kFlMetaBytes = kFlWarps * 32 * 16;
 #ifndef BB_FL_DENSE

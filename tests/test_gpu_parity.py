@@ -167,11 +167,11 @@ def test_layer_hist_exact(levels, layer, d, hist_path):
 
 
 def test_layer_hist_fl_long_runs(monkeypatch):
-    """Feature-lane kernel with > kFlFlushStages stages per CTA (mid-run
+    """Feature-lane kernel with > kFlFlushStages (63) stages per CTA (mid-run
     flushes of the 16/16-bit limbs) and the largest |q| (2^32 - 1)."""
     monkeypatch.setenv("BB_HIST_PATH", "fl")
     rng = np.random.default_rng(5)
-    n, n_sig, d, levels, layer = 3_000_000, 1_100_001, 2, 8, 2
+    n, n_sig, d, levels, layer = 6_000_000, 2_200_001, 2, 8, 2
     codes, node, q = _random_layer(rng, n, n_sig, d, levels, layer)
     q[::7] = (1 << 32) - 1
     q[3::11] = -((1 << 32) - 1)

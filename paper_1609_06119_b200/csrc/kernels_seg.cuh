@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(64) k_seg_chain(SegArgs a) {
   SegTab* tring = reinterpret_cast<SegTab*>(cs_sm + (size_t)kSegRing * kSegMaxSub * sizeof(SegRec));
   unsigned int* sd = reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned char*>(tring) +
                                                     (size_t)kTabChunk * kTabChunks * sizeof(SegTab));
-  __shared__ SegTab slot_tab[kSegRing];  // the table entry of the segment in each record slot
+  __shared__ __align__(16) SegTab slot_tab[kSegRing];  // the table entry of the segment in each record slot
   __shared__ __align__(8) uint64_t tab_bar[kTabChunks], full_bar[kSegRing], empty_bar[kSegRing], st_bar;
   __shared__ int s_s0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -767,23 +767,25 @@ __global__ void __launch_bounds__(64) k_seg_chain(SegArgs a) {
     mbar_wait(&full_bar[slot], (unsigned)((rs / kSegRing) & 1));
     if (lane == 0) a.seg_start[s] = i;
     const SegTab& t = slot_tab[slot];
-    int j = -1, lo = 0;
-    if (i >= t.loA && i <= t.hiA) {
-      j = (i - t.loA) / kSub;
-      lo = t.loA + kSub * j;
-    } else if (t.nB > 0 && i >= t.loB && i <= t.hiB) {
-      j = t.nA + (i - t.loB) / kSub;
-      lo = t.loB + kSub * (j - t.nA);
-    }
+    // record lookup, branch-free: piece A [loA, hiA] or B [loB, hiB] (nB > 0),
+    // sub-window j = offset / kSub, rank r = offset % kSub
+    const int4 ta4 = *reinterpret_cast<const int4*>(&t);                                   // off, len, loA, nA
+    const int4 tb4 = *reinterpret_cast<const int4*>(reinterpret_cast<const int*>(&t) + 4);  // hiA, loB, nB, hiB
+    const int dA = i - ta4.z, dB = i - tb4.y;
+    const bool inA = (unsigned)dA <= (unsigned)(tb4.x - ta4.z);
+    const bool inB = tb4.z > 0 && (unsigned)dB <= (unsigned)(tb4.w - tb4.y);
+    const int dd = inA ? dA : dB;
+    const int j = (inA ? 0 : ta4.w) + (int)((unsigned)dd / kSub);
     int next = -1;
-    if (j >= 0) {
+    if (inA || inB) {
       const SegRec& R = ring[slot * kSegMaxSub + j];
-      const int r = i - lo, w = r >> 5, bt = r & 31;
+      const int r = (int)((unsigned)dd % kSub), w = r >> 5, bt = r & 31;
       const unsigned int m = bt == 31 ? 0xffffffffu : ((2u << bt) - 1u);
-      const int e = R.a_end + (int)R.pref[w] + __popc(R.words[w] & m);
-      if (e > R.h) next = e;
+      const int2 ah = *reinterpret_cast<const int2*>(&R.a_end);  // a_end, h
+      const int e = ah.x + (int)R.pref[w] + __popc(R.words[w] & m);
+      if (e > ah.y) next = e;
     }
-    const int off = t.off, len = t.len;
+    const int off = ta4.x, len = ta4.y;
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty_bar[slot])) : "memory");
     if (next < 0) {

@@ -65,6 +65,10 @@ constexpr int kSegThreads = 32 * kSubPerCta;
 constexpr int kSegRing = 16;       // segments of records in flight in k_seg_compose
 constexpr int kRows = 16;          // rows of 32 draws classified at once by phase 1 (512-draw chunks)
 constexpr int kScalarBelow = 64;
+// lean_walk for the tail (states < kSegTail: 3.8M vs 4.5M cycles per 80 cfg2
+// jobs with warp_walk); warp_walk for the crossing-zone re-walks (2-4x faster
+// at high states, tools/microbench/crosswalk.cu)
+constexpr bool kLeanTail = true, kLeanResim = false;
 #ifndef BB_WALK_ROWS_SHIFT
 #define BB_WALK_ROWS_SHIFT 0
 #endif   // walk states below this one draw at a time
@@ -227,7 +231,15 @@ struct SegArgs {
 
 constexpr int kSegPassSmem = kSegMaxLen * 4;
 constexpr int kTabChunk = 64, kTabChunks = 4;  // table entries streamed into k_seg_compose
-constexpr int kSegComposeSmem = kSegRing * kSegMaxSub * 128 + kTabChunk * kTabChunks * 48 + (kSegMaxLen + 16) * 4;
+#ifndef BB_CHAIN_SMEM_KB
+#define BB_CHAIN_SMEM_KB 0
+#endif
+// dynamic shared memory of the chain kernel; BB_CHAIN_SMEM_KB pads it so that
+// no other CTA can share the chain's SM (its single-warp dependent chains
+// lose issue slots to co-resident phase-1 warps)
+constexpr int kSegComposeSmemUsed = kSegRing * kSegMaxSub * 128 + kTabChunk * kTabChunks * 48 + (kSegMaxLen + 16) * 4;
+constexpr int kSegComposeSmem =
+    kSegComposeSmemUsed > BB_CHAIN_SMEM_KB * 1024 ? kSegComposeSmemUsed : BB_CHAIN_SMEM_KB * 1024;
 
 __device__ __forceinline__ unsigned int seg_get(const SegArgs& a, const RngState& r0, long long idx) {
   return idx < a.n_draws ? __ldg(&a.draws[idx]) : draw_at(*a.jump, r0, idx);
@@ -793,7 +805,7 @@ __global__ void __launch_bounds__(64) k_seg_chain(SegArgs a) {
       // J values are emitted by phase 3
       const long long cr = clock64();
       long long used;
-      next = walk(a, r0, anc + off, len, i, jb.k, nullptr, lane, &used, true);
+      next = walk(a, r0, anc + off, len, i, jb.k, nullptr, lane, &used, kLeanResim);
       c_resim += clock64() - cr;
       ++n_resim;
     }
@@ -842,7 +854,7 @@ __global__ void __launch_bounds__(32) k_seg_tail(SegArgs a) {
   long long tail = 0;
   while (i >= 1) {
     long long used;
-    i = walk(a, r0, p, 8 * kSegMaxLen, i, jb.k, jb.J, lane, &used, true);
+    i = walk(a, r0, p, 8 * kSegMaxLen, i, jb.k, jb.J, lane, &used, kLeanTail);
     p += used;
     tail += used;
   }

@@ -643,7 +643,9 @@ struct MaskGen {
   long long* sanchor = nullptr;  // anchor (predicted first draw + slack) of each job
   long long* stail = nullptr;    // chain -> tail hand-off: draw
   int* stail_i = nullptr;        //                         state
-  cudaStream_t sb = nullptr;     // phase 1 / 3 stream (overlaps the tails)
+  cudaStream_t sb = nullptr;     // phase 1 stream (overlaps the tails)
+  cudaStream_t se = nullptr;     // phase 3 (emit) stream: phase 1 of job j+2 does not queue behind emit(j)
+  cudaEvent_t evE[2] = {}, evEnd = nullptr;
   cudaStream_t sc = nullptr;     // value resolution + mask bits (overlaps the next chunk's parse)
   cudaEvent_t evA = nullptr, evB = nullptr;
   cudaEvent_t evT[kChunk] = {};  // tree t of the chunk emitted (sb -> sc)
@@ -735,6 +737,9 @@ struct MaskGen {
     BB_CUDA(cudaEventCreateWithFlags(&evTl, cudaEventDisableTiming));
     for (int q = 0; q < 2; ++q) BB_CUDA(cudaEventCreateWithFlags(&evF[q], cudaEventDisableTiming));
     BB_CUDA(cudaStreamCreateWithPriority(&sc, cudaStreamNonBlocking, hi_prio));
+    BB_CUDA(cudaStreamCreateWithPriority(&se, cudaStreamNonBlocking, hi_prio));
+    for (int q = 0; q < 2; ++q) BB_CUDA(cudaEventCreateWithFlags(&evE[q], cudaEventDisableTiming));
+    BB_CUDA(cudaEventCreateWithFlags(&evEnd, cudaEventDisableTiming));
     for (int q = 0; q < kChunk; ++q) BB_CUDA(cudaEventCreateWithFlags(&evT[q], cudaEventDisableTiming));
     for (int q = 0; q < 2; ++q) BB_CUDA(cudaEventCreateWithFlags(&evR[q], cudaEventDisableTiming));
     rng0 = A.alloc<RngState>(1);
@@ -744,9 +749,17 @@ struct MaskGen {
   }
   void sync() {
     if (sb) cudaStreamSynchronize(sb);
+    if (se) cudaStreamSynchronize(se);
     if (sc) cudaStreamSynchronize(sc);
   }
   ~MaskGen() {
+    if (se) {
+      cudaStreamSynchronize(se);
+      cudaStreamDestroy(se);
+    }
+    for (int q = 0; q < 2; ++q)
+      if (evE[q]) cudaEventDestroy(evE[q]);
+    if (evEnd) cudaEventDestroy(evEnd);
     if (sb) {
       cudaStreamSynchronize(sb);
       cudaStreamDestroy(sb);
@@ -834,22 +847,23 @@ struct MaskGen {
       }
       BB_CUDA(cudaEventRecord(evF[jj & 1], sb));
     };
-    auto emit = [&](int jj) {  // phase 3 of job jj (stream sb)
+    auto emit = [&](int jj) {  // phase 3 of job jj (stream se)
       const SegJob job = make_job(jj);
       const int nb = (int)ceil_div(job.S, kSubPerCta);
       if (nb > 0) {
         SegArgs a = args(jj);
         a.func = SegJob{};
         a.emit = job;
-        k_seg_pass<<<nb, kSegThreads, kSegPassSmem, sb>>>(a, 0);
+        k_seg_pass<<<nb, kSegThreads, kSegPassSmem, se>>>(a, 0);
         BB_LAUNCH_CHECK();
         launches += 1;
       }
     };
     // stream st: chain(j) -> tail(j) -> chain(j+1) ...  Stream sb: phase 1 of
     // job j+2 right after tail(j) (its anchor is then known), overlapping
-    // chain(j+1) + tail(j+1); phase 3 of job j after chain(j).  Records and
-    // segment starts alternate between two buffers by job parity.
+    // chain(j+1) + tail(j+1).  Stream se: phase 3 of job j after chain(j).
+    // Records and segment starts alternate between two buffers by job parity
+    // (chain(j+2) waits for emit(j), which reads the same seg_start).
     BB_CUDA(cudaEventRecord(evA, st));
     BB_CUDA(cudaStreamWaitEvent(sb, evA, 0));
     func(0);
@@ -859,7 +873,8 @@ struct MaskGen {
       SegArgs a = args(jj);
       a.func = job;
       a.emit = SegJob{};
-      BB_CUDA(cudaStreamWaitEvent(st, evF[jj & 1], 0));  // phase 1 of job jj (and emit of jj-2) done
+      BB_CUDA(cudaStreamWaitEvent(st, evF[jj & 1], 0));  // phase 1 of job jj done
+      if (jj >= 2) BB_CUDA(cudaStreamWaitEvent(st, evE[jj & 1], 0));  // emit of jj-2 read this parity's seg_start
       k_seg_chain<<<1, 64, kSegComposeSmem, st>>>(a);
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaEventRecord(evC, st));
@@ -867,16 +882,19 @@ struct MaskGen {
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaEventRecord(evTl, st));
       launches += 2;
-      BB_CUDA(cudaStreamWaitEvent(sb, evC, 0));
+      BB_CUDA(cudaStreamWaitEvent(se, evC, 0));
       emit(jj);
-      if (jj & 1) BB_CUDA(cudaEventRecord(evT[jj >> 1], sb));  // both jobs of tree jj/2 emitted
+      BB_CUDA(cudaEventRecord(evE[jj & 1], se));
+      if (jj & 1) BB_CUDA(cudaEventRecord(evT[jj >> 1], se));  // both jobs of tree jj/2 emitted
       if (jj + 2 < jobs) {
         BB_CUDA(cudaStreamWaitEvent(sb, evTl, 0));
         func(jj + 2);
       }
     }
     BB_CUDA(cudaEventRecord(evB, sb));
-    BB_CUDA(cudaStreamWaitEvent(st, evB, 0));  // the next chunk's draws overwrite what the emits read
+    BB_CUDA(cudaStreamWaitEvent(st, evB, 0));
+    BB_CUDA(cudaEventRecord(evEnd, se));
+    BB_CUDA(cudaStreamWaitEvent(st, evEnd, 0));  // the next chunk's draws overwrite what the emits read
     return launches;
   }
 

@@ -646,6 +646,8 @@ struct MaskGen {
   cudaStream_t sb = nullptr;     // phase 1 stream (overlaps the tails)
   cudaStream_t se = nullptr;     // phase 3 (emit) stream: phase 1 of job j+2 does not queue behind emit(j)
   cudaEvent_t evE[2] = {}, evEnd = nullptr;
+  cudaStream_t sg = nullptr;     // the chunk's draws beyond the first two jobs
+  cudaEvent_t evPre = nullptr, evG2 = nullptr;
   cudaStream_t sc = nullptr;     // value resolution + mask bits (overlaps the next chunk's parse)
   cudaEvent_t evA = nullptr, evB = nullptr;
   cudaEvent_t evT[kChunk] = {};  // tree t of the chunk emitted (sb -> sc)
@@ -740,6 +742,9 @@ struct MaskGen {
     BB_CUDA(cudaStreamCreateWithPriority(&se, cudaStreamNonBlocking, hi_prio));
     for (int q = 0; q < 2; ++q) BB_CUDA(cudaEventCreateWithFlags(&evE[q], cudaEventDisableTiming));
     BB_CUDA(cudaEventCreateWithFlags(&evEnd, cudaEventDisableTiming));
+    BB_CUDA(cudaStreamCreateWithPriority(&sg, cudaStreamNonBlocking, hi_prio));
+    BB_CUDA(cudaEventCreateWithFlags(&evPre, cudaEventDisableTiming));
+    BB_CUDA(cudaEventCreateWithFlags(&evG2, cudaEventDisableTiming));
     for (int q = 0; q < kChunk; ++q) BB_CUDA(cudaEventCreateWithFlags(&evT[q], cudaEventDisableTiming));
     for (int q = 0; q < 2; ++q) BB_CUDA(cudaEventCreateWithFlags(&evR[q], cudaEventDisableTiming));
     rng0 = A.alloc<RngState>(1);
@@ -748,11 +753,18 @@ struct MaskGen {
     BB_CUDA(cudaFuncSetAttribute(k_seg_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, kSegComposeSmem));
   }
   void sync() {
+    if (sg) cudaStreamSynchronize(sg);
     if (sb) cudaStreamSynchronize(sb);
     if (se) cudaStreamSynchronize(se);
     if (sc) cudaStreamSynchronize(sc);
   }
   ~MaskGen() {
+    if (sg) {
+      cudaStreamSynchronize(sg);
+      cudaStreamDestroy(sg);
+    }
+    if (evPre) cudaEventDestroy(evPre);
+    if (evG2) cudaEventDestroy(evG2);
     if (se) {
       cudaStreamSynchronize(se);
       cudaStreamDestroy(se);
@@ -836,6 +848,7 @@ struct MaskGen {
       return job;
     };
     auto func = [&](int jj) {  // phase 1 of job jj (stream sb)
+      if (jj == 2) BB_CUDA(cudaStreamWaitEvent(sb, evG2, 0));  // draws beyond the first two jobs
       const SegJob job = make_job(jj);
       if (job.n_tasks > 0) {
         SegArgs a = args(jj);
@@ -874,6 +887,7 @@ struct MaskGen {
       a.func = job;
       a.emit = SegJob{};
       BB_CUDA(cudaStreamWaitEvent(st, evF[jj & 1], 0));  // phase 1 of job jj done
+      if (jj == 1) BB_CUDA(cudaStreamWaitEvent(st, evG2, 0));  // job 1 may read past the first part
       if (jj >= 2) BB_CUDA(cudaStreamWaitEvent(st, evE[jj & 1], 0));  // emit of jj-2 read this parity's seg_start
       k_seg_chain<<<1, 64, kSegComposeSmem, st>>>(a);
       BB_LAUNCH_CHECK();
@@ -902,9 +916,20 @@ struct MaskGen {
   // ready[j] (optional) recorded when tree j's bits are written
   void enqueue_chunk(cudaStream_t st, unsigned int* const* bits, int count, const cudaEvent_t* ready,
                      int64_t& launches) {
-    const long long n_out = (n_draws + 1) / 2;
-    k_pcg_draws<<<(unsigned)ceil_div(ceil_div(n_out, kDrawChunk), 256), 256, 0, st>>>(jump, rng, draws, n_draws);
-    BB_LAUNCH_CHECK();
+    // the first two jobs' draws on the critical stream, the rest on sg
+    // (waited by chain(1) and by phase 1 of jobs >= 2)
+    const long long n1 = std::min(n_draws, (long long)(1.25 * (double)(exp_draws[0] + exp_draws[1])) + 65536);
+    auto draws_part = [&](long long lo, long long hi, cudaStream_t s2) {
+      if (hi <= lo) return;
+      const long long outs = (hi - lo) / 2 + 2;
+      k_pcg_draws<<<(unsigned)ceil_div(ceil_div(outs, kDrawChunk), 256), 256, 0, s2>>>(jump, rng, draws, lo, hi);
+      BB_LAUNCH_CHECK();
+    };
+    BB_CUDA(cudaEventRecord(evPre, st));
+    draws_part(0, n1, st);
+    BB_CUDA(cudaStreamWaitEvent(sg, evPre, 0));
+    draws_part(n1, n_draws, sg);
+    BB_CUDA(cudaEventRecord(evG2, sg));
     BB_CUDA(cudaStreamWaitEvent(st, evR[parity], 0));  // J half free (no-op before its first use)
     launches += enqueue_seg(st, count) + 1;
     const long long stride = std::max(n[0], n[1]);

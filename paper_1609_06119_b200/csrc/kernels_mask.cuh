@@ -81,23 +81,26 @@ __device__ __forceinline__ unsigned int draw_at(const PcgJump& J, const RngState
 
 constexpr int kDrawChunk = 64;  // PCG outputs per thread
 
+// draws [j_lo, j_hi) of the buffer (a chunk's draws are generated in two
+// parts: the first jobs' range on the critical stream, the rest overlapped)
 __global__ void k_pcg_draws(const PcgJump* __restrict__ Jp, const RngState* __restrict__ rs,
-                            unsigned int* __restrict__ draws, long long n_draws) {
+                            unsigned int* __restrict__ draws, long long j_lo, long long j_hi) {
   const RngState r = *rs;
   const long long h = r.has_uint32 ? 1 : 0;
-  const long long n_out = (n_draws - h + 1) / 2;
-  const long long q0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kDrawChunk;
-  if (q0 >= n_out) return;
-  if (q0 == 0 && h) draws[0] = r.uinteger;
+  const long long out_lo = j_lo > h ? (j_lo - h) / 2 : 0;   // first output touching [j_lo, j_hi)
+  const long long out_hi = (j_hi - h + 1) / 2;              // outputs before this cover j < j_hi
+  const long long q0 = out_lo + ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kDrawChunk;
+  if (q0 >= out_hi) return;
+  if (q0 == 0 && h && j_lo == 0) draws[0] = r.uinteger;
   U128 s = pcg_jump(*Jp, r.s, (unsigned long long)q0);  // state before output q0
   const U128 a = Jp->A[0], c = Jp->C[0];
-  const long long q1 = min(n_out, q0 + kDrawChunk);
+  const long long q1 = min(out_hi, q0 + kDrawChunk);
   for (long long qq = q0; qq < q1; ++qq) {
     s = u128_add(u128_mul(a, s), c);
     const unsigned long long o = xsl_rr(s);
     const long long j = h + 2 * qq;
-    if (j < n_draws) draws[j] = (unsigned int)o;
-    if (j + 1 < n_draws) draws[j + 1] = (unsigned int)(o >> 32);
+    if (j >= j_lo && j < j_hi) draws[j] = (unsigned int)o;
+    if (j + 1 >= j_lo && j + 1 < j_hi) draws[j + 1] = (unsigned int)(o >> 32);
   }
 }
 

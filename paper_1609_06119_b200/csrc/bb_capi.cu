@@ -877,6 +877,10 @@ struct MaskGen {
     // chain(j+1) + tail(j+1).  Stream se: phase 3 of job j after chain(j).
     // Records and segment starts alternate between two buffers by job parity
     // (chain(j+2) waits for emit(j), which reads the same seg_start).
+    // BB_MASK_TIMELINE=1 (debug): per-job waits / chain / tail on the critical stream, printed at the end
+    static const bool mtl_on = getenv("BB_MASK_TIMELINE") != nullptr;
+    std::vector<cudaEvent_t> mtl;
+    if (mtl_on) { mtl.emplace_back(); BB_CUDA(cudaEventCreate(&mtl.back())); BB_CUDA(cudaEventRecord(mtl.back(), st)); }
     BB_CUDA(cudaEventRecord(evA, st));
     BB_CUDA(cudaStreamWaitEvent(sb, evA, 0));
     func(0);
@@ -889,12 +893,15 @@ struct MaskGen {
       BB_CUDA(cudaStreamWaitEvent(st, evF[jj & 1], 0));  // phase 1 of job jj done
       if (jj == 1) BB_CUDA(cudaStreamWaitEvent(st, evG2, 0));  // job 1 may read past the first part
       if (jj >= 2) BB_CUDA(cudaStreamWaitEvent(st, evE[jj & 1], 0));  // emit of jj-2 read this parity's seg_start
+      if (mtl_on) { mtl.emplace_back(); BB_CUDA(cudaEventCreate(&mtl.back())); BB_CUDA(cudaEventRecord(mtl.back(), st)); }
       k_seg_chain<<<1, 64, kSegComposeSmem, st>>>(a);
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaEventRecord(evC, st));
+      if (mtl_on) { mtl.emplace_back(); BB_CUDA(cudaEventCreate(&mtl.back())); BB_CUDA(cudaEventRecord(mtl.back(), st)); }
       k_seg_tail<<<1, 32, kSegTailSmem, st>>>(a);
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaEventRecord(evTl, st));
+      if (mtl_on) { mtl.emplace_back(); BB_CUDA(cudaEventCreate(&mtl.back())); BB_CUDA(cudaEventRecord(mtl.back(), st)); }
       launches += 2;
       BB_CUDA(cudaStreamWaitEvent(se, evC, 0));
       emit(jj);
@@ -909,6 +916,25 @@ struct MaskGen {
     BB_CUDA(cudaStreamWaitEvent(st, evB, 0));
     BB_CUDA(cudaEventRecord(evEnd, se));
     BB_CUDA(cudaStreamWaitEvent(st, evEnd, 0));  // the next chunk's draws overwrite what the emits read
+    if (mtl_on) {
+      mtl.emplace_back();
+      BB_CUDA(cudaEventCreate(&mtl.back()));
+      BB_CUDA(cudaEventRecord(mtl.back(), st));
+      BB_CUDA(cudaEventSynchronize(mtl.back()));
+      // events: start, then per job (before chain, before tail, after tail), then end
+      double wait = 0, chain = 0, tail = 0;
+      float x;
+      for (int jj = 0; jj < jobs; ++jj) {
+        cudaEvent_t prev = mtl[3 * jj], c0 = mtl[3 * jj + 1], t0 = mtl[3 * jj + 2], t1 = mtl[3 * jj + 3];
+        BB_CUDA(cudaEventElapsedTime(&x, prev, c0)); wait += x;
+        BB_CUDA(cudaEventElapsedTime(&x, c0, t0)); chain += x;
+        BB_CUDA(cudaEventElapsedTime(&x, t0, t1)); tail += x;
+      }
+      BB_CUDA(cudaEventElapsedTime(&x, mtl[3 * jobs], mtl.back()));
+      BB_CUDA(cudaEventElapsedTime(&x, mtl[0], mtl.back()));
+      fprintf(stderr, "mask chunk: %d jobs, total %.3f ms: waits %.3f, chains %.3f, tails %.3f\n", jobs, x, wait, chain, tail);
+      for (auto e : mtl) cudaEventDestroy(e);
+    }
     return launches;
   }
 

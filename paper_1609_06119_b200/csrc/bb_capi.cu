@@ -898,8 +898,10 @@ struct MaskGen {
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaEventRecord(evC, st));
       if (mtl_on) { mtl.emplace_back(); BB_CUDA(cudaEventCreate(&mtl.back())); BB_CUDA(cudaEventRecord(mtl.back(), st)); }
-      k_seg_tail<<<1, 32, kSegTailSmem, st>>>(a);
-      BB_LAUNCH_CHECK();
+      if (!kFuseTail) {
+        k_seg_tail<<<1, 32, kSegTailSmem, st>>>(a);
+        BB_LAUNCH_CHECK();
+      }
       BB_CUDA(cudaEventRecord(evTl, st));
       if (mtl_on) { mtl.emplace_back(); BB_CUDA(cudaEventCreate(&mtl.back())); BB_CUDA(cudaEventRecord(mtl.back(), st)); }
       launches += 2;

@@ -69,6 +69,7 @@ constexpr int kScalarBelow = 64;
 // jobs with warp_walk); warp_walk for the crossing-zone re-walks (2-4x faster
 // at high states, tools/microbench/crosswalk.cu)
 constexpr bool kLeanTail = true, kLeanResim = false;
+constexpr bool kFuseTail = false;  // true: the tail walk runs in the chain kernel (one launch per job; masks alone -1.5%, but the fit measured 3.07 vs 3.15 G rows*trees/s)
 #ifndef BB_WALK_ROWS_SHIFT
 #define BB_WALK_ROWS_SHIFT 0
 #endif   // walk states below this one draw at a time
@@ -680,6 +681,8 @@ struct StageWalk {
   }
 };
 
+__device__ void seg_tail_walk(const SegArgs& a, const RngState& r0, StageWalk& walk, long long p, int i, int lane);
+
 // phase 2a: two warps.  Warp 1 (producer) streams the table entries and
 // the segments' records into shared memory with bulk copies (full/empty
 // mbarriers per record slot) and prefetches the draws of band-crossing-zone
@@ -831,25 +834,16 @@ __global__ void __launch_bounds__(64) k_seg_chain(SegArgs a) {
       atomicAdd((unsigned long long*)&a.prof[13], (unsigned long long)s0);
     }
   }
+  if (kFuseTail) seg_tail_walk(a, r0, walk, p, i, lane);  // phase 2b in the same warp (one launch per job)
 }
 
 // phase 2b: one warp walks the tail (states below kSegTail) to the job's
 // last draw, writing J for steps >= k; the next draw is the next job's first.
 constexpr int kSegTailSmem = (kSegMaxLen + 16) * 4;
-__global__ void __launch_bounds__(32) k_seg_tail(SegArgs a) {
-  extern __shared__ __align__(16) unsigned int sd[];  // kSegMaxLen + 16 draws
-  __shared__ __align__(8) uint64_t st_bar;
-  const int lane = threadIdx.x;
+// phase 2b: walk the tail (states below kSegTail) from (p, i) to the job's
+// last draw, writing J for steps >= k; the next draw is the next job's first.
+__device__ void seg_tail_walk(const SegArgs& a, const RngState& r0, StageWalk& walk, long long p, int i, int lane) {
   const SegJob& jb = a.func;
-  const RngState r0 = *a.rng0;
-  if (lane == 0) {
-    mbar_init(&st_bar, 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  StageWalk walk{sd, &st_bar, 0u};
-  long long p = *a.tail_p;
-  int i = *a.tail_i;
   const long long ct = clock64();
   long long tail = 0;
   while (i >= 1) {
@@ -892,6 +886,20 @@ __global__ void __launch_bounds__(32) k_seg_tail(SegArgs a) {
       *a.rng = r;
     }
   }
+}
+
+__global__ void __launch_bounds__(32) k_seg_tail(SegArgs a) {
+  extern __shared__ __align__(16) unsigned int sd[];  // kSegMaxLen + 16 draws
+  __shared__ __align__(8) uint64_t st_bar;
+  const int lane = threadIdx.x;
+  const RngState r0 = *a.rng0;
+  if (lane == 0) {
+    mbar_init(&st_bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  StageWalk walk{sd, &st_bar, 0u};
+  seg_tail_walk(a, r0, walk, *a.tail_p, *a.tail_i, lane);
 }
 
 __global__ void k_seg_init(long long* pos, long long* anchor, long long a0, long long a1) {

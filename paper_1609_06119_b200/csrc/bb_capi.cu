@@ -280,7 +280,7 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, bool sib_
   p.sib = (sib_ok && layer >= 2) ? 1 : 0;  // left children only; right = parent - left (k_split)
   const int built = p.sib ? p.nodes / 2 : p.nodes;
   constexpr int64_t kSmemMax = 227 * 1024 - 1024;
-  static const int64_t hist_budget = (getenv("BB_HIST_BUDGET_KB") ? atoi(getenv("BB_HIST_BUDGET_KB")) : 128) * 1024;
+  static const int64_t hist_budget = (getenv("BB_HIST_BUDGET_KB") ? atoi(getenv("BB_HIST_BUDGET_KB")) : 160) * 1024;
   const int64_t fn_budget = std::max<int64_t>(1, hist_budget / ((int64_t)s.B * 8));
   if (built <= fn_budget) {
     p.ngs = built;
@@ -302,6 +302,10 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, bool sib_
     p.n_fg += 1;
     p.fg = (int)ceil_div(s.d, p.n_fg);
     p.n_fg = (int)ceil_div(s.d, p.fg);
+  }
+  while (p.ngs > 1 && need(p.fg) > kSmemMax) {  // a budget above what the stage leaves: fewer nodes per group
+    p.ngs -= 1;
+    p.n_ng = (int)ceil_div(built, p.ngs);
   }
   if (need(p.fg) > kSmemMax) throw InvalidArg{"histogram stage does not fit in shared memory"};
   p.tile = tile;

@@ -466,25 +466,29 @@ __global__ void __launch_bounds__(256)
                    const long long* __restrict__ q, int64_t n, int64_t n_sig, int d, int B, HistPlan p,
                    unsigned long long* __restrict__ hist) {
   const int nfb = (d + 7) >> 3;
-  const int64_t items = ((n + kTile - 1) / kTile) * kTile * nfb;  // whole tiles x feature blocks
-  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
-       it += (int64_t)gridDim.x * blockDim.x) {
-    // consecutive threads take consecutive rows of one feature block (coalesced codes)
-    const int64_t tile = it / ((int64_t)kTile * nfb);
-    const int64_t rem = it - tile * (int64_t)kTile * nfb;
-    const int fb = (int)(rem / kTile);
-    const int64_t r = tile * kTile + (rem - (int64_t)fb * kTile);
-    if (r >= n) continue;
-    const int ln = (int)node[r] - p.start;
-    if (ln < 0 || ln >= p.nodes || (p.sib && (ln & 1))) continue;
-    const long long qq = q[r];
-    if (qq == 0) continue;
-    const int cls = r >= n_sig ? 1 : 0;
-    const int64_t base = ((int64_t)cls * p.nodes + ln) * d;
-    const int f0 = fb * 8, f1 = min(d, f0 + 8);
-    for (int f = f0; f < f1; ++f) {
-      const int c = (int)codes[code_index(r, f, d)] + code_off;
-      if (c != 0) atomicAdd(&hist[(base + f) * B + (c - 1)], as_ull(qq));
+  const int per_tile = kTile * nfb;  // (feature block, row) items of a tile
+  const int64_t tiles = (n + kTile - 1) / kTile;
+  // grid-stride over tiles, 32-bit item math inside a tile (the 64-bit
+  // divisions of a flat item index cost more than the loads they address)
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const CodeT* ct = codes + tile * (int64_t)d * kTile;
+    for (int e = threadIdx.x; e < per_tile; e += blockDim.x) {
+      // consecutive threads take consecutive rows of one feature block (coalesced codes)
+      const int fb = e >> kTileLog, rl = e & (kTile - 1);
+      const int64_t r = tile * kTile + rl;
+      if (r >= n) continue;
+      const int ln = (int)node[r] - p.start;
+      if (ln < 0 || ln >= p.nodes || (p.sib && (ln & 1))) continue;
+      const long long qq = q[r];
+      if (qq == 0) continue;
+      const int cls = r >= n_sig ? 1 : 0;
+      unsigned long long* hb = hist + ((int64_t)cls * p.nodes + ln) * d * B - 1 + code_off;
+      const int f0 = fb * 8, f1 = min(d, f0 + 8);
+#pragma unroll 8
+      for (int f = f0; f < f1; ++f) {
+        const int c = (int)ct[f * kTile + rl];
+        if (c + code_off != 0) atomicAdd(hb + (int64_t)f * B + c, as_ull(qq));
+      }
     }
   }
 }

@@ -141,6 +141,12 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// TMA bulk reduction shared -> global (int64 add at L2; 16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_reduce_add_u64(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   const unsigned a = smem_u32(bar);
   unsigned ok = 0;

@@ -443,6 +443,32 @@ __global__ void __launch_bounds__(kHistWThreads, 1)
     }
   }
   __syncthreads();
+  // flush: int64 rows [node][feature][bin] staged in the drained ring, one TMA
+  // bulk reduction per row (scattered 64-bit global atomics cost ~1 LSU
+  // cycle per lane: ~10 us per CTA for cfg2's 20k slots)
+  const int cap_rows = (2 * bufb) / (B * 8);
+  if (cap_rows >= 1 && (B & 1) == 0) {
+    long long* st = reinterpret_cast<long long*>(stage);
+    const int rows = ncount * fcount;
+    for (int r0 = 0; r0 < rows; r0 += cap_rows) {
+      const int rn = min(cap_rows, rows - r0);
+      for (int e = threadIdx.x; e < rn * B; e += kHistWThreads) {
+        const int s = r0 * B + e;  // slot = (nd * fcount + j) * B + bin = row * B + bin
+        st[e] = (long long)(((unsigned long long)hi[s] << 32) | (unsigned long long)lo[s]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      for (int rl = threadIdx.x; rl < rn; rl += kHistWThreads) {
+        const int row = r0 + rl, nd = row / fcount, j = row - nd * fcount;
+        const int ln = p.sib ? 2 * (n0 + nd) : (n0 + nd);
+        bulk_reduce_add_u64(hist + (((int64_t)cls * p.nodes + ln) * d + (f0 + j)) * B, st + (size_t)rl * B,
+                            (unsigned)B * 8u);
+      }
+      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncthreads();
+    }
+    return;
+  }
   for (int s = threadIdx.x; s < nslots; s += kHistWThreads) {
     const long long v = (long long)(((unsigned long long)hi[s] << 32) | (unsigned long long)lo[s]);
     if (v != 0) {

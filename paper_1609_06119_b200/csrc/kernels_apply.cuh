@@ -160,6 +160,10 @@ __global__ void __launch_bounds__(kApplyRows) k_apply_f32(const float* __restric
 // walk over the original records (global memory; rare).
 constexpr int kApplyDRows = 256;
 constexpr int kApplyDTB = 64;  // trees per smem batch
+#ifndef BB_APPLY_ILP
+#define BB_APPLY_ILP 4
+#endif
+constexpr int kApplyDIlp = BB_APPLY_ILP;  // trees walked together per thread
 
 struct ApplyD {
   int n_trees;
@@ -220,19 +224,21 @@ __global__ void __launch_bounds__(kApplyDRows) k_apply_d(const float* __restrict
     const unsigned char* recb = reinterpret_cast<const unsigned char*>(s_rec);
     const unsigned char* leafb = reinterpret_cast<const unsigned char*>(s_leaf) - 8 * I;
     int t = 0;
-    for (; t + 4 <= nt; t += 4) {
-      int off[4] = {0, 0, 0, 0};
+    for (; t + kApplyDIlp <= nt; t += kApplyDIlp) {
+      int off[kApplyDIlp];
+#pragma unroll
+      for (int u = 0; u < kApplyDIlp; ++u) off[u] = 0;
 #pragma unroll
       for (int l = 0; l < D; ++l) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kApplyDIlp; ++u) {
           const int2 rc = *reinterpret_cast<const int2*>(recb + (t + u) * (8 * I) + off[u]);
           const float v = *reinterpret_cast<const float*>(rb + rc.x);
           off[u] = 2 * off[u] + 8 + (v >= __int_as_float(rc.y) ? 8 : 0);
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < kApplyDIlp; ++u)
         F = __dadd_rn(F, *reinterpret_cast<const double*>(leafb + (t + u) * (8 * L) + off[u]));
     }
     for (; t < nt; ++t) {

@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -1740,18 +1741,25 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
       if (!hl.empty()) BB_CUDA(cudaMemcpyAsync(ld, hl.data(), hl.size() * 8, cudaMemcpyHostToDevice, st));
       ApplyD ad{fo->n_trees, rd, ld, nd2, nw, fo->f0};
       const unsigned gd = (unsigned)ceil_div(n, kApplyDRows);
+      // roots of the first kApplyRoots trees through the parameter space
+      auto roots = std::make_unique<ApplyRoots>();  // host staging; the launch copies the parameters
+      const bool use_roots = fo->n_trees <= kApplyRoots && !getenv("BB_APPLY_NO_ROOTS");
+      if (use_roots)
+        for (int t = 0; t < fo->n_trees; ++t) roots->r[t] = hr[(size_t)t * I];
       auto launch = [&](auto kern) {
         BB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        kern<<<gd, kApplyDRows, smemD, st>>>((const float*)Xd, n, d, ad, pd, fd);
+        kern<<<gd, kApplyDRows, smemD, st>>>((const float*)Xd, n, d, ad, pd, fd, *roots);
       };
+#define BB_APPLY_D(DD) (use_roots ? launch(k_apply_d<DD, true>) : launch(k_apply_d<DD, false>))
       switch (D) {
-        case 1: launch(k_apply_d<1>); break;
-        case 2: launch(k_apply_d<2>); break;
-        case 3: launch(k_apply_d<3>); break;
-        case 4: launch(k_apply_d<4>); break;
-        case 5: launch(k_apply_d<5>); break;
-        default: launch(k_apply_d<6>); break;
+        case 1: BB_APPLY_D(1); break;
+        case 2: BB_APPLY_D(2); break;
+        case 3: BB_APPLY_D(3); break;
+        case 4: BB_APPLY_D(4); break;
+        case 5: BB_APPLY_D(5); break;
+        default: BB_APPLY_D(6); break;
       }
+#undef BB_APPLY_D
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaStreamSynchronize(st));  // host staging vectors
     } else if (x_dtype == BB_F32 && smem32 <= 200 * 1024) {

@@ -174,9 +174,18 @@ struct ApplyD {
   double f0;
 };
 
-template <int D>
+// root records of up to kApplyRoots trees in the kernel's parameter space:
+// the root is the same for every thread of a tree, so its record comes from
+// the uniform datapath (constant bank) instead of a shared-memory wavefront
+constexpr int kApplyRoots = 3900;
+struct ApplyRoots {
+  int2 r[kApplyRoots];
+};
+
+template <int D, bool ROOTS>
 __global__ void __launch_bounds__(kApplyDRows) k_apply_d(const float* __restrict__ X, int64_t n, int d, ApplyD fo,
-                                                         double* __restrict__ out_p, double* __restrict__ out_F) {
+                                                         double* __restrict__ out_p, double* __restrict__ out_F,
+                                                         const __grid_constant__ ApplyRoots roots) {
   constexpr int I = (1 << D) - 1, L = 1 << D, N = (1 << (D + 1)) - 1;
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int ld = d + 1;
@@ -232,7 +241,8 @@ __global__ void __launch_bounds__(kApplyDRows) k_apply_d(const float* __restrict
       for (int l = 0; l < D; ++l) {
 #pragma unroll
         for (int u = 0; u < kApplyDIlp; ++u) {
-          const int2 rc = *reinterpret_cast<const int2*>(recb + (t + u) * (8 * I) + off[u]);
+          const int2 rc = (ROOTS && l == 0) ? roots.r[tb + t + u]
+                                            : *reinterpret_cast<const int2*>(recb + (t + u) * (8 * I) + off[u]);
           const float v = *reinterpret_cast<const float*>(rb + rc.x);
           off[u] = 2 * off[u] + 8 + (v >= __int_as_float(rc.y) ? 8 : 0);
         }

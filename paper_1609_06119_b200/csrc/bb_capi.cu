@@ -1745,7 +1745,8 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
       auto roots = std::make_unique<ApplyRoots>();  // host staging; the launch copies the parameters
       const bool use_roots = fo->n_trees <= kApplyRoots && !getenv("BB_APPLY_NO_ROOTS");
       if (use_roots)
-        for (int t = 0; t < fo->n_trees; ++t) roots->r[t] = hr[(size_t)t * I];
+        for (int t = 0; t < fo->n_trees; ++t)
+          for (int k = 0; k < 3 && k < I; ++k) roots->r[3 * t + k] = hr[(size_t)t * I + k];
       auto launch = [&](auto kern) {
         BB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         kern<<<gd, kApplyDRows, smemD, st>>>((const float*)Xd, n, d, ad, pd, fd, *roots);

@@ -177,9 +177,9 @@ struct ApplyD {
 // root records of up to kApplyRoots trees in the kernel's parameter space:
 // the root is the same for every thread of a tree, so its record comes from
 // the uniform datapath (constant bank) instead of a shared-memory wavefront
-constexpr int kApplyRoots = 3900;
+constexpr int kApplyRoots = 1300;  // trees: root and both children (3 records each)
 struct ApplyRoots {
-  int2 r[kApplyRoots];
+  int2 r[3 * kApplyRoots];
 };
 
 template <int D, bool ROOTS>
@@ -241,8 +241,15 @@ __global__ void __launch_bounds__(kApplyDRows) k_apply_d(const float* __restrict
       for (int l = 0; l < D; ++l) {
 #pragma unroll
         for (int u = 0; u < kApplyDIlp; ++u) {
-          const int2 rc = (ROOTS && l == 0) ? roots.r[tb + t + u]
-                                            : *reinterpret_cast<const int2*>(recb + (t + u) * (8 * I) + off[u]);
+          int2 rc;
+          if (ROOTS && l == 0) {
+            rc = roots.r[3 * (tb + t + u)];
+          } else if (ROOTS && l == 1) {  // node 1 or 2: off = 8 or 16
+            const int2 a = roots.r[3 * (tb + t + u) + 1], b = roots.r[3 * (tb + t + u) + 2];
+            rc = off[u] == 8 ? a : b;
+          } else {
+            rc = *reinterpret_cast<const int2*>(recb + (t + u) * (8 * I) + off[u]);
+          }
           const float v = *reinterpret_cast<const float*>(rb + rc.x);
           off[u] = 2 * off[u] + 8 + (v >= __int_as_float(rc.y) ? 8 : 0);
         }

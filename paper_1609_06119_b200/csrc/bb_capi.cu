@@ -1739,26 +1739,46 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
         BB_CUDA(cudaMemcpyAsync(nd2, hn.data(), TI * sizeof(int2), cudaMemcpyHostToDevice, st));
       }
       if (!hl.empty()) BB_CUDA(cudaMemcpyAsync(ld, hl.data(), hl.size() * 8, cudaMemcpyHostToDevice, st));
-      ApplyD ad{fo->n_trees, rd, ld, nd2, nw, fo->f0};
+      // the first PL levels' records of each tree come from the kernel's
+      // parameter space (uniform loads instead of shared-memory wavefronts);
+      // a forest larger than the parameter space takes several launches,
+      // each continuing F in tree order
+      // (2 levels measured best: cfg4 889 M rows/s; 3 levels need two launches
+      // for 1000 trees and a 4-way select: 583 M)
+      const int PL = getenv("BB_APPLY_PARAM_LEVELS") ? std::max(0, std::min(3, atoi(getenv("BB_APPLY_PARAM_LEVELS"))))
+                                                     : std::min(D, 2);
+      const int RP = (1 << PL) - 1;
+      const int per_launch = RP ? kApplyParamRecs / RP : fo->n_trees;
+      const int n_launch = fo->n_trees > 0 ? (int)ceil_div(fo->n_trees, per_launch) : 1;
+      double* fa = fd;
+      if (n_launch > 1 && !fa) fa = A.alloc<double>(n);  // F between launches
       const unsigned gd = (unsigned)ceil_div(n, kApplyDRows);
-      // roots of the first kApplyRoots trees through the parameter space
-      auto roots = std::make_unique<ApplyRoots>();  // host staging; the launch copies the parameters
-      const bool use_roots = fo->n_trees <= kApplyRoots && !getenv("BB_APPLY_NO_ROOTS");
-      if (use_roots)
-        for (int t = 0; t < fo->n_trees; ++t)
-          for (int k = 0; k < 3 && k < I; ++k) roots->r[3 * t + k] = hr[(size_t)t * I + k];
-      auto launch = [&](auto kern) {
-        BB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        kern<<<gd, kApplyDRows, smemD, st>>>((const float*)Xd, n, d, ad, pd, fd, *roots);
-      };
-#define BB_APPLY_D(DD) (use_roots ? launch(k_apply_d<DD, true>) : launch(k_apply_d<DD, false>))
-      switch (D) {
-        case 1: BB_APPLY_D(1); break;
-        case 2: BB_APPLY_D(2); break;
-        case 3: BB_APPLY_D(3); break;
-        case 4: BB_APPLY_D(4); break;
-        case 5: BB_APPLY_D(5); break;
-        default: BB_APPLY_D(6); break;
+      auto roots = std::make_unique<ApplyRoots>();  // host staging; each launch copies its parameters
+      for (int li = 0; li < n_launch; ++li) {
+        const int t0 = li * per_launch, t1 = std::min(fo->n_trees, t0 + per_launch);
+        for (int t = t0; t < t1; ++t)
+          for (int k = 0; k < RP; ++k) roots->r[(t - t0) * RP + k] = hr[(size_t)t * I + k];
+        ApplyD ad{fo->n_trees, t0, t1, li == 0 ? 1 : 0, li == n_launch - 1 ? 1 : 0, rd, ld, nd2, nw, fo->f0};
+        auto launch = [&](auto kern) {
+          BB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+          kern<<<gd, kApplyDRows, smemD, st>>>((const float*)Xd, n, d, ad, pd, fa, *roots);
+          BB_LAUNCH_CHECK();
+        };
+#define BB_APPLY_D(DD)                                      \
+  do {                                                      \
+    if (PL >= 3 && DD >= 3) launch(k_apply_d<DD, 3>);       \
+    else if (PL >= 2 && DD >= 2) launch(k_apply_d<DD, 2>);  \
+    else if (PL >= 1) launch(k_apply_d<DD, 1>);             \
+    else launch(k_apply_d<DD, 0>);                          \
+  } while (0)
+        switch (D) {
+          case 1: BB_APPLY_D(1); break;
+          case 2: BB_APPLY_D(2); break;
+          case 3: BB_APPLY_D(3); break;
+          case 4: BB_APPLY_D(4); break;
+          case 5: BB_APPLY_D(5); break;
+          default: BB_APPLY_D(6); break;
+        }
       }
 #undef BB_APPLY_D
       BB_LAUNCH_CHECK();

@@ -167,6 +167,8 @@ constexpr int kApplyDIlp = BB_APPLY_ILP;  // trees walked together per thread
 
 struct ApplyD {
   int n_trees;
+  int t_begin, t_end;  // trees of this launch (a forest may take several launches)
+  int first, last;     // first launch: F = f0; last launch: write the probabilities
   const int2* rec;    // [T][2^D - 1]: x = 4 * feature (byte offset; 0 for invalid), y = float bits of ceil_f32(thr)
   const double* leaf; // [T][2^D]
   const int2* node;   // [T][2^D - 1] original records (x = -1: invalid) for NaN rows
@@ -177,12 +179,12 @@ struct ApplyD {
 // root records of up to kApplyRoots trees in the kernel's parameter space:
 // the root is the same for every thread of a tree, so its record comes from
 // the uniform datapath (constant bank) instead of a shared-memory wavefront
-constexpr int kApplyRoots = 1300;  // trees: root and both children (3 records each)
+constexpr int kApplyParamRecs = 3900;  // records (8 B) in the parameter space per launch
 struct ApplyRoots {
-  int2 r[3 * kApplyRoots];
+  int2 r[kApplyParamRecs];  // [launch tree][the first PL levels' 2^PL - 1 records]
 };
 
-template <int D, bool ROOTS>
+template <int D, int PL>  // PL: levels whose records come from the parameter space (0 .. 3)
 __global__ void __launch_bounds__(kApplyDRows) k_apply_d(const float* __restrict__ X, int64_t n, int d, ApplyD fo,
                                                          double* __restrict__ out_p, double* __restrict__ out_F,
                                                          const __grid_constant__ ApplyRoots roots) {
@@ -206,9 +208,10 @@ __global__ void __launch_bounds__(kApplyDRows) k_apply_d(const float* __restrict
   if ((int)threadIdx.x < rows)
     for (int f = 0; f < d; ++f) has_nan |= row[f] != row[f];
   double F = fo.f0;
+  if (!fo.first && (int)threadIdx.x < rows) F = out_F[row0 + threadIdx.x];  // trees before this launch
   if (has_nan) {
     // exact per-node walk (the generic rule), original records in global memory
-    for (int t = 0; t < fo.n_trees; ++t) {
+    for (int t = fo.t_begin; t < fo.t_end; ++t) {
       int nd = 0;
       for (int l = 0; l < D; ++l) {
         const int2 rc = __ldg(&fo.node[(int64_t)t * I + nd]);
@@ -220,8 +223,9 @@ __global__ void __launch_bounds__(kApplyDRows) k_apply_d(const float* __restrict
       F = __dadd_rn(F, __ldg(&fo.nw[(int64_t)t * N + nd]));
     }
   }
-  for (int tb = 0; tb < fo.n_trees; tb += kApplyDTB) {
-    const int nt = min(kApplyDTB, fo.n_trees - tb);
+  constexpr int RP = (1 << PL) - 1;  // parameter records per tree
+  for (int tb = fo.t_begin; tb < fo.t_end; tb += kApplyDTB) {
+    const int nt = min(kApplyDTB, fo.t_end - tb);
     __syncthreads();
     for (int e = threadIdx.x; e < nt * I; e += kApplyDRows) s_rec[e] = fo.rec[(int64_t)tb * I + e];
     for (int e = threadIdx.x; e < nt * L; e += kApplyDRows) s_leaf[e] = fo.leaf[(int64_t)tb * L + e];
@@ -242,11 +246,15 @@ __global__ void __launch_bounds__(kApplyDRows) k_apply_d(const float* __restrict
 #pragma unroll
         for (int u = 0; u < kApplyDIlp; ++u) {
           int2 rc;
-          if (ROOTS && l == 0) {
-            rc = roots.r[3 * (tb + t + u)];
-          } else if (ROOTS && l == 1) {  // node 1 or 2: off = 8 or 16
-            const int2 a = roots.r[3 * (tb + t + u) + 1], b = roots.r[3 * (tb + t + u) + 2];
-            rc = off[u] == 8 ? a : b;
+          const int2* pr = roots.r + (tb - fo.t_begin + t + u) * RP;  // uniform: the same tree for all threads
+          if (l < PL && l == 0) {
+            rc = pr[0];
+          } else if (l < PL && l == 1) {  // node 1 or 2: off = 8 or 16
+            rc = off[u] == 8 ? pr[1] : pr[2];
+          } else if (l < PL && l == 2) {  // nodes 3 .. 6: off = 24 .. 48
+            const int2 a = off[u] & 8 ? pr[3] : pr[4];  // 24: node 3, 32: node 4
+            const int2 b = off[u] & 8 ? pr[5] : pr[6];  // 40: node 5, 48: node 6
+            rc = off[u] < 40 ? a : b;
           } else {
             rc = *reinterpret_cast<const int2*>(recb + (t + u) * (8 * I) + off[u]);
           }
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(kApplyDRows) k_apply_d(const float* __restrict
   if ((int)threadIdx.x < rows) {
     const int64_t i = row0 + threadIdx.x;
     if (out_F) out_F[i] = F;
-    if (out_p) out_p[i] = sigmoid2(F);
+    if (out_p && fo.last) out_p[i] = sigmoid2(F);
   }
 }
 

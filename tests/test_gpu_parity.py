@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import hashlib
+import os
 import json
 import math
 import threading
@@ -328,6 +329,36 @@ def test_apply_nan_and_invalid_nodes():
                                 np.stack([t.node_weight for t in forest.trees]), 4, X)
     p, F = predict_batch(forest, X, return_scores=True)
     np.testing.assert_array_equal(F, ref)
+
+
+def test_apply_large_forest_multi_launch():
+    """More trees than one launch's parameter-space records (1300 trees at the
+    default 2 levels, 557 at 3): F continues across launches in tree order;
+    NaN rows and invalid nodes."""
+    from paper_1609_06119_b200.engine import FeatureBinning, Forest, Tree
+
+    rng = np.random.default_rng(11)
+    T, D, d = 1400, 3, 6
+    X = rng.normal(size=(3000, d)).astype(np.float32)
+    X[rng.random(X.shape) < 0.03] = np.nan
+    bounds = [np.sort(rng.normal(size=255)) for _ in range(d)]
+    feature = rng.integers(0, d, (T, 7)).astype(np.int32)
+    cut = rng.integers(1, 256, (T, 7)).astype(np.int32)
+    valid = rng.random((T, 7)) > 0.05
+    thr = np.array([[bounds[feature[t, k]][cut[t, k] - 1] for k in range(7)] for t in range(T)])
+    nw = rng.uniform(-1, 1, (T, 15))
+    trees = [Tree(depth=D, feature=np.where(valid[t], feature[t], -1), cut_bin=np.where(valid[t], cut[t], 0),
+                  threshold=np.where(valid[t], thr[t], np.nan), gain=np.zeros(7), valid=valid[t], node_weight=nw[t],
+                  node_purity=np.zeros(15)) for t in range(T)]
+    forest = Forest(f0=0.25, trees=trees, binnings=[FeatureBinning(b, 8) for b in bounds])
+    ref = oracle.predict_scores(0.25, valid, np.where(valid, feature, -1), np.where(valid, thr, np.nan), nw, D, X)
+    for levels in ("2", "3"):
+        os.environ["BB_APPLY_PARAM_LEVELS"] = levels  # read per call
+        try:
+            p, F = predict_batch(forest, X, return_scores=True)
+        finally:
+            del os.environ["BB_APPLY_PARAM_LEVELS"]
+        np.testing.assert_array_equal(F, ref)
 
 
 # ------------------------------------------------------------------ bridge

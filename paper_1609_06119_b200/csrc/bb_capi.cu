@@ -737,17 +737,21 @@ struct MaskGen {
     stail_i = A.alloc<int>(1);
     int lo_prio = 0, hi_prio = 0;
     BB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-    BB_CUDA(cudaStreamCreateWithPriority(&sb, cudaStreamNonBlocking, hi_prio));
+    // BB_MASK_PRIO: 0 all mask streams high priority; 1 phase 1 high, emits /
+    // resolution / draws normal; 2 all normal (the chain stream stays high)
+    static const int prio_mode = getenv("BB_MASK_PRIO") ? atoi(getenv("BB_MASK_PRIO")) : 0;
+    const int p_sb = prio_mode >= 2 ? lo_prio : hi_prio, p_rest = prio_mode >= 1 ? lo_prio : hi_prio;
+    BB_CUDA(cudaStreamCreateWithPriority(&sb, cudaStreamNonBlocking, p_sb));
     BB_CUDA(cudaEventCreateWithFlags(&evA, cudaEventDisableTiming));
     BB_CUDA(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
     BB_CUDA(cudaEventCreateWithFlags(&evC, cudaEventDisableTiming));
     BB_CUDA(cudaEventCreateWithFlags(&evTl, cudaEventDisableTiming));
     for (int q = 0; q < 2; ++q) BB_CUDA(cudaEventCreateWithFlags(&evF[q], cudaEventDisableTiming));
-    BB_CUDA(cudaStreamCreateWithPriority(&sc, cudaStreamNonBlocking, hi_prio));
-    BB_CUDA(cudaStreamCreateWithPriority(&se, cudaStreamNonBlocking, hi_prio));
+    BB_CUDA(cudaStreamCreateWithPriority(&sc, cudaStreamNonBlocking, p_rest));
+    BB_CUDA(cudaStreamCreateWithPriority(&se, cudaStreamNonBlocking, p_rest));
     for (int q = 0; q < 2; ++q) BB_CUDA(cudaEventCreateWithFlags(&evE[q], cudaEventDisableTiming));
     BB_CUDA(cudaEventCreateWithFlags(&evEnd, cudaEventDisableTiming));
-    BB_CUDA(cudaStreamCreateWithPriority(&sg, cudaStreamNonBlocking, hi_prio));
+    BB_CUDA(cudaStreamCreateWithPriority(&sg, cudaStreamNonBlocking, p_rest));
     BB_CUDA(cudaEventCreateWithFlags(&evPre, cudaEventDisableTiming));
     BB_CUDA(cudaEventCreateWithFlags(&evG2, cudaEventDisableTiming));
     for (int q = 0; q < kChunk; ++q) BB_CUDA(cudaEventCreateWithFlags(&evT[q], cudaEventDisableTiming));

@@ -1289,7 +1289,9 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaMemcpyAsync(out->scores, F, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
     }
+    const double enq_ms = elapsed_ms(t0);  // host time to enqueue every tree (launch-bound if ~ the fit)
     BB_CUDA(cudaStreamSynchronize(st));
+    if (tl_on) fprintf(stderr, "timeline: host enqueue %.2f ms, enqueue+sync %.2f ms\n", enq_ms, elapsed_ms(t0));
     if (tl_on && tl.size() >= 2) {
       double wait = 0.0, busy = 0.0;
       int waits = 0;

@@ -979,16 +979,17 @@ struct MaskGen {
         const int nn = n[cc], kk = k[cc];
         int* Jt = J[cc] + (size_t)(half + t) * stride;
         // k == 0: nothing is active (position 0 is never a step target)
-        BB_CUDA(cudaMemsetAsync(removed[cc], kk == 0 ? 1 : 0, (size_t)std::max(1, nn), st));
-        if (kk == 0 || nn <= 1 || kk >= nn) continue;
-        BB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)nn * 4, st));
-        BB_CUDA(cudaMemsetAsync(fill, 0, (size_t)nn * 4, st));
+        if (kk == 0 || nn <= 1 || kk >= nn) {
+          BB_CUDA(cudaMemsetAsync(removed[cc], kk == 0 ? 1 : 0, (size_t)std::max(1, nn), st));
+          continue;
+        }
+        BB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)nn * 4, st));  // fill and removed: cleared by k_scan_apply
         const int g = grid_for(nn - kk, 256, sm);
         k_bucket_count<<<g, 256, 0, st>>>(Jt, kk, nn, cnt);
         const int nb = (int)ceil_div(nn, kScanBlock);
         k_scan_block_sums<<<nb, 256, 0, st>>>(cnt, nn, sums);
         k_scan_sums<<<1, 1024, 0, st>>>(sums, nb);
-        k_scan_apply<<<nb, 256, 0, st>>>(cnt, nn, sums, off);
+        k_scan_apply<<<nb, 256, 0, st>>>(cnt, nn, sums, off, fill, removed[cc]);
         k_bucket_fill<<<g, 256, 0, st>>>(Jt, kk, nn, off, fill, bucket);
         k_bucket_sort<<<grid_for(nn, 256, sm), 256, 0, st>>>(cnt, off, nn, bucket);
         k_resolve<<<g, 256, 0, st>>>(Jt, kk, nn, cnt, off, bucket, removed[cc]);

@@ -177,13 +177,29 @@ __global__ void __launch_bounds__(1024) k_select_scan(SelectState<K> st, int db)
   const int* gft = st.grp_first_tgt + (int64_t)f * nt;
   const int nbins = 1 << db;
   const int per_lane = (nbins + 31) / 32;  // <= 128
+  // lane owns bins [lane*per_lane, (lane+1)*per_lane), summed in sub-blocks
+  // of kSub bins (offsets kept in registers); each lane then resolves its own
+  // target per round of 32 (owner lane by a shuffle search over the lanes'
+  // inclusive sums, then the sub-block, then <= kSub bins walked in global).
+  constexpr int kSub = 16, kMaxSub = 8;  // per_lane <= 128
+  const int nsub = (per_lane + kSub - 1) / kSub;
   for (int g = warp; g < ng; g += nwarps) {
     const unsigned int* h = gh + ((int64_t)g << db);
-    // lane owns bins [lane*per_lane, (lane+1)*per_lane)
+    const int lb = lane * per_lane;
+    const int le = min(nbins, lb + per_lane);
+    unsigned long long sub_excl[kMaxSub];
     unsigned long long local = 0;
-    for (int j = 0; j < per_lane; ++j) {
-      const int b = lane * per_lane + j;
-      if (b < nbins) local += h[b];
+#pragma unroll
+    for (int sb = 0; sb < kMaxSub; ++sb) {
+      sub_excl[sb] = local;
+      if (sb < nsub) {
+        unsigned long long ss = 0;
+        for (int j = 0; j < kSub; ++j) {
+          const int b = lb + sb * kSub + j;
+          if (sb * kSub + j < per_lane && b < le) ss += h[b];
+        }
+        local += ss;
+      }
     }
     unsigned long long incl = local;
     for (int o = 1; o < 32; o <<= 1) {
@@ -193,44 +209,74 @@ __global__ void __launch_bounds__(1024) k_select_scan(SelectState<K> st, int db)
     const unsigned long long excl = incl - local;
     const int t_begin = gft[g];
     const int t_end = (g + 1 < ng) ? gft[g + 1] : nt;
-    for (int t = t_begin; t < t_end; ++t) {
-      const unsigned long long r = tr[t];
-      // the lane whose [excl, incl) holds r resolves the digit
-      const bool mine = (r >= excl) && (r < incl);
-      const unsigned int who = __ballot_sync(0xffffffffu, mine);
-      if (mine) {
-        unsigned long long c = excl;
-        int b = lane * per_lane;
-        for (;; ++b) {
+    for (int tb = t_begin; tb < t_end; tb += 32) {
+      const int t = tb + lane;
+      const bool act = t < t_end;
+      const unsigned long long r = act ? tr[t] : ~0ull;
+      // owner = first lane whose inclusive sum exceeds r
+      int owner = 0;
+      for (int step = 16; step >= 1; step >>= 1) {
+        const unsigned long long v = __shfl_sync(0xffffffffu, incl, min(31, owner + step - 1));
+        if (owner + step <= 32 && v <= r) owner += step;
+      }
+      if (__shfl_sync(0xffffffffu, incl, owner) <= r) owner = 32;  // r past every bin: no digit
+      const int src = min(owner, 31);
+      const unsigned long long oe = __shfl_sync(0xffffffffu, excl, src);
+      const unsigned long long rin = r - oe;
+      int sidx = 0;
+      unsigned long long se_sel = 0;
+#pragma unroll
+      for (int sb = 0; sb < kMaxSub; ++sb) {
+        const unsigned long long se = __shfl_sync(0xffffffffu, sub_excl[sb], src);
+        if (sb < nsub && se <= rin) { sidx = sb; se_sel = se; }
+      }
+      if (act && owner < 32) {
+        unsigned long long c = rin - se_sel;
+        const int ob = owner * per_lane;
+        const int oend = min(nbins, ob + per_lane);
+        int b = ob + sidx * kSub;
+        for (; b < oend - 1; ++b) {
           const unsigned long long hb = h[b];
-          if (r < c + hb) break;
-          c += hb;
+          if (c < hb) break;
+          c -= hb;
         }
-        tr[t] = r - c;
+        tr[t] = c;
         tp[t] = (tp[t] << db) | (K)b;
       }
-      (void)who;
     }
   }
   __syncthreads();
-  // rebuild groups: a target starts a group when its prefix differs from the previous one
-  __shared__ int s_count;
-  if (threadIdx.x == 0) {
+  // rebuild groups: a target starts a group when its prefix differs from the
+  // previous one (block-wide ballot scan, blockDim.x targets per round)
+  __shared__ int s_wcnt[32];
+  __shared__ int s_carry;
+  {
     K* gp = st.grp_prefix + (int64_t)f * nt;
     int* gf = st.grp_first_tgt + (int64_t)f * nt;
-    int c = 0;
-    for (int t = 0; t < nt; ++t) {
-      if (t == 0 || tp[t] != tp[t - 1]) {
-        gp[c] = tp[t];
-        gf[c] = t;
-        ++c;
+    int carry = 0;
+    for (int base = 0; base < nt; base += blockDim.x) {
+      const int t = base + threadIdx.x;
+      const bool flag = t < nt && (t == 0 || tp[t] != tp[t - 1]);
+      const unsigned int bal = __ballot_sync(0xffffffffu, flag);
+      if (lane == 0) s_wcnt[warp] = __popc(bal);
+      __syncthreads();
+      int before = carry;
+      for (int w = 0; w < warp; ++w) before += s_wcnt[w];
+      const int idx = before + __popc(bal & ((2u << lane) - 1u));  // inclusive count
+      if (t < nt) {
+        tg[t] = idx - 1;
+        if (flag) {
+          gp[idx - 1] = tp[t];
+          gf[idx - 1] = t;
+        }
       }
-      tg[t] = c - 1;
+      if (threadIdx.x == blockDim.x - 1) s_carry = idx;
+      __syncthreads();
+      carry = s_carry;
+      __syncthreads();
     }
-    s_count = c;
-    st.grp_count[f] = c;
+    if (threadIdx.x == 0) st.grp_count[f] = carry;
   }
-  __syncthreads();
   // zero the histogram rows this pass used (next pass reuses the buffer)
   const int64_t used = (int64_t)ng << db;
   for (int64_t i = threadIdx.x; i < used; i += blockDim.x) gh[i] = 0;

@@ -29,6 +29,7 @@
 #include "kernels_seg.cuh"
 #include "kernels_tree.cuh"
 #include "kernels_hist_fl.cuh"
+#include "kernels_hist_list.cuh"
 
 namespace bb {
 
@@ -339,6 +340,11 @@ static bool hist_warp_mode() {  // the warp-independent histogram kernel (BB_HIS
   return !e || atoi(e) != 0;
 }
 
+static int hist_reserve() {  // SMs left to the concurrent mask streams during a histogram launch
+  static const int r = getenv("BB_HIST_RESERVE") ? atoi(getenv("BB_HIST_RESERVE")) : 9;
+  return r;
+}
+
 static inline int hist_grid(const HistPlan& p) { return p.n_fg * p.n_ng * (p.split_sig + p.split_bkg); }
 
 // Histogram path: BB_HIST_PATH = fl | w | cta | g (read per call: tests force
@@ -351,6 +357,7 @@ static int hist_path_env() {
   if (!strcmp(e, "w")) return 2;
   if (!strcmp(e, "cta")) return 3;
   if (!strcmp(e, "g")) return 4;
+  if (!strcmp(e, "list")) return 5;
   return 0;
 }
 
@@ -1199,6 +1206,35 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   long long* fl_partials = part_elems ? A.alloc<long long>((size_t)part_elems) : nullptr;
   set_hist_smem_attrs<CodeT, NodeT>();
 
+  // node-partitioned row lists + row-major codes (kernels_hist_list.cuh):
+  // u8 codes, d <= 64, every built (node, class) list gets a CTA
+  const int lh_nw = s.d <= 32 ? 8 : 16;
+  const int lh_grid = lh_nw == 8 ? 2 * (c.sm_count - hist_reserve()) : c.sm_count - hist_reserve();
+  const int hp_env = hist_path_env();
+  const bool lists = sizeof(CodeT) == 1 && s.d <= 64 && s.depth <= 8 && (hp_env == 0 || hp_env == 5) &&
+                     2 * (1 << (s.depth - 1)) <= lh_grid && !getenv("BB_HIST_WARP") && !getenv("BB_HIST_GLOBAL_GROUPS");
+  uint32_t* rc = nullptr;
+  int* lrow[2] = {nullptr, nullptr};
+  long long* lq[2] = {nullptr, nullptr};
+  int* cnt = nullptr;
+  if (lists) {
+    rc = A.alloc<uint32_t>((size_t)npad * lh_nw);
+    for (int b = 0; b < 2; ++b) {
+      lrow[b] = A.alloc<int>(npad);
+      lq[b] = A.alloc<long long>(npad);
+    }
+    cnt = A.alloc<int>((size_t)2 * s.n_nodes);
+    const int tiles = (int)ceil_div(n, kTile);
+    const uint8_t* c8 = reinterpret_cast<const uint8_t*>(codes);
+    BB_CUDA(cudaFuncSetAttribute(k_hist_list<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, lh_smem_bytes<8>()));
+    BB_CUDA(cudaFuncSetAttribute(k_hist_list<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lh_smem_bytes<16>()));
+    BB_CUDA(cudaFuncSetAttribute(k_rowcodes<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * kTile));
+    BB_CUDA(cudaFuncSetAttribute(k_rowcodes<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * kTile));
+    if (lh_nw == 8) k_rowcodes<8><<<tiles, 256, (size_t)s.d * kTile, st>>>(c8, n, s.d, rc);
+    else k_rowcodes<16><<<tiles, 256, (size_t)s.d * kTile, st>>>(c8, n, s.d, rc);
+    BB_LAUNCH_CHECK();
+  }
+
   std::vector<NodeT> leaf_tmp;
   const bool prof = (cfg.flags & 1) != 0;
   std::vector<cudaEvent_t> hev;
@@ -1220,7 +1256,16 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
     for (auto e : hev) cudaEventDestroy(e);
   };
   const int gridN = grid_for(n, 256, c.sm_count);
-  const int gridA = grid_for(n, 512, c.sm_count, 4);
+  // refresh / advance: 2048-row tiles, grid-stride over exactly the resident
+  // CTAs (a grid larger than one wave leaves its tail CTAs for a second pass)
+  auto resident = [&](auto kern, size_t smem) {
+    int per = 1;
+    BB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kListThreads, smem));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kListTileRows), (int64_t)std::max(1, per) * c.sm_count));
+  };
+  const int gridR = resident(k_update_refresh<NodeT>, 0);
+  const int gridL = resident(k_advance<CodeT, NodeT>, 0);
+  const int gridLL = resident(k_advance<CodeT, NodeT>, (size_t)32 * s.n_nodes);
   const auto t0 = std::chrono::steady_clock::now();
   try {
     const bool tl_on = getenv("BB_TIMELINE") != nullptr;  // debug: main-stream waits for masks
@@ -1240,8 +1285,10 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         BB_CUDA(cudaEventCreate(&tl.back()));
         BB_CUDA(cudaEventRecord(tl.back(), st));  // ... and tree t's mask ready
       }
-      k_update_refresh<NodeT><<<gridN, 256, 0, st>>>(n, s.n_sig, F, node, w_cb, q, mask,
-                                                      t > 0 ? ta.nw + (size_t)(t - 1) * s.n_nodes : nullptr, two_s);
+      if (lists) BB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)2 * s.n_nodes * 4, st));
+      k_update_refresh<NodeT><<<gridR, kListThreads, 0, st>>>(n, s.n_sig, F, node, w_cb, q, mask,
+                                                      t > 0 ? ta.nw + (size_t)(t - 1) * s.n_nodes : nullptr, two_s,
+                                                      cnt, lrow[0], lq[0]);
       BB_LAUNCH_CHECK();
       stats.launches += 1;
       for (int layer = 1; layer <= s.depth; ++layer) {
@@ -1249,8 +1296,19 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         unsigned long long* hist = hbuf[layer & 1];
         unsigned long long* par = hbuf[(layer - 1) & 1];
         if (prof) hist_event();
-        launch_layer_hist<CodeT, NodeT>(p, fl_plans[layer], c.sm_count, codes, code_off, node, q, n, s.n_sig, s.d,
-                                        s.B, hist, st, fl_partials);
+        if (lists) {
+          const int lb = (layer - 1) & 1;
+          if (lh_nw == 8)
+            k_hist_list<8><<<lh_grid, kLhThreads, lh_smem_bytes<8>(), st>>>(rc, lrow[lb], lq[lb], cnt, layer, p.sib,
+                                                                          s.n_sig, s.d, s.B, code_off, p.nodes, hist);
+          else
+            k_hist_list<16><<<lh_grid, kLhThreads, lh_smem_bytes<16>(), st>>>(rc, lrow[lb], lq[lb], cnt, layer, p.sib,
+                                                                            s.n_sig, s.d, s.B, code_off, p.nodes, hist);
+          BB_LAUNCH_CHECK();
+        } else {
+          launch_layer_hist<CodeT, NodeT>(p, fl_plans[layer], c.sm_count, codes, code_off, node, q, n, s.n_sig, s.d,
+                                          s.B, hist, st, fl_partials);
+        }
         if (prof) hist_event();
         c.comm.all_reduce(hist, (size_t)2 * p.nodes * s.d * s.B, kNcclI64, kNcclSum, st);  // sharded fits
         stats.launches += 3;
@@ -1266,9 +1324,10 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         BB_LAUNCH_CHECK();
         const bool last = layer == s.depth;
         if (last && p.sib) BB_CUDA(cudaMemsetAsync(hist, 0, (size_t)2 * nodes * s.d * s.B * 8, st));
-        k_advance<CodeT, NodeT><<<gridA, 512, last ? (size_t)32 * s.n_nodes : 0, st>>>(
+        k_advance<CodeT, NodeT><<<last ? gridLL : gridL, kListThreads, last ? (size_t)32 * s.n_nodes : 0, st>>>(
             codes, s.d, code_off, node, n, s.n_sig, p.start, t, s.n_internal, ta, last ? 1 : 0, s.n_nodes, q, mask,
-            F, w_cb, two_s, sums);
+            F, w_cb, two_s, sums, cnt, lists ? lrow[layer & 1] : nullptr, lists ? lq[layer & 1] : nullptr,
+            (layer < s.depth && plans[layer + 1].sib) ? 1 : 0);
         BB_LAUNCH_CHECK();
       }
       BB_CUDA(cudaEventRecord(feed.freed[slot], st));
@@ -1875,6 +1934,91 @@ int bb_layer_hist(bb_ctx* ctx, const uint16_t* codes, const uint16_t* node, cons
     Arena A(st);
     const int B = 1 << levels;
     const int64_t npad = ceil_div(n, kRowPad) * kRowPad;
+    if (hist_path_env() == 5) {
+      // node-partitioned row lists (kernels_hist_list.cuh), built on the host
+      // with the fit's region rule (full layer: both children listed)
+      if (B > 256 || d > 64) throw InvalidArg{"list histogram: needs B <= 256 and d <= 64"};
+      const int code_off = B == 256 ? 1 : 0;
+      const int NW = d <= 32 ? 8 : 16;
+      std::vector<uint32_t> rch((size_t)npad * NW, 0u);
+      for (int f = 0; f < d; ++f)
+        for (int64_t i = 0; i < n; ++i) {
+          const int v = (int)codes[(size_t)f * n + i] - code_off;
+          if (v < 0) throw InvalidArg{"list histogram: B = 256 needs NaN-free codes"};
+          rch[(size_t)i * NW + f / 4] |= (uint32_t)v << (8 * (f & 3));
+        }
+      const int nodes = 1 << (layer - 1), start = nodes - 1;
+      const int nn = 2 * nodes + 1;  // heap ids < 2^layer + ...
+      std::vector<int> cnth((size_t)2 * (2 * nodes + nodes), 0);
+      auto cls_of = [&](int64_t i) { return i < n_sig ? 0 : 1; };
+      std::vector<int> lr(std::max<int64_t>(1, n), 0);
+      std::vector<long long> lqv(std::max<int64_t>(1, n), 0);
+      if (layer == 1) {
+        int fill[2] = {0, 0};
+        for (int64_t i = 0; i < n; ++i) {
+          if (node[i] != 0) continue;
+          const int k = cls_of(i);
+          const int64_t pos = (k ? n_sig : 0) + fill[k]++;
+          lr[pos] = (int)i;
+          lqv[pos] = q[i];
+        }
+        cnth[0] = fill[0];
+        cnth[1] = fill[1];
+      } else {
+        const int ps = (1 << (layer - 2)) - 1, np = 1 << (layer - 2);
+        for (int64_t i = 0; i < n; ++i) {
+          const int nd = node[i];
+          if (nd < start || nd >= start + nodes) continue;
+          const int k = cls_of(i), par = (nd - 1) / 2;
+          cnth[2 * nd + k] += 1;
+          cnth[2 * par + k] += 1;
+        }
+        std::vector<int> reg(2 * np), fl(2 * np, 0), fr(2 * np, 0);
+        int off = 0;
+        for (int k = 0; k < 2; ++k)
+          for (int pp = 0; pp < np; ++pp) {
+            reg[k * np + pp] = off;
+            off += cnth[2 * (ps + pp) + k];
+          }
+        for (int64_t i = 0; i < n; ++i) {
+          const int nd = node[i];
+          if (nd < start || nd >= start + nodes) continue;
+          const int k = cls_of(i), par = (nd - 1) / 2, pl = par - ps;
+          int pos;
+          if (nd & 1) pos = reg[k * np + pl] + fl[k * np + pl]++;
+          else pos = reg[k * np + pl] + cnth[2 * par + k] - 1 - fr[k * np + pl]++;
+          lr[pos] = (int)i;
+          lqv[pos] = q[i];
+        }
+      }
+      (void)nn;
+      uint32_t* rcd = A.alloc<uint32_t>(rch.size());
+      int* lrd = A.alloc<int>(lr.size());
+      long long* lqd = A.alloc<long long>(lqv.size());
+      int* cd = A.alloc<int>(cnth.size());
+      BB_CUDA(cudaMemcpyAsync(rcd, rch.data(), rch.size() * 4, cudaMemcpyHostToDevice, st));
+      BB_CUDA(cudaMemcpyAsync(lrd, lr.data(), lr.size() * 4, cudaMemcpyHostToDevice, st));
+      BB_CUDA(cudaMemcpyAsync(lqd, lqv.data(), lqv.size() * 8, cudaMemcpyHostToDevice, st));
+      BB_CUDA(cudaMemcpyAsync(cd, cnth.data(), cnth.size() * 4, cudaMemcpyHostToDevice, st));
+      const size_t hsz = (size_t)2 * nodes * d * B;
+      unsigned long long* hist = A.alloc<unsigned long long>(hsz);
+      BB_CUDA(cudaMemsetAsync(hist, 0, hsz * 8, st));
+      const int grid = NW == 8 ? 2 * c.sm_count : c.sm_count;
+      if (NW == 8) {
+        BB_CUDA(cudaFuncSetAttribute(k_hist_list<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, lh_smem_bytes<8>()));
+        k_hist_list<8><<<grid, kLhThreads, lh_smem_bytes<8>(), st>>>(rcd, lrd, lqd, cd, layer, 0, n_sig, d, B, code_off,
+                                                                     nodes, hist);
+      } else {
+        BB_CUDA(cudaFuncSetAttribute(k_hist_list<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lh_smem_bytes<16>()));
+        k_hist_list<16><<<grid, kLhThreads, lh_smem_bytes<16>(), st>>>(rcd, lrd, lqd, cd, layer, 0, n_sig, d, B,
+                                                                       code_off, nodes, hist);
+      }
+      BB_LAUNCH_CHECK();
+      BB_CUDA(cudaStreamSynchronize(st));
+      BB_CUDA(cudaMemcpyAsync(out_hist, hist, hsz * 8, cudaMemcpyDeviceToHost, st));
+      BB_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
     std::vector<uint16_t> tiled((size_t)d * npad, 0);
     for (int f = 0; f < d; ++f)
       for (int64_t i = 0; i < n; ++i) tiled[(size_t)code_index(i, f, d)] = codes[(size_t)f * n + i];

@@ -1,0 +1,329 @@
+// Node-partitioned ("list") layer histogram (trees.py:139-167) for u8 codes
+// (B <= 256) and d <= 64 features.
+//
+// Row lists.  The active rows of a tree are kept in per-(node, class) lists
+// of (row id, fixed-point weight q): the refresh kernel lists every active
+// row for layer 1 (class regions [0, n_sig) and [n_sig, n)), and each
+// advance appends the rows entering the next layer's children into the
+// parent's region (left child from the region start, right child from its
+// end; the region of parent p and class k starts at the class-major prefix
+// of the parents' active counts).  A layer's histogram therefore reads only
+// the rows of the nodes it builds (with sibling subtraction: the left
+// children, ~half the active rows), each once, in one launch for every node.
+//
+// Row codes.  Codes are gathered from a row-major copy (NW u32 words per
+// row, NW = 8 for d <= 32, 16 for d <= 64; zero-padded) with cp.async into a
+// per-warp double buffer.
+//
+// Lane owns a row.  Lane l adds its own row's weight at every feature: at
+// step (w, b) it takes byte c of word g of its row (NW = 16: g = (w + l/2)
+// mod 16, c = (b + 2 (l&1)) mod 4; NW = 8: g = (w + l/4) mod 8, c = (b + l)
+// mod 4).  The 32 lanes then touch 32 distinct features, and the slot word of
+// feature 4g + c inside a bin row (NW = 16: 32 (c&1) + 16 (c>>1) + g; NW = 8:
+// 4g + c) puts them in 32 distinct banks: every warp-wide atomic is one
+// shared-memory wavefront for any codes, with no lane-private copies.  The
+// row reads (word g of row l, row pitch NW words) are conflict-free as well
+// (checked exhaustively for both NW).  The per-row weight stays in the
+// lane's registers (no broadcast meta loads).
+//
+// Limbs as in the feature-lane kernel: q is added as lo16 = q & 0xffff and
+// hi = q >> 16 (signed) with non-returning 32-bit atomics; a slot is exact
+// while it takes < 2^15 adds, so a CTA flushes at least every kLhFlushRows
+// rows.  Flush: int64 rows [feature][bin] staged in the drained buffers and
+// added to the global layer histogram by TMA bulk reductions.
+#pragma once
+#include "common.cuh"
+
+namespace bb {
+
+constexpr int kLhWarps = 16;
+constexpr int kLhThreads = 32 * kLhWarps;
+constexpr int kLhFlushRows = 32767;
+constexpr int kLhMaxSegs = 256;
+#ifndef BB_LH_PF
+#define BB_LH_PF 4
+#endif
+constexpr int kLhPf = BB_LH_PF;  // slices of row codes in flight per warp (registers)
+
+// byte offset of the (lo) slot of feature f in a bin row
+template <int NW>
+__host__ __device__ __forceinline__ int lh_slot_word(int f) {
+  const int g = f >> 2, c = f & 3;
+  return NW == 16 ? 32 * (c & 1) + 16 * ((c >> 1) & 1) + g : 4 * g + c;
+}
+// shared memory: NW = 16: lo limbs [256][64] words, then hi limbs (128 KB);
+// NW = 8: bin rows of [32 lo | 32 hi] words (64 KB).  Then the warp buffers.
+template <int NW>
+__host__ __device__ constexpr int lh_hist_bytes() { return NW == 16 ? 2 * 256 * 64 * 4 : 256 * 64 * 4; }
+template <int NW>
+__host__ __device__ constexpr int lh_buf_bytes() {  // per-warp slice buffers; also the flush staging (rows of pitch 258 int64)
+  return kLhWarps * 32 * NW * 4 > (NW == 16 ? 32 : 16) * 258 * 8 ? kLhWarps * 32 * NW * 4 : (NW == 16 ? 32 : 16) * 258 * 8;
+}
+template <int NW>
+__host__ __device__ constexpr int lh_smem_bytes() { return lh_hist_bytes<NW>() + lh_buf_bytes<NW>() + 16 * kLhMaxSegs + 64; }
+
+// Segments (list ranges) of the histogram launch of `layer`: every built
+// node's (class, node) list.  cnt is heap-indexed [node][class].  Layer 1:
+// the refresh's class regions [0, n_sig), [n_sig, n).  Layer >= 2: parent p
+// (layer-1 node) and class k own the region at the class-major prefix of
+// the parents' counts; the left child fills it from the start, the right
+// child (built only without sibling subtraction) from the end.
+// seg = {list offset, rows, layer-local node index, class}
+__device__ __forceinline__ int lh_segments(const int* __restrict__ cnt, int layer, int sib, long long n_sig,
+                                           int4* segs) {
+  int ns = 0;
+  if (layer == 1) {
+    segs[ns++] = make_int4(0, __ldcg(cnt + 0), 0, 0);
+    segs[ns++] = make_int4((int)n_sig, __ldcg(cnt + 1), 0, 1);
+    return ns;
+  }
+  const int ps = (1 << (layer - 2)) - 1, np = 1 << (layer - 2), st = (1 << (layer - 1)) - 1;
+  int off = 0;
+  for (int k = 0; k < 2; ++k) {
+    for (int p = ps; p < ps + np; ++p) {
+      const int cp = __ldcg(cnt + 2 * p + k);
+      const int c = 2 * p + 1;
+      segs[ns++] = make_int4(off, __ldcg(cnt + 2 * c + k), c - st, k);
+      if (!sib) {
+        const int cr = __ldcg(cnt + 2 * (c + 1) + k);
+        segs[ns++] = make_int4(off + cp - cr, cr, c + 1 - st, k);
+      }
+      off += cp;
+    }
+  }
+  return ns;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int NW>
+__global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
+    k_hist_list(const uint32_t* __restrict__ rc, const int* __restrict__ lrow, const long long* __restrict__ lq,
+                const int* __restrict__ cnt, int layer, int sib, long long n_sig, int d, int B, int code_off,
+                int nodes, unsigned long long* __restrict__ hist) {
+  extern __shared__ __align__(16) unsigned char lh_sm[];
+  unsigned char* hb = lh_sm;                                             // histogram limbs
+  uint32_t* bufs = reinterpret_cast<uint32_t*>(lh_sm + lh_hist_bytes<NW>());  // [warp][2][32 rows][NW]
+  int4* segs = reinterpret_cast<int4*>(lh_sm + lh_hist_bytes<NW>() + lh_buf_bytes<NW>());
+  __shared__ int s_ns;
+  __shared__ int s_seg, s_r0, s_r1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    const int ns = lh_segments(cnt, layer, sib, n_sig, segs);
+    s_ns = ns;
+    // CTAs per non-empty segment: 1 + share of the rest by rows
+    long long R = 0;
+    int E = 0;
+    for (int s = 0; s < ns; ++s) {
+      R += segs[s].y;
+      E += segs[s].y > 0;
+    }
+    const int G = gridDim.x, Gp = G > E ? G - E : 0;
+    int cum = 0, seg = -1;
+    long long r0 = 0, r1 = 0;
+    for (int s = 0; s < ns && seg < 0; ++s) {
+      if (segs[s].y == 0) continue;
+      const int k = 1 + (int)((long long)Gp * segs[s].y / (R > 0 ? R : 1));
+      if ((int)blockIdx.x < cum + k) {
+        const int j = (int)blockIdx.x - cum;
+        seg = s;
+        r0 = (long long)segs[s].y * j / k;
+        r1 = (long long)segs[s].y * (j + 1) / k;
+      }
+      cum += k;
+    }
+    s_seg = seg;
+    s_r0 = (int)r0;
+    s_r1 = (int)r1;
+  }
+  // zero the histogram limbs
+  for (int i = threadIdx.x; i < lh_hist_bytes<NW>() / 16; i += kLhThreads)
+    reinterpret_cast<uint4*>(hb)[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  if (s_seg < 0) return;
+  const int4 sg = segs[s_seg];
+  const int r_begin = s_r0, r_end = s_r1;
+  const int* lr = lrow + sg.x;
+  const long long* lqs = lq + sg.x;
+  uint32_t* wbuf = bufs + warp * 32 * NW;
+  constexpr int CPR = NW / 4;  // 16-byte chunks per row
+
+  // per-lane constants of the rotated schedule
+  const uint32_t sel = NW == 16 ? ((lane & 1) ? 0x1032u : 0x3210u)
+                                : ((lane & 3) == 0 ? 0x3210u : (lane & 3) == 1 ? 0x0321u : (lane & 3) == 2 ? 0x1032u : 0x2103u);
+  const int gsh = NW == 16 ? (lane >> 1) : (lane >> 2);
+  uint32_t cb[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    if (NW == 16) {
+      const int c = (b + 2 * (lane & 1)) & 3;
+      cb[b] = 4u * (uint32_t)(32 * (c & 1) + 16 * ((c >> 1) & 1));
+    } else {
+      const int c = (b + lane) & 3;
+      cb[b] = 4u * (uint32_t)c;
+    }
+  }
+
+  for (int p0 = r_begin; p0 < r_end; p0 += kLhFlushRows) {
+    const int p1 = min(r_end, p0 + kLhFlushRows);
+    const int nsl = (p1 - p0 + 31) >> 5;  // 32-row slices of the piece; warp w takes w, w + 16, ...
+    // Pipeline per warp: the row codes of the next two slices are in flight
+    // in registers (4 lanes per row, 16-byte coalesced loads) while the
+    // current slice, stored to the warp's shared buffer, is accumulated.
+    uint32_t* sbuf = wbuf;  // [32 rows][NW]
+    auto entry = [&](int j, int& row, long long& qq) {  // the lane's own list entry of slice j
+      const int sl = warp + kLhWarps * j;
+      const int e = p0 + 32 * sl + lane;
+      row = -1;
+      qq = 0;
+      if (sl < nsl && e < p1) {
+        row = __ldg(lr + e);
+        qq = __ldg(lqs + e);
+      }
+    };
+    auto fetch = [&](int row_of_lane, uint4 (&x)[CPR]) {  // lane loads chunk (lane % CPR) of rows lane / CPR + (32 / CPR) t
+#pragma unroll
+      for (int t = 0; t < CPR; ++t) {
+        const int rr = lane / CPR + (32 / CPR) * t;
+        const int srow = __shfl_sync(0xffffffffu, row_of_lane, rr);
+        x[t] = srow >= 0 ? __ldg(reinterpret_cast<const uint4*>(rc + (size_t)srow * NW) + (lane % CPR))
+                         : make_uint4(0u, 0u, 0u, 0u);
+      }
+    };
+    auto store = [&](const uint4 (&x)[CPR]) {
+#pragma unroll
+      for (int t = 0; t < CPR; ++t) {
+        const int rr = lane / CPR + (32 / CPR) * t;
+        reinterpret_cast<uint4*>(sbuf + rr * NW)[lane % CPR] = x[t];
+      }
+    };
+    auto accumulate = [&](long long qq) {
+      const uint32_t qlo = (uint32_t)((unsigned long long)qq & 0xffffull);
+      const uint32_t qhi = (uint32_t)(int)(qq >> 16);
+      const uint32_t* rowp = sbuf + lane * NW;
+      // rows past the piece end carry q = 0 (zero codes): branch-free
+#pragma unroll 4
+      for (int w = 0; w < NW; ++w) {
+        const int g = (w + gsh) & (NW - 1);
+        const uint32_t word = __byte_perm(rowp[g], 0u, sel);
+        const uint32_t g4 = (uint32_t)(NW == 16 ? 4 * g : 16 * g);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint32_t off = __byte_perm(word, g4 + cb[b], 0x5504u | ((uint32_t)b << 4));
+          atomicAdd(reinterpret_cast<uint32_t*>(hb + off), qlo);
+          atomicAdd(reinterpret_cast<uint32_t*>(hb + off + (NW == 16 ? 65536u : 128u)), qhi);
+        }
+      }
+    };
+    const int nj = nsl > warp ? (nsl - warp + kLhWarps - 1) / kLhWarps : 0;  // this warp's slices
+    // kLhPf slices in flight in registers (register-file capacity, not shared
+    // memory, bounds the bytes in flight: 16 warps x kLhPf x 32 rows x NW words)
+    int rr_;
+    long long qv[kLhPf];
+    uint4 xv[kLhPf][CPR];
+#pragma unroll
+    for (int u = 0; u < kLhPf; ++u) {
+      entry(u, rr_, qv[u]);
+      fetch(rr_, xv[u]);
+    }
+    for (int j = 0; j < nj; j += kLhPf) {
+#pragma unroll
+      for (int u = 0; u < kLhPf; ++u) {
+        if (j + u < nj) {
+          store(xv[u]);
+          __syncwarp();
+          long long qn;
+          entry(j + u + kLhPf, rr_, qn);
+          fetch(rr_, xv[u]);
+          accumulate(qv[u]);
+          qv[u] = qn;
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+    // ---- flush: lanes take 32 features whose slots sit in distinct banks (a
+    // bin's slot row read is one wavefront; reading one feature's bins would
+    // hit one bank 32 times), warps take bins; int64 rows [feature][bin]
+    // (pitch B + 2) are staged in the drained buffers and added to the global
+    // layer histogram with one bulk reduction per row
+    const uint32_t* lo = reinterpret_cast<const uint32_t*>(hb);
+    long long* stg = reinterpret_cast<long long*>(bufs);
+    const int pitch = B + 2;
+    // NW = 16: 2 rounds of 32 feature rows, warps take bins; NW = 8 (2 CTAs
+    // per SM, half the staging): 2 rounds of 16 rows, half-warps take bins
+    constexpr int RPR = NW == 16 ? 32 : 16;  // staged rows per round
+#pragma unroll 1
+    for (int round = 0; round < 2; ++round) {
+      const int f = NW == 16 ? 4 * (lane & 15) + 2 * (lane >> 4) + round : (lane & 15) + 16 * round;
+      const int srow = NW == 16 ? lane : (lane & 15);
+      if (f < d) {
+        const int wa = lh_slot_word<NW>(f);
+        const int b0 = NW == 16 ? warp : 2 * warp + (lane >> 4), bstep = NW == 16 ? kLhWarps : 2 * kLhWarps;
+        for (int bin = b0; bin < B; bin += bstep) {
+          const int v = bin + 1 - code_off;  // stored code of this bin
+          long long val = 0;
+          if (v >= 0 && v < 256) {
+            if (NW == 16) val = (long long)(int)lo[16384 + v * 64 + wa] * 65536ll + (long long)lo[v * 64 + wa];
+            else val = (long long)(int)lo[v * 64 + 32 + wa] * 65536ll + (long long)lo[v * 64 + wa];
+          }
+          stg[(size_t)srow * pitch + bin] = val;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x < RPR) {
+        const int ff = NW == 16 ? 4 * (threadIdx.x & 15) + 2 * (threadIdx.x >> 4) + round : threadIdx.x + 16 * round;
+        if (ff < d)
+          bulk_reduce_add_u64(hist + (((size_t)sg.w * nodes + sg.z) * d + ff) * B, stg + (size_t)threadIdx.x * pitch,
+                              (unsigned)B * 8u);
+      }
+      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncthreads();
+    }
+    if (p1 < r_end) {
+      for (int i = threadIdx.x; i < lh_hist_bytes<NW>() / 16; i += kLhThreads)
+        reinterpret_cast<uint4*>(hb)[i] = make_uint4(0u, 0u, 0u, 0u);
+      __syncthreads();
+    }
+  }
+}
+
+// Row-major copy of the tiled column-major codes (u8): rc[row][NW words],
+// bytes of features >= d zero.  One CTA per 1024-row tile.
+template <int NW>
+__global__ void __launch_bounds__(256) k_rowcodes(const uint8_t* __restrict__ codes, int64_t n, int d,
+                                                  uint32_t* __restrict__ rc) {
+  extern __shared__ __align__(16) unsigned char rk_sm[];
+  const int64_t tile = blockIdx.x;
+  const uint8_t* src = codes + tile * (int64_t)d * kTile;
+  const int bytes = d * kTile;
+  for (int i = threadIdx.x; i < bytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(rk_sm)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+  __syncthreads();
+  for (int r = threadIdx.x; r < kTile; r += blockDim.x) {
+    const int64_t row = tile * kTile + r;
+    if (row >= n) break;
+    uint32_t wv[NW];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int f = 4 * j + b;
+        if (f < d) x |= (uint32_t)rk_sm[f * kTile + r] << (8 * b);
+      }
+      wv[j] = x;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(rc + row * NW);
+#pragma unroll
+    for (int j = 0; j < NW / 4; ++j) dst[j] = make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]);
+  }
+}
+
+}  // namespace bb

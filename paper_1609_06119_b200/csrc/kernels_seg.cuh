@@ -773,8 +773,11 @@ __global__ void __launch_bounds__(64) k_seg_chain(SegArgs a) {
   long long p = p0;
   if (s0 < S) {
     long long used;
-    i = walk(a, r0, p0, anc + jb.tab[s0].off - p0, i, jb.k, jb.J, lane, &used);  // n-1 >= kSegTail: never ends the job
-    p = anc + jb.tab[s0].off;
+    // the anchor slack (up to kAnchorSlackMax draws) can exceed a short job's
+    // whole draw count: the job may end inside this walk, so the position
+    // is where the walk stopped, not the anchor
+    i = walk(a, r0, p0, anc + jb.tab[s0].off - p0, i, jb.k, jb.J, lane, &used);
+    p = p0 + used;
   }
   int s = s0;
   for (; s < S && i >= kSegTail; ++s) {

@@ -48,24 +48,93 @@ __global__ void k_iota(int* __restrict__ a, int64_t n) {
 // ---------------------------------------------------------------- refresh
 // F += gamma_prev[node] (score update of the previous tree, all rows), then
 // responses, boost weights and the quantised effective weight of tree t.
+// Row lists are appended per CTA tile: entries are ranked per key in shared
+// memory, one global atomic per (tile, key) reserves their block (a global
+// counter per key hit by every warp serialises at L2: 5x slower at cfg3).
+constexpr int kListTileRows = 2048;  // rows per CTA tile (512 threads x 4)
+constexpr int kListThreads = 512;
+
 template <typename NodeT>
-__global__ void k_update_refresh(int64_t n, int64_t n_sig, double* __restrict__ F, NodeT* __restrict__ node,
-                                 const double* __restrict__ w, long long* __restrict__ q,
-                                 const unsigned int* __restrict__ mask, const double* __restrict__ nw_prev,
-                                 double two_s) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double f = F[i];
-    if (nw_prev) {
-      f = __dadd_rn(f, nw_prev[node[i]]);
-      F[i] = f;
+__global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, int64_t n_sig, double* __restrict__ F,
+                                                                NodeT* __restrict__ node, const double* __restrict__ w,
+                                                                long long* __restrict__ q,
+                                                                const unsigned int* __restrict__ mask,
+                                                                const double* __restrict__ nw_prev, double two_s,
+                                                                int* __restrict__ cnt, int* __restrict__ lrow,
+                                                                long long* __restrict__ lq) {
+  __shared__ int s_cnt[2], s_base[2];
+  constexpr int R = kListTileRows / kListThreads;
+  for (int64_t t0 = (int64_t)blockIdx.x * kListTileRows; t0 < n; t0 += (int64_t)gridDim.x * kListTileRows) {
+    if (lrow && threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    if (lrow) __syncthreads();
+    int loc[R];
+    long long qs[R];
+    double fr[R], wr[R];
+    unsigned mw[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {  // loads first: their latencies overlap
+      const int64_t i = t0 + k * kListThreads + threadIdx.x;
+      const bool in = i < n;
+      fr[k] = in ? F[i] : 0.0;
+      wr[k] = (in && w) ? w[i] : 1.0;
+      mw[k] = in ? mask[i >> 5] : 0u;
     }
-    const int lab = row_label(i, n_sig);
-    const double r = residual_of(f, lab);
-    const double bw = boost_weight_of(r);
-    const bool act = (mask[i >> 5] >> (i & 31)) & 1u;
-    const double wi = w ? w[i] : 1.0;
-    q[i] = act ? __double2ll_rn(__dmul_rn(__dmul_rn(wi, bw), two_s)) : 0ll;
-    node[i] = 0;
+    if (nw_prev) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int64_t i = t0 + k * kListThreads + threadIdx.x;
+        if (i < n) {
+          fr[k] = __dadd_rn(fr[k], nw_prev[node[i]]);
+          F[i] = fr[k];
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int64_t i = t0 + k * kListThreads + threadIdx.x;
+      loc[k] = -1;
+      qs[k] = 0;
+      if (i < n) {
+        const int lab = row_label(i, n_sig);
+        const double r = residual_of(fr[k], lab);
+        const double bw = boost_weight_of(r);
+        const bool act = (mw[k] >> (i & 31)) & 1u;
+        const long long qv = act ? __double2ll_rn(__dmul_rn(__dmul_rn(wr[k], bw), two_s)) : 0ll;
+        q[i] = qv;
+        node[i] = 0;
+        qs[k] = qv;
+        if (lrow && act) loc[k] = i < n_sig ? 0 : 1;  // class, ranked below
+      }
+      // layer-1 row lists (kernels_hist_list.cuh): class regions [0, n_sig),
+      // [n_sig, n); one shared atomic per warp and class
+      if (lrow) {
+        const int lane = threadIdx.x & 31, cls = loc[k];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const unsigned m = __ballot_sync(0xffffffffu, cls == c);
+          if (!m) continue;
+          const int leader = __ffs(m) - 1;
+          int b0 = 0;
+          if (lane == leader) b0 = atomicAdd(&s_cnt[c], __popc(m));
+          b0 = __shfl_sync(0xffffffffu, b0, leader);
+          if (cls == c) loc[k] = (c << 30) | (b0 + __popc(m & ((1u << lane) - 1u)));
+        }
+      }
+    }
+    if (!lrow) continue;
+    __syncthreads();
+    if (threadIdx.x < 2) s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(cnt + threadIdx.x, s_cnt[threadIdx.x]) : 0;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      if (loc[k] < 0) continue;
+      const int64_t i = t0 + k * kListThreads + threadIdx.x;
+      const int c = loc[k] >> 30;
+      const int64_t pos = (c ? n_sig : 0) + s_base[c] + (loc[k] & 0x3fffffff);
+      lrow[pos] = (int)i;
+      lq[pos] = qs[k];
+    }
+    __syncthreads();
   }
 }
 
@@ -714,6 +783,7 @@ __global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restric
 }
 
 // ---------------------------------------------------------------- advance
+constexpr int kAdvMaxNodes = 128;  // layer nodes with row lists (depth <= 8)
 // Move every row at the layer to its child (trees.py:207-228 for active rows,
 // which traverse_bins, trees.py:318-330, repeats for all rows): left iff
 // code <= cut; invalid cut or missing code parks the row.  Advancing ALL rows
@@ -721,39 +791,120 @@ __global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restric
 // the active rows' (eff, resp) fixed-point sums are accumulated per final
 // node, from which k_node_weights derives every node's sums (trees.py:231-244).
 template <typename CodeT, typename NodeT>
-__global__ void __launch_bounds__(512) k_advance(const CodeT* __restrict__ codes, int d, int code_off,
-                                                 NodeT* __restrict__ node, int64_t n, int64_t n_sig, int start,
-                                                 int tree, int n_internal, TreeArrays ta, int last_layer, int n_nodes,
-                                                 const long long* __restrict__ q, const unsigned int* __restrict__ mask,
-                                                 const double* __restrict__ F, const double* __restrict__ w,
-                                                 double two_s, unsigned long long* __restrict__ sums) {
+__global__ void __launch_bounds__(kListThreads, 4) k_advance(const CodeT* __restrict__ codes, int d, int code_off,
+                                                         NodeT* __restrict__ node, int64_t n, int64_t n_sig, int start,
+                                                         int tree, int n_internal, TreeArrays ta, int last_layer,
+                                                         int n_nodes, const long long* __restrict__ q,
+                                                         const unsigned int* __restrict__ mask,
+                                                         const double* __restrict__ F, const double* __restrict__ w,
+                                                         double two_s, unsigned long long* __restrict__ sums,
+                                                         int* __restrict__ cnt, int* __restrict__ lrow,
+                                                         long long* __restrict__ lq, int sib) {
   extern __shared__ uint32_t s_sums[];  // [2 cls][n_nodes][2 kinds] 2-limb
+  __shared__ int s_reg[2 * kAdvMaxNodes];  // list region of (class, node of this layer)
+  __shared__ int s_cnt[4 * kAdvMaxNodes], s_base[4 * kAdvMaxNodes];  // per (child, class) of the tile
+  constexpr int R = kListTileRows / kListThreads;
   const int* feat = ta.feature + (int64_t)tree * n_internal;
   const int* cutp = ta.cut + (int64_t)tree * n_internal;
   const unsigned char* vld = ta.valid + (int64_t)tree * n_internal;
+  const bool lists = lrow != nullptr && !last_layer;
+  const int nodes = start + 1;           // nodes of this layer: heap [start, 2 start]
+  const int c0 = 2 * start + 1, nkeys = 4 * nodes;  // children heap [c0, c0 + 2 nodes), key = 2 (child - c0) + class
   if (last_layer) {
     for (int i = threadIdx.x; i < 2 * n_nodes * 2 * 2; i += blockDim.x) s_sums[i] = 0u;
-    __syncthreads();
   }
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int nd = node[i];
-    if (nd >= start && vld[nd]) {
-      const int c = (int)codes[code_index(i, feat[nd], d)] + code_off;
-      if (c != 0) {
-        nd = 2 * nd + 1 + (c > cutp[nd] ? 1 : 0);
+  if (lists && threadIdx.x == 0) {
+    // class-major prefix of this layer's active counts (kernels_hist_list.cuh lh_segments)
+    int off = 0;
+    for (int k = 0; k < 2; ++k)
+      for (int p = 0; p < nodes; ++p) {
+        s_reg[k * nodes + p] = off;
+        off += cnt[2 * (start + p) + k];
+      }
+  }
+  for (int64_t t0 = (int64_t)blockIdx.x * kListTileRows; t0 < n; t0 += (int64_t)gridDim.x * kListTileRows) {
+    if (lists) {
+      for (int k = threadIdx.x; k < nkeys; k += blockDim.x) s_cnt[k] = 0;
+    }
+    __syncthreads();
+    // loads batched across the tile's R rows per thread (node ids, then the
+    // cut tables, then the code gathers) so their latencies overlap
+    int key[R], loc[R], ndv[R], fv[R];
+    bool act[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int64_t i = t0 + k * kListThreads + threadIdx.x;
+      ndv[k] = i < n ? (int)node[i] : -1;
+      act[k] = i < n && ((mask[i >> 5] >> (i & 31)) & 1u);
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const bool go = ndv[k] >= start && vld[ndv[k]];
+      fv[k] = go ? feat[ndv[k]] : -1;
+    }
+    int cv[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int64_t i = t0 + k * kListThreads + threadIdx.x;
+      cv[k] = fv[k] >= 0 ? (int)codes[code_index(i, fv[k], d)] + code_off : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int64_t i = t0 + k * kListThreads + threadIdx.x;
+      key[k] = -1;
+      loc[k] = 0;
+      int nd = ndv[k];
+      if (fv[k] >= 0 && cv[k] != 0) {
+        nd = 2 * nd + 1 + (cv[k] > cutp[nd] ? 1 : 0);
         node[i] = (NodeT)nd;
+        if (lists && act[k]) key[k] = 2 * (nd - c0) + (i < n_sig ? 0 : 1);
+      }
+      if (last_layer && act[k]) {
+        const int lab = row_label(i, n_sig);
+        const int cls = lab > 0 ? 0 : 1;
+        const double r = residual_of(F[i], lab);
+        const double wi = w ? w[i] : 1.0;
+        const long long qr = __double2ll_rn(__dmul_rn(__dmul_rn(wi, r), two_s));
+        uint32_t* sp = s_sums + 4 * (cls * n_nodes + nd);
+        slot_add(sp, q[i]);
+        slot_add(sp + 2, qr);
       }
     }
-    if (last_layer && ((mask[i >> 5] >> (i & 31)) & 1u)) {
-      const int lab = row_label(i, n_sig);
-      const int cls = lab > 0 ? 0 : 1;
-      const double r = residual_of(F[i], lab);
-      const double wi = w ? w[i] : 1.0;
-      const long long qr = __double2ll_rn(__dmul_rn(__dmul_rn(wi, r), two_s));
-      uint32_t* s = s_sums + 4 * (cls * n_nodes + nd);
-      slot_add(s, q[i]);
-      slot_add(s + 2, qr);
+    if (!lists) continue;
+    {  // rank within the tile: one shared atomic per warp and key
+      const int lane = threadIdx.x & 31;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const unsigned grp = __match_any_sync(0xffffffffu, key[k]);
+        const int leader = __ffs(grp) - 1;
+        int b0 = 0;
+        if (key[k] >= 0 && lane == leader) b0 = atomicAdd(&s_cnt[key[k]], __popc(grp));
+        b0 = __shfl_sync(0xffffffffu, b0, leader);
+        loc[k] = b0 + __popc(grp & ((1u << lane) - 1u));
+      }
     }
+    __syncthreads();
+    // active rows entering a child: counted per (child, class); the rows of
+    // the children a histogram builds are listed in the parent's region (left
+    // child from its start, right child from its end)
+    for (int k = threadIdx.x; k < nkeys; k += blockDim.x)
+      s_base[k] = s_cnt[k] ? atomicAdd(cnt + 2 * c0 + k, s_cnt[k]) : 0;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      if (key[k] < 0) continue;
+      const int child = c0 + (key[k] >> 1), cls = key[k] & 1;
+      const bool left = child & 1;
+      if (!left && sib) continue;
+      const int par = (child - 1) >> 1;
+      const int old = s_base[key[k]] + loc[k];
+      const int reg = s_reg[cls * nodes + (par - start)];
+      const int pos = left ? reg + old : reg + cnt[2 * par + cls] - 1 - old;
+      const int64_t i = t0 + k * kListThreads + threadIdx.x;
+      lrow[pos] = (int)i;
+      lq[pos] = q[i];
+    }
+    __syncthreads();
   }
   if (last_layer) {
     __syncthreads();

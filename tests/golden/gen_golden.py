@@ -271,10 +271,56 @@ def gen_model_doc():
     np.save(os.path.join(HERE, "ref_model_pred.npy"), predict_batch(f, X[:300]))
 
 
+def gen_huge(which):
+    """Full-size / near-full-size reference runs (tens of minutes on one core).
+    Only compact outputs are stored: cuts, thresholds, node weights, per-tree
+    leaf and mask hashes, the node audit and predictions on a row subset."""
+    def slim(arrs):
+        arrs.pop("node_purity", None)
+        return arrs
+
+    if "cfg2" in which:  # BASELINE configs[1] exactly: 1M rows x 40, 200 trees
+        X, y, w, kw = make_config("cfg2")
+        cfg = FitConfig(n_trees=200, depth=3, shrinkage=0.1, subsample=0.5, binning_levels=8, seed=0)
+        np.savez_compressed(os.path.join(HERE, "cfg2_full_fit.npz"),
+                            **slim(run_fit(X, y, w, cfg, np.arange(0, X.shape[0], 100))))
+        print("cfg2 full done", flush=True)
+    if "cfg3" in which:  # configs[2] at its full 10M rows, first 4 of 400 trees
+        X, y, w, kw = make_config("cfg3")
+        cfg = FitConfig(n_trees=4, depth=5, shrinkage=0.05, subsample=0.5, binning_levels=8, seed=0)
+        np.savez_compressed(os.path.join(HERE, "cfg3_10M_prefix.npz"),
+                            **slim(run_fit(X, y, w, cfg, np.arange(0, X.shape[0], 1000))))
+        print("cfg3 prefix done", flush=True)
+    if "cfg5" in which:  # configs[4] generator, 1M-row slice x 100 features, 1024 bins, depth 6
+        X, y, w, kw = make_config("cfg5", n=1_000_000)
+        cfg = FitConfig(n_trees=3, depth=6, shrinkage=0.1, subsample=0.5, binning_levels=10, seed=0)
+        np.savez_compressed(os.path.join(HERE, "cfg5_1M_slice.npz"),
+                            **slim(run_fit(X, y, w, cfg, np.arange(0, X.shape[0], 100))))
+        print("cfg5 slice done", flush=True)
+    if "cfg4" in which:  # configs[3]: the full 1000-tree depth-3 forest on the first 100k rows
+        Xa, _, _, _ = make_config("cfg4", n=100_000)
+        bnd = np.stack([fit_binning(Xa[:, j], 8).boundaries for j in range(Xa.shape[1])])
+        feat, cut, thr, nw = make_apply_forest(bnd, n_trees=1000, depth=3, seed=1)
+        forest = bb.Forest(
+            f0=0.0,
+            trees=[bt.Tree(depth=3, feature=feat[t], cut_bin=cut[t], threshold=thr[t], gain=np.zeros(7),
+                           valid=np.ones(7, bool), node_weight=nw[t], node_purity=np.zeros(15)) for t in range(1000)],
+            binnings=[fit_binning(Xa[:, j], 8) for j in range(Xa.shape[1])],
+        )
+        np.savez_compressed(os.path.join(HERE, "apply_cfg4_1000trees.npz"), boundaries=bnd,
+                            pred=predict_batch(forest, Xa.astype(np.float64), threads=8))
+        print("cfg4 forest done", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the cfg2 slice and cfg3 proxy (minutes)")
+    ap.add_argument("--huge", nargs="*", default=None,
+                    help="only the full-size runs: any of cfg2 cfg3 cfg4 cfg5 (default all; ~30 min)")
     args = ap.parse_args()
+    if args.huge is not None:
+        gen_huge(set(args.huge or ["cfg2", "cfg3", "cfg4", "cfg5"]))
+        return
 
     gen_kats(os.path.join(HERE, "kats.json"))
     gen_binning(os.path.join(HERE, "binning_random.npz"))

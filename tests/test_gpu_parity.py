@@ -96,6 +96,21 @@ def _np_masks(seed, a, b, rate, T):
                                              (5, 0, 9, 0.5, 2), (8, 2_000_003, 1_048_577, 0.5, 1),
                                              (17, 300_000, 700_000, 0.5, 10)])
 def test_gpu_subsample_masks_match_numpy(seed, a, b, rate, T):
+    _check_masks(seed, a, b, rate, T)
+
+
+# short jobs next to huge ones: the anchor slack (up to 4000 draws) exceeds the
+# short job's whole draw count, so it ends inside the chain's first walk
+# (kernels_seg.cuh k_seg_chain); then the BASELINE class-block sizes: cfg3
+# 5M/5M and cfg5 20M/30M (datagen proportions), chained trees
+@pytest.mark.parametrize("seed,a,b,rate,T", [(1, 2_100, 10_000_000, 0.5, 2), (4, 2_500, 1_000_000, 0.5, 50),
+                                             (6, 3_000_000, 2_049, 0.5, 3), (0, 5_000_000, 5_000_000, 0.5, 3),
+                                             (0, 20_000_000, 30_000_000, 0.5, 2)])
+def test_gpu_subsample_masks_large_blocks(seed, a, b, rate, T):
+    _check_masks(seed, a, b, rate, T)
+
+
+def _check_masks(seed, a, b, rate, T):
     cfg = _lib.FitConfigC(**_lib.pcg_config(seed))
     words = (a + b + 31) // 32
     bits = np.zeros(max(1, words) * T, np.uint32)
@@ -139,15 +154,15 @@ def _oracle_hist(codes, node, q, n_sig, d, levels, layer):
     return out
 
 
-@pytest.fixture(params=["fl", "fl_partials", "warp", "cta", "global"])
+@pytest.fixture(params=["list", "fl", "fl_partials", "warp", "cta", "global"])
 def hist_path(request, monkeypatch):
-    """Every histogram kernel: the feature-lane one (default where its plan
-    fits; TMA bulk reductions into the histogram, or with BB_FL_PARTIALS=1
-    per-CTA partial rows summed by k_fl_reduce), the warp-independent
-    shared-memory one, the CTA-barrier one and the global-atomic one
-    (BB_HIST_PATH = fl | w | cta | g)."""
-    monkeypatch.setenv("BB_HIST_PATH", {"fl": "fl", "fl_partials": "fl", "warp": "w", "cta": "cta", "global": "g"}[
-        request.param])
+    """Every histogram kernel: the node-partitioned row-list one (default for
+    u8 codes and d <= 64), the feature-lane one (TMA bulk reductions into the
+    histogram, or with BB_FL_PARTIALS=1 per-CTA partial rows summed by
+    k_fl_reduce), the warp-independent shared-memory one, the CTA-barrier one
+    and the global-atomic one (BB_HIST_PATH = list | fl | w | cta | g)."""
+    monkeypatch.setenv("BB_HIST_PATH", {"list": "list", "fl": "fl", "fl_partials": "fl", "warp": "w", "cta": "cta",
+                                        "global": "g"}[request.param])
     if request.param == "fl_partials":
         monkeypatch.setenv("BB_FL_PARTIALS", "1")
     return request.param
@@ -156,15 +171,56 @@ def hist_path(request, monkeypatch):
 @pytest.mark.parametrize("levels,layer,d", [(8, 1, 10), (8, 3, 40), (8, 5, 7), (10, 6, 3), (3, 2, 5), (1, 1, 2),
                                              (8, 2, 50), (8, 4, 33), (6, 3, 17), (8, 2, 70), (4, 3, 100)])
 def test_layer_hist_exact(levels, layer, d, hist_path):
+    if hist_path == "list" and (d > 64 or levels > 8):
+        pytest.skip("row-list kernel: u8 codes, d <= 64 (other shapes take the other kernels)")
     rng = np.random.default_rng(levels * 100 + layer)
     n, n_sig = 60_000, 23_456
-    codes, node, q = _random_layer(rng, n, n_sig, d, levels, layer)
+    # u8 codes with B = 256 hold no NaN bin (the fit stores code - 1)
+    nan_rate = 0.0 if (hist_path == "list" and levels == 8) else 0.05
+    codes, node, q = _random_layer(rng, n, n_sig, d, levels, layer, nan_rate=nan_rate)
     B = 1 << levels
     nodes = 1 << (layer - 1)
     out = np.zeros((2, nodes, d, B), np.int64)
     _lib.check(_lib.lib().bb_layer_hist(_lib.context(), _lib.ptr(codes), _lib.ptr(node), _lib.ptr(q), n, n_sig, d,
                                         levels, layer, _lib.ptr(out)))
     np.testing.assert_array_equal(out, _oracle_hist(codes, node, q, n_sig, d, levels, layer))
+
+
+def test_layer_hist_list_long_runs(monkeypatch):
+    """Row-list kernel with > kLhFlushRows (32767) rows per CTA (mid-run
+    flushes of the 16/16-bit limbs), the largest |q| and one tied bin."""
+    monkeypatch.setenv("BB_HIST_PATH", "list")
+    rng = np.random.default_rng(6)
+    n, n_sig, d, levels, layer = 12_000_000, 4_400_001, 3, 8, 1
+    codes, node, q = _random_layer(rng, n, n_sig, d, levels, layer, nan_rate=0.0)
+    q[::7] = (1 << 32) - 1
+    q[3::11] = -((1 << 32) - 1)
+    codes[1, : n // 2] = 17
+    B = 1 << levels
+    out = np.zeros((2, 1, d, B), np.int64)
+    _lib.check(_lib.lib().bb_layer_hist(_lib.context(), _lib.ptr(codes), _lib.ptr(node), _lib.ptr(q), n, n_sig, d,
+                                        levels, layer, _lib.ptr(out)))
+    np.testing.assert_array_equal(out, _oracle_hist(codes, node, q, n_sig, d, levels, layer))
+
+
+@pytest.mark.parametrize("name,n,T,D,L", [("cfg3", 300_000, 6, 5, 8), ("cfg1", 50_000, 8, 3, 8),
+                                          ("cfg2", 200_000, 8, 4, 8), ("cfg2", 100_000, 5, 6, 6)])
+def test_fit_list_path_matches_fl(name, n, T, D, L, monkeypatch):
+    """The fit with the row-list histogram (default) against the same fit on
+    the feature-lane / warp kernels: identical cuts, leaves and weights."""
+    X, y, w, _ = make_config(name, n=n)
+    cfg = FitConfig(n_trees=T, depth=D, shrinkage=0.1, subsample=0.5, binning_levels=L, seed=4)
+    monkeypatch.setenv("BB_HIST_PATH", "list")
+    a = fit_forest(X, y, w, cfg, return_leaves=True)
+    monkeypatch.setenv("BB_HIST_PATH", "w")
+    b = fit_forest(X, y, w, cfg, return_leaves=True)
+    for ta, tb in zip(a.trees, b.trees):
+        np.testing.assert_array_equal(ta.valid, tb.valid)
+        np.testing.assert_array_equal(ta.feature, tb.feature)
+        np.testing.assert_array_equal(ta.cut_bin, tb.cut_bin)
+        np.testing.assert_array_equal(ta.node_weight, tb.node_weight)
+        np.testing.assert_array_equal(ta.gain, tb.gain)
+    np.testing.assert_array_equal(a.fit_info["leaves"], b.fit_info["leaves"])
 
 
 def test_layer_hist_fl_long_runs(monkeypatch):

@@ -137,7 +137,8 @@ int bb_predict(bb_ctx* ctx, const bb_forest* forest, const void* X, int32_t x_dt
 
 /* Parity entry points ------------------------------------------------ */
 
-/* Boundaries [d][B-1] and codes [d][n] (int16, input row order). */
+/* Boundaries [d][B-1] and codes [d][n] (int16, input row order; out_codes
+ * may be NULL: boundaries only). */
 int bb_bin(bb_ctx* ctx, const void* X, int32_t x_dtype, int64_t n, int32_t d, int32_t levels,
            double* out_boundaries, int16_t* out_codes);
 

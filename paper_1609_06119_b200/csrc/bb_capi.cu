@@ -1905,15 +1905,17 @@ int bb_bin(bb_ctx* ctx, const void* X, int32_t x_dtype, int64_t n, int32_t d, in
       double* bounds = A.alloc<double>((size_t)d * nt);
       K* bkeys = A.alloc<K>((size_t)d * nt);
       run_select<T>(c, A, keys, n, d, levels, fdev, bounds, bkeys);
-      int* pos = A.alloc<int>(n);
-      k_iota<<<grid_for(n, 256, c.sm_count), 256, 0, st>>>(pos, n);
-      BB_LAUNCH_CHECK();
-      uint16_t* codes = A.alloc<uint16_t>((size_t)d * n);
-      k_codes<K, uint16_t><<<dim3((unsigned)std::max<int64_t>(1, ceil_div(n, 1024)), d), 256, (size_t)nt * sizeof(K), st>>>(
-          keys, n, nt, bkeys, pos, codes, n, 0, d, 0);
-      BB_LAUNCH_CHECK();
       BB_CUDA(cudaMemcpyAsync(out_boundaries, bounds, (size_t)d * nt * 8, cudaMemcpyDeviceToHost, st));
-      BB_CUDA(cudaMemcpyAsync(out_codes, codes, (size_t)d * n * 2, cudaMemcpyDeviceToHost, st));
+      if (out_codes) {  // null: boundaries only
+        int* pos = A.alloc<int>(n);
+        k_iota<<<grid_for(n, 256, c.sm_count), 256, 0, st>>>(pos, n);
+        BB_LAUNCH_CHECK();
+        uint16_t* codes = A.alloc<uint16_t>((size_t)d * n);
+        k_codes<K, uint16_t><<<dim3((unsigned)std::max<int64_t>(1, ceil_div(n, 1024)), d), 256, (size_t)nt * sizeof(K),
+                               st>>>(keys, n, nt, bkeys, pos, codes, n, 0, d, 0);
+        BB_LAUNCH_CHECK();
+        BB_CUDA(cudaMemcpyAsync(out_codes, codes, (size_t)d * n * 2, cudaMemcpyDeviceToHost, st));
+      }
       BB_CUDA(cudaStreamSynchronize(st));
     };
     if (x_dtype == BB_F32) body(float{});

@@ -68,12 +68,23 @@ def _cfg2(seed, n):
     return X, y, w
 
 
-def _cfg4(seed, n, d=40, chunk=1 << 20):
-    rng = np.random.Generator(np.random.PCG64(seed))
+def _cfg4(seed, n, d=40, chunk=1 << 20, threads=None):
+    """N(0,1) rows; chunk c of 2^20 rows comes from PCG64(seed) jumped c
+    times (chunk 0 is the plain seed-1 stream), so the 100M-row apply set is
+    generated in parallel and any prefix is reproducible on its own."""
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+
     X = np.empty((n, d), dtype=np.float32)
-    for lo in range(0, n, chunk):
-        hi = min(n, lo + chunk)
-        X[lo:hi] = rng.standard_normal((hi - lo, d))
+    base = np.random.PCG64(seed)
+
+    def fill(c):
+        lo, hi = c * chunk, min(n, (c + 1) * chunk)
+        X[lo:hi] = np.random.Generator(base.jumped(c) if c else np.random.PCG64(seed)).standard_normal((hi - lo, d))
+
+    nc = (n + chunk - 1) // chunk
+    with ThreadPoolExecutor(max_workers=threads or min(32, os.cpu_count() or 1)) as pool:
+        list(pool.map(fill, range(nc)))
     return X, None, None
 
 

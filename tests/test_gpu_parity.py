@@ -534,3 +534,90 @@ def test_sharded_fit_world1_matches_single(weighted):
         np.testing.assert_array_equal(ta.cut_bin[ta.valid], tb.cut_bin[tb.valid])
         np.testing.assert_array_equal(ta.node_weight, tb.node_weight)
     np.testing.assert_array_equal(got.fit_info["leaves"], ref.fit_info["leaves"])
+
+
+# ------------------------------------------------------------ full-size configs
+def _fit_golden_config(name, fixture, golden_dir, n=None):
+    g = np.load(f"{golden_dir}/{fixture}")
+    X, y, w, _ = make_config(name, n=n)
+    T, D, eta, alpha, L, seed = g["config"]
+    cfg = FitConfig(n_trees=int(T), depth=int(D), shrinkage=float(eta), subsample=float(alpha),
+                    binning_levels=int(L), seed=int(seed))
+    forced = _forced_from_golden(g)
+    forest = fit_forest(X, y, w, cfg, forced_cuts=forced, return_leaves=True)
+    return g, X, forest, forced
+
+
+def test_fit_cfg2_full_vs_reference_golden(golden_dir):
+    """BASELINE configs[1] exactly (1M rows x 40, 200 trees) against the
+    unmodified reference: no tie-ambiguous node, so free-running; every cut,
+    threshold and per-row leaf id of all 200 trees, probabilities <= 1e-5."""
+    g, X, forest, forced = _fit_golden_config("cfg2", "cfg2_full_fit.npz", golden_dir)
+    assert not forced
+    assert forest.f0 == float(g["f0"])
+    _check_fit_vs_golden(forest, g, X[g["pred_rows"]])
+
+
+def test_fit_cfg3_10M_prefix_vs_reference_golden(golden_dir):
+    """BASELINE configs[2] at its full 10M rows x 50 features: the first 4
+    of the 400 depth-5 trees (a fit's first trees do not depend on the tree
+    count) against the reference, free-running."""
+    g, X, forest, forced = _fit_golden_config("cfg3", "cfg3_10M_prefix.npz", golden_dir)
+    assert not forced
+    _check_fit_vs_golden(forest, g, X[g["pred_rows"]])
+
+
+def test_fit_cfg5_1M_slice_vs_reference_golden(golden_dir):
+    """BASELINE configs[4] generator (t3 + Gaussian mixtures, exponential
+    weights, 40% signal) on a 1M-row slice x 100 features, 1024 bins (u16
+    codes), depth 6, against the reference (not only the fixed-point
+    oracle)."""
+    g, X, forest, forced = _fit_golden_config("cfg5", "cfg5_1M_slice.npz", golden_dir, n=1_000_000)
+    assert not forced
+    _check_fit_vs_golden(forest, g, X[g["pred_rows"]])
+
+
+def test_apply_cfg4_1000_trees_vs_reference_golden(golden_dir):
+    """BASELINE configs[3]: the full 1000-tree depth-3 forest (seed 1) over
+    the first 100k rows of the seed-1 N(0,1) data, boundaries fitted on those
+    rows, against the reference's predict_batch."""
+    from paper_1609_06119_b200.engine import FeatureBinning, Forest, Tree
+
+    g = np.load(f"{golden_dir}/apply_cfg4_1000trees.npz")
+    X, _, _, _ = make_config("cfg4", n=100_000)
+    bnd = g["boundaries"]
+    b, _ = gpu_bin(X, 8)
+    np.testing.assert_array_equal(b, bnd)
+    from paper_1609_06119_b200.datagen import make_apply_forest
+
+    feat, cut, thr, nw = make_apply_forest(bnd, n_trees=1000, depth=3, seed=1)
+    trees = [Tree(depth=3, feature=feat[t], cut_bin=cut[t], threshold=thr[t], gain=np.zeros(7),
+                  valid=np.ones(7, bool), node_weight=nw[t], node_purity=np.zeros(15)) for t in range(1000)]
+    forest = Forest(f0=0.0, trees=trees, binnings=[FeatureBinning(bnd[j], 8) for j in range(X.shape[1])])
+    for arr in (X, X.astype(np.float64)):
+        p = predict_batch(forest, arr)
+        assert np.max(np.abs(p - g["pred"])) <= 1e-15
+
+
+def test_binning_cfg3_full_and_cfg5_50M_columns():
+    """bb_bin bit-exact against the oracle: all 50 cfg3 features at 10M rows,
+    and 10 cfg5-shaped columns (5 Student-t(3), 5 Gaussian mixtures) at 50M
+    rows, 1024 bins."""
+    X, _, _, _ = make_config("cfg3")
+    b, c = gpu_bin(X, 8)
+    for j in range(X.shape[1]):
+        ref_b = oracle.fit_boundaries(X[:, j], 8)
+        np.testing.assert_array_equal(b[j], ref_b, err_msg=f"cfg3 feature {j}")
+        np.testing.assert_array_equal(c[j], oracle.bin_codes(ref_b, X[:, j]), err_msg=f"cfg3 feature {j}")
+    del X, b, c
+    rng = np.random.Generator(np.random.PCG64(55))
+    n = 50_000_000
+    cols = np.empty((n, 10), np.float32)
+    for j in range(5):
+        cols[:, j] = rng.standard_t(3, n)
+        cols[:, 5 + j] = np.where(rng.random(n) < 0.5, -1.0, 1.0) + 0.5 * rng.standard_normal(n)
+    b, c = gpu_bin(cols, 10)
+    for j in range(10):
+        ref_b = oracle.fit_boundaries(cols[:, j], 10)
+        np.testing.assert_array_equal(b[j], ref_b, err_msg=f"cfg5 column {j}")
+        np.testing.assert_array_equal(c[j], oracle.bin_codes(ref_b, cols[:, j]), err_msg=f"cfg5 column {j}")

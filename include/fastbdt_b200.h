@@ -22,6 +22,11 @@
  *   bb_pairwise_sum
  *               numpy's pairwise float64 sum used by prior (boosting.py:76-83);
  *               host only
+ *   bb_roc_auc  replaces binboost.analysis.roc_auc (pkg/src/binboost/analysis.py:45-70)
+ *   bb_elim_create / bb_elim_fit / bb_elim_destroy
+ *               the refits of binboost.analysis.elimination_importance
+ *               (analysis.py:104-173, fit loop :136-142): training rows binned
+ *               once, each refit on a feature subset returns its validation AUC
  *
  * Conventions: every function returns BB_OK (0) or an error code and sets a
  * thread-local message readable with bb_last_error().  BB_EINVAL maps to the
@@ -163,6 +168,28 @@ int bb_subsample_masks_gpu(bb_ctx* ctx, int64_t n_sig, int64_t n_bkg, double rat
 int bb_subsample_masks(int64_t n_sig, int64_t n_bkg, double rate, int32_t n_trees, const bb_fit_config* rng,
                        uint32_t* out_bits);
 double bb_pairwise_sum(const double* a, int64_t n);
+
+/* Analysis ------------------------------------------------------------ */
+
+/* Weighted ROC AUC of host scores (labels y01 > 0 = signal; w may be NULL).
+ * BB_EINVAL if either class has non-positive total weight. */
+int bb_roc_auc(bb_ctx* ctx, const double* scores, const int8_t* y01, const double* w, int64_t n, double* out_auc);
+
+/* Elimination session: training rows X[n][d] (row-major, x_dtype), y01, w
+ * (NULL = unit) binned once with `levels`; validation rows Xv[n_val][d]
+ * binned with the training boundaries.  Read-only after creation: refits may
+ * run concurrently from several contexts on the session's device. */
+typedef struct bb_elim bb_elim;
+int bb_elim_create(bb_ctx* ctx, const void* X, int32_t x_dtype, int64_t n, int32_t d, const int8_t* y01,
+                   const double* w, int32_t levels, const void* Xv, int64_t n_val, const int8_t* y01_val,
+                   const double* w_val, bb_elim** out);
+/* Refit on feature columns cols[n_cols] (the forest's feature j is column
+ * cols[j]); out_auc (may be NULL) = validation AUC; out (may be NULL)
+ * receives the forest arrays like bb_fit (boundaries, leaves, scores and
+ * timing are not written). */
+int bb_elim_fit(bb_ctx* ctx, const bb_elim* session, const int32_t* cols, int32_t n_cols, const bb_fit_config* cfg,
+                double* out_auc, bb_fit_out* out);
+int bb_elim_destroy(bb_elim* session);
 
 #ifdef __cplusplus
 }

@@ -103,6 +103,12 @@ _SIGS = {
     "bb_subsample_masks_gpu": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_int32,
                                          C.POINTER(FitConfigC), C.c_void_p]),
     "bb_pairwise_sum": (C.c_double, [C.c_void_p, C.c_int64]),
+    "bb_roc_auc": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "bb_elim_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
+                                 C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "bb_elim_fit": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(FitConfigC), C.c_void_p,
+                              C.c_void_p]),
+    "bb_elim_destroy": (C.c_int, [C.c_void_p]),
 }
 
 _lib = None
@@ -159,6 +165,23 @@ def context(device: int = 0):
             h = out
             _ctx[device] = h
         return h
+
+
+_pool = {}
+
+
+def worker_contexts(device: int, k: int) -> list:
+    """k contexts on `device` (the first is the process-wide one): each owns a
+    CUDA stream, so calls from different threads run concurrently."""
+    with _ctx_lock:
+        pool = _pool.setdefault(device, [])
+    first = context(device)
+    with _ctx_lock:
+        while len(pool) < k - 1:
+            out = C.c_void_p()
+            check(lib().bb_ctx_create(device, C.byref(out)))
+            pool.append(out)
+        return [first] + pool[: k - 1]
 
 
 def pcg_config(seed) -> dict:

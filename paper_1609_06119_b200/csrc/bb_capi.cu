@@ -30,6 +30,7 @@
 #include "kernels_tree.cuh"
 #include "kernels_hist_fl.cuh"
 #include "kernels_hist_list.cuh"
+#include "kernels_auc.cuh"
 
 namespace bb {
 
@@ -1616,12 +1617,335 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   }
 }
 
+// ------------------------------------------------------------- ROC AUC
+// analysis.py:45-70 on the device (kernels_auc.cuh).  p, y01, w (w may be
+// null) are device arrays of n rows; returns the AUC and the class totals.
+static double auc_device(Ctx& c, Arena& A, const double* p, const int8_t* y01, const double* w, int64_t n,
+                         double* w_sig_out, double* w_bkg_out) {
+  cudaStream_t st = c.stream;
+  unsigned long long* k[2] = {A.alloc<unsigned long long>(n), A.alloc<unsigned long long>(n)};
+  unsigned int* v[2] = {A.alloc<unsigned int>(n), A.alloc<unsigned int>(n)};
+  const int tiles = (int)ceil_div(n, kAucTile);
+  unsigned int* cnt = A.alloc<unsigned int>((size_t)kAucDigits * tiles);
+  k_auc_keys<<<grid_for(n, 256, c.sm_count), 256, 0, st>>>(p, n, k[0], v[0]);
+  BB_LAUNCH_CHECK();
+  int cur = 0;
+  for (int shift = 0; shift < 64; shift += 4) {
+    k_radix_count<<<tiles, kAucThreads, 0, st>>>(k[cur], n, shift, tiles, cnt);
+    k_radix_scan<<<1, 1024, 0, st>>>(cnt, kAucDigits * tiles);
+    k_radix_scatter<<<tiles, kAucThreads, 0, st>>>(k[cur], v[cur], n, shift, tiles, cnt, k[cur ^ 1], v[cur ^ 1]);
+    BB_LAUNCH_CHECK();
+    cur ^= 1;
+  }
+  double* S = A.alloc<double>(n);
+  double* Bc = A.alloc<double>(n);
+  long long* start = A.alloc<long long>(n);
+  k_auc_prep<<<grid_for(n, 256, c.sm_count), 256, 0, st>>>(k[cur], v[cur], reinterpret_cast<const signed char*>(y01),
+                                                           w, n, S, Bc, start);
+  BB_LAUNCH_CHECK();
+  const int nb = (int)ceil_div(n, 1024);
+  double* sums_d = A.alloc<double>(nb);
+  long long* sums_l = A.alloc<long long>(nb);
+  for (double* a : {S, Bc}) {
+    k_scan_tiles<double, false><<<nb, 1024, 0, st>>>(a, n, sums_d, 0.0);
+    k_scan_sums_serial<double, false><<<1, 1024, 0, st>>>(sums_d, nb, 0.0);
+    k_scan_add<double, false><<<nb, 1024, 0, st>>>(a, n, sums_d);
+    BB_LAUNCH_CHECK();
+  }
+  k_scan_tiles<long long, true><<<nb, 1024, 0, st>>>(start, n, sums_l, -1ll);
+  k_scan_sums_serial<long long, true><<<1, 1024, 0, st>>>(sums_l, nb, -1ll);
+  k_scan_add<long long, true><<<nb, 1024, 0, st>>>(start, n, sums_l);
+  BB_LAUNCH_CHECK();
+  const int tb = (int)std::min<int64_t>(1024, ceil_div(n, 256));
+  double* part = A.alloc<double>(tb);
+  k_auc_terms<<<tb, 256, 0, st>>>(k[cur], S, Bc, start, n, part);
+  BB_LAUNCH_CHECK();
+  std::vector<double> hp(tb);
+  double tot[2];
+  BB_CUDA(cudaMemcpyAsync(hp.data(), part, (size_t)tb * 8, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaMemcpyAsync(&tot[0], S + n - 1, 8, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaMemcpyAsync(&tot[1], Bc + n - 1, 8, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaStreamSynchronize(st));
+  double won = 0.0;
+  for (double x : hp) won += x;
+  *w_sig_out = tot[0];
+  *w_bkg_out = tot[1];
+  if (!(tot[0] > 0.0) || !(tot[1] > 0.0)) throw InvalidArg{"roc_auc needs both classes with positive total weight"};
+  return won / (tot[0] * tot[1]);
+}
+
+// ------------------------------------------------------------- elimination
+// Batched refits for elimination_importance (analysis.py:104-173): the
+// training rows are uploaded, class-blocked and binned ONCE (boundaries of a
+// feature do not depend on the other features), and the validation rows are
+// binned with the training boundaries once.  Each refit gathers the code
+// columns of its feature subset, runs the tree loop, applies the forest to
+// the validation codes (traverse over codes == traverse over values,
+// SURVEY.md A5) and computes the validation AUC on the device.  Refits of one
+// round run concurrently from several contexts (one stream each).
+struct ElimSession {
+  int device = 0;
+  int64_t n = 0, n_sig = 0, nv = 0;
+  int d = 0, levels = 0, B = 0, code_bytes = 1, code_off = 0;
+  void* codes = nullptr;     // training codes, tiled, class-block order
+  double* bounds = nullptr;  // [d][B-1]
+  double* w_cb = nullptr;    // class-block training weights (null: unit)
+  std::vector<unsigned long long> nans;
+  double f0 = 0.0;
+  int shift = 32;
+  void* vcodes = nullptr;    // validation codes, tiled, input row order
+  int8_t* vy = nullptr;
+  double* vw = nullptr;
+  std::vector<void*> owned;
+  template <typename T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    BB_CUDA(cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T)));
+    owned.push_back(p);
+    return reinterpret_cast<T*>(p);
+  }
+  ~ElimSession() {
+    cudaSetDevice(device);
+    for (void* p : owned) cudaFree(p);
+  }
+};
+
+template <typename CodeT>
+__global__ void k_gather_cols(const CodeT* __restrict__ src, int d, const int* __restrict__ cols, int nc,
+                              CodeT* __restrict__ dst) {
+  const int64_t tile = blockIdx.x;
+  const int j = blockIdx.y;
+  const CodeT* a = src + (tile * d + cols[j]) * (int64_t)kTile;
+  CodeT* b = dst + (tile * nc + j) * (int64_t)kTile;
+  for (int r = threadIdx.x; r < kTile; r += blockDim.x) b[r] = a[r];
+}
+
+// F and p over tiled validation codes: right iff code > cut_bin (code
+// 0 = missing stops), features mapped to the session's columns
+template <typename CodeT>
+__global__ void k_apply_codes(const CodeT* __restrict__ codes, int64_t n, int d, int code_off,
+                              const int* __restrict__ colmap, int T, int depth, const int* __restrict__ feat,
+                              const int* __restrict__ cut, const unsigned char* __restrict__ vld,
+                              const double* __restrict__ nw, double f0, double* __restrict__ p) {
+  const int I = (1 << depth) - 1, N = (1 << (depth + 1)) - 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double F = f0;
+    for (int t = 0; t < T; ++t) {
+      int nd = 0;
+      for (int l = 0; l < depth; ++l) {
+        const int e = t * I + nd;
+        if (!__ldg(&vld[e])) break;
+        const int c = (int)codes[code_index(i, __ldg(&colmap[__ldg(&feat[e])]), d)] + code_off;
+        if (c == 0) break;
+        nd = 2 * nd + 1 + (c > __ldg(&cut[e]) ? 1 : 0);
+      }
+      F = __dadd_rn(F, __ldg(&nw[(int64_t)t * N + nd]));
+    }
+    p[i] = sigmoid2(F);
+  }
+}
+
+template <typename T>
+static ElimSession* elim_prepare(Ctx& c, const T* X, int64_t n, int d, const int8_t* y, const double* w, int levels,
+                                 const T* Xv, int64_t nv, const int8_t* yv, const double* wv) {
+  using K = typename KeyOf<T>::K;
+  cudaStream_t st = c.stream;
+  auto S = std::make_unique<ElimSession>();
+  ElimSession& s = *S;
+  s.device = c.device;
+  s.n = n;
+  s.nv = nv;
+  s.d = d;
+  s.levels = levels;
+  s.B = 1 << levels;
+  const int nt = s.B - 1;
+  Arena A(st);
+  T* Xd = A.alloc<T>((size_t)n * d);
+  int8_t* yd = A.alloc<int8_t>(n);
+  BB_CUDA(cudaMemcpyAsync(Xd, X, (size_t)n * d * sizeof(T), cudaMemcpyHostToDevice, st));
+  BB_CUDA(cudaMemcpyAsync(yd, y, (size_t)n, cudaMemcpyHostToDevice, st));
+  double* wd = nullptr;
+  if (w) {
+    wd = A.alloc<double>(n);
+    BB_CUDA(cudaMemcpyAsync(wd, w, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  }
+  // class blocks (sample.py:112-116)
+  const int n_tiles = (int)ceil_div(n, CLS_TILE);
+  int* tile_sig = A.alloc<int>(n_tiles + 1);
+  int* pos = A.alloc<int>(n);
+  if (w) s.w_cb = s.alloc<double>(n);
+  k_class_tile_counts<<<n_tiles, 256, 0, st>>>(yd, n, tile_sig);
+  k_class_scan<<<1, 1024, 0, st>>>(tile_sig, n_tiles);
+  k_class_positions<<<n_tiles, 256, 0, st>>>(yd, n, tile_sig, pos, wd, s.w_cb);
+  BB_LAUNCH_CHECK();
+  int n_sig_i = 0;
+  BB_CUDA(cudaMemcpyAsync(&n_sig_i, tile_sig + n_tiles, 4, cudaMemcpyDeviceToHost, st));
+  BB_CUDA(cudaStreamSynchronize(st));
+  s.n_sig = n_sig_i;
+  if (s.n_sig == 0 || s.n_sig == n) throw InvalidArg{"training data must contain both classes"};
+  // prior (boosting.py:76-83) and the fixed-point shift, as fit_impl
+  double w_sig = (double)s.n_sig, w_bkg = (double)(n - s.n_sig), max_abs = 1.0;
+  if (w) {
+    std::vector<double> hw(s.w_cb ? (size_t)n : 0);
+    BB_CUDA(cudaMemcpyAsync(hw.data(), s.w_cb, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    BB_CUDA(cudaStreamSynchronize(st));
+    w_sig = pairwise(hw.data(), s.n_sig);
+    w_bkg = pairwise(hw.data() + s.n_sig, n - s.n_sig);
+    max_abs = 0.0;
+    for (double x : hw) {
+      if (!std::isfinite(x)) throw InvalidArg{"user weights must be finite"};
+      max_abs = std::max(max_abs, std::fabs(x));
+    }
+  }
+  s.f0 = (w_sig <= 0.0 || w_bkg <= 0.0) ? 0.0 : 0.5 * std::log(w_sig / w_bkg);
+  s.shift = fixed_shift_for(max_abs);
+  // binning of every feature over the training rows
+  std::vector<unsigned long long> finite;
+  unsigned long long* finite_dev = nullptr;
+  K* keys = make_keys<T>(c, A, Xd, n, d, finite, s.nans, &finite_dev);
+  s.bounds = s.alloc<double>((size_t)d * nt);
+  K* bkeys = A.alloc<K>((size_t)d * nt);
+  run_select<T>(c, A, keys, n, d, levels, finite_dev, s.bounds, bkeys);
+  bool any_nan = false;
+  for (int f = 0; f < d; ++f) any_nan |= s.nans[f] > 0;
+  s.code_bytes = (s.B <= 256) && (s.B <= 255 || !any_nan) ? 1 : 2;
+  s.code_off = (s.B == 256 && s.code_bytes == 1) ? 1 : 0;
+  const int64_t stride = ceil_div(n, kTile) * kTile;
+  auto emit = [&](const K* kk, int64_t rows, const int* pp, void* out) {
+    const dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 256 * 4), 4 * c.sm_count / d + 1)), d);
+    const int64_t str = ceil_div(rows, kTile) * kTile;
+    if (s.code_bytes == 1) {
+      if (rows % kTile)
+        BB_CUDA(cudaMemsetAsync((uint8_t*)out + (size_t)(ceil_div(rows, kTile) - 1) * d * kTile, 0, (size_t)d * kTile, st));
+      k_codes<K, uint8_t><<<g, 256, (size_t)nt * sizeof(K), st>>>(kk, rows, nt, bkeys, pp, (uint8_t*)out, str,
+                                                                  s.code_off, d, 1);
+    } else {
+      if (rows % kTile)
+        BB_CUDA(cudaMemsetAsync((uint16_t*)out + (size_t)(ceil_div(rows, kTile) - 1) * d * kTile, 0,
+                                (size_t)d * kTile * 2, st));
+      k_codes<K, uint16_t><<<g, 256, (size_t)nt * sizeof(K), st>>>(kk, rows, nt, bkeys, pp, (uint16_t*)out, str,
+                                                                   s.code_off, d, 1);
+    }
+    BB_LAUNCH_CHECK();
+  };
+  s.codes = s.code_bytes == 1 ? (void*)s.alloc<uint8_t>((size_t)d * stride) : (void*)s.alloc<uint16_t>((size_t)d * stride);
+  emit(keys, n, pos, s.codes);
+  // validation rows: keys, codes with the training boundaries, input order
+  if (nv > 0) {
+    T* Xvd = A.alloc<T>((size_t)nv * d);
+    BB_CUDA(cudaMemcpyAsync(Xvd, Xv, (size_t)nv * d * sizeof(T), cudaMemcpyHostToDevice, st));
+    std::vector<unsigned long long> f2, n2;
+    unsigned long long* fd2 = nullptr;
+    K* vkeys = make_keys<T>(c, A, Xvd, nv, d, f2, n2, &fd2);
+    int* vpos = A.alloc<int>(nv);
+    k_iota<<<grid_for(nv, 256, c.sm_count), 256, 0, st>>>(vpos, nv);
+    const int64_t vstride = ceil_div(nv, kTile) * kTile;
+    s.vcodes = s.code_bytes == 1 ? (void*)s.alloc<uint8_t>((size_t)d * vstride)
+                                 : (void*)s.alloc<uint16_t>((size_t)d * vstride);
+    emit(vkeys, nv, vpos, s.vcodes);
+    s.vy = s.alloc<int8_t>(nv);
+    BB_CUDA(cudaMemcpyAsync(s.vy, yv, (size_t)nv, cudaMemcpyHostToDevice, st));
+    if (wv) {
+      s.vw = s.alloc<double>(nv);
+      BB_CUDA(cudaMemcpyAsync(s.vw, wv, (size_t)nv * 8, cudaMemcpyHostToDevice, st));
+    }
+  }
+  BB_CUDA(cudaStreamSynchronize(st));
+  return S.release();
+}
+
+static void elim_fit(Ctx& c, const ElimSession& s, const int* cols, int nc, const bb_fit_config& cfg, double* auc,
+                     bb_fit_out* fo) {
+  if (nc < 1 || nc > s.d) throw InvalidArg{"need 1..d feature columns"};
+  for (int j = 0; j < nc; ++j)
+    if (cols[j] < 0 || cols[j] >= s.d) throw InvalidArg{"feature column out of range"};
+  if (cfg.binning_levels != s.levels) throw InvalidArg{"binning_levels differs from the prepared session"};
+  cudaStream_t st = c.stream;
+  Arena A(st);
+  const int64_t tiles = ceil_div(s.n, kTile);
+  int* cd = A.alloc<int>(nc);
+  BB_CUDA(cudaMemcpyAsync(cd, cols, (size_t)nc * 4, cudaMemcpyHostToDevice, st));
+  const int nt = s.B - 1;
+  double* bsub = A.alloc<double>((size_t)nc * nt);
+  for (int j = 0; j < nc; ++j)
+    BB_CUDA(cudaMemcpyAsync(bsub + (size_t)j * nt, s.bounds + (size_t)cols[j] * nt, (size_t)nt * 8,
+                            cudaMemcpyDeviceToDevice, st));
+  bool any_nan = false;
+  for (int j = 0; j < nc; ++j) any_nan |= s.nans[cols[j]] > 0;
+  const int D = cfg.depth, T = cfg.n_trees, I = (1 << D) - 1, N = (1 << (D + 1)) - 1;
+  FitShape fs{s.n, s.n_sig, nc, s.levels, s.B, D, I, N, T};
+  std::vector<int> feat((size_t)T * I), cut((size_t)T * I);
+  std::vector<unsigned char> vld((size_t)T * I);
+  std::vector<double> gain((size_t)T * I), thr((size_t)T * I), nw((size_t)T * N), pur((size_t)T * N);
+  bb_fit_out o{};
+  if (fo) o = *fo;
+  if (!o.feature) o.feature = feat.data();
+  if (!o.cut_bin) o.cut_bin = cut.data();
+  if (!o.valid) o.valid = vld.data();
+  if (!o.gain) o.gain = gain.data();
+  if (!o.threshold) o.threshold = thr.data();
+  if (!o.node_weight) o.node_weight = nw.data();
+  if (!o.node_purity) o.node_purity = pur.data();
+  o.leaves = nullptr;
+  o.scores = nullptr;
+  FitStats stats;
+  Shard shard;
+  MaskFeed feed;
+  feed.init(c, A, s.n, s.n_sig, cfg, shard, &stats);
+  feed.ahead(0);
+  double ms = 0.0;
+  auto go = [&](auto* codes) {
+    using CodeT = std::remove_pointer_t<decltype(codes)>;
+    CodeT* sub = A.alloc<CodeT>((size_t)tiles * nc * kTile);
+    k_gather_cols<CodeT><<<dim3((unsigned)tiles, nc), 256, 0, st>>>(codes, s.d, cd, nc, sub);
+    BB_LAUNCH_CHECK();
+    if (D <= 7)
+      run_trees<CodeT, uint8_t>(c, A, fs, sub, s.code_off, s.w_cb, s.f0, s.shift, cfg, nullptr, 0, bsub, &o, &ms,
+                                stats, shard, any_nan, feed);
+    else
+      run_trees<CodeT, uint16_t>(c, A, fs, sub, s.code_off, s.w_cb, s.f0, s.shift, cfg, nullptr, 0, bsub, &o, &ms,
+                                 stats, shard, any_nan, feed);
+  };
+  if (s.code_bytes == 1) go(static_cast<uint8_t*>(s.codes));
+  else go(static_cast<uint16_t*>(s.codes));
+  if (fo) {
+    if (fo->f0) *fo->f0 = s.f0;
+    if (fo->fixed_shift) *fo->fixed_shift = s.shift;
+  }
+  if (!auc || s.nv == 0) return;
+  // validation AUC of the refit
+  int* fd = A.alloc<int>((size_t)T * I);
+  int* cutd = A.alloc<int>((size_t)T * I);
+  unsigned char* vd = A.alloc<unsigned char>((size_t)T * I);
+  double* nwd = A.alloc<double>((size_t)T * N);
+  std::vector<int> fz((size_t)T * I);
+  for (size_t e = 0; e < fz.size(); ++e) fz[e] = o.valid[e] ? o.feature[e] : 0;
+  BB_CUDA(cudaMemcpyAsync(fd, fz.data(), fz.size() * 4, cudaMemcpyHostToDevice, st));
+  BB_CUDA(cudaMemcpyAsync(cutd, o.cut_bin, (size_t)T * I * 4, cudaMemcpyHostToDevice, st));
+  BB_CUDA(cudaMemcpyAsync(vd, o.valid, (size_t)T * I, cudaMemcpyHostToDevice, st));
+  BB_CUDA(cudaMemcpyAsync(nwd, o.node_weight, (size_t)T * N * 8, cudaMemcpyHostToDevice, st));
+  double* p = A.alloc<double>(s.nv);
+  const int g = grid_for(s.nv, 256, c.sm_count);
+  if (s.code_bytes == 1)
+    k_apply_codes<uint8_t><<<g, 256, 0, st>>>(static_cast<const uint8_t*>(s.vcodes), s.nv, s.d, s.code_off, cd, T, D,
+                                              fd, cutd, vd, nwd, s.f0, p);
+  else
+    k_apply_codes<uint16_t><<<g, 256, 0, st>>>(static_cast<const uint16_t*>(s.vcodes), s.nv, s.d, s.code_off, cd, T,
+                                               D, fd, cutd, vd, nwd, s.f0, p);
+  BB_LAUNCH_CHECK();
+  double ws, wb;
+  *auc = auc_device(c, A, p, s.vy, s.vw, s.nv, &ws, &wb);
+}
+
 }  // namespace bb
 
 using namespace bb;
 
 struct bb_ctx {
   Ctx c;
+};
+struct bb_elim {
+  ElimSession* s;
 };
 
 template <typename Fn>
@@ -2144,3 +2468,68 @@ int bb_subsample_masks_gpu(bb_ctx* ctx, int64_t n_sig, int64_t n_bkg, double rat
 double bb_pairwise_sum(const double* a, int64_t n) { return pairwise(a, n); }
 
 }  // extern "C"
+
+int bb_roc_auc(bb_ctx* ctx, const double* scores, const int8_t* y01, const double* w, int64_t n, double* out_auc) {
+  return guarded([&] {
+    if (!ctx || !scores || !y01 || !out_auc) throw InvalidArg{"null argument"};
+    if (n < 1) throw InvalidArg{"roc_auc needs both classes with positive total weight"};
+    std::lock_guard<std::mutex> lock(ctx->c.mu);
+    Ctx& c = ctx->c;
+    BB_CUDA(cudaSetDevice(c.device));
+    Arena A(c.stream);
+    double* p = A.alloc<double>(n);
+    int8_t* y = A.alloc<int8_t>(n);
+    double* wd = w ? A.alloc<double>(n) : nullptr;
+    BB_CUDA(cudaMemcpyAsync(p, scores, (size_t)n * 8, cudaMemcpyHostToDevice, c.stream));
+    BB_CUDA(cudaMemcpyAsync(y, y01, (size_t)n, cudaMemcpyHostToDevice, c.stream));
+    if (w) BB_CUDA(cudaMemcpyAsync(wd, w, (size_t)n * 8, cudaMemcpyHostToDevice, c.stream));
+    double ws, wb;
+    *out_auc = auc_device(c, A, p, y, wd, n, &ws, &wb);
+  });
+}
+
+int bb_elim_create(bb_ctx* ctx, const void* X, int32_t x_dtype, int64_t n, int32_t d, const int8_t* y01,
+                   const double* w, int32_t levels, const void* Xv, int64_t n_val, const int8_t* y01_val,
+                   const double* w_val, bb_elim** out) {
+  return guarded([&] {
+    if (!ctx || !X || !y01 || !out) throw InvalidArg{"null argument"};
+    if (n < 2 || d < 1) throw InvalidArg{"need at least 2 rows and 1 feature"};
+    if (n >= (int64_t)1 << 31 || n_val >= (int64_t)1 << 31) throw InvalidArg{"at most 2^31-1 rows per device"};
+    if (levels < 1 || levels > 11) throw InvalidArg{"binning_levels must be in [1, 11] on the GPU path"};
+    if (n_val > 0 && (!Xv || !y01_val)) throw InvalidArg{"null validation argument"};
+    std::lock_guard<std::mutex> lock(ctx->c.mu);
+    BB_CUDA(cudaSetDevice(ctx->c.device));
+    ElimSession* s;
+    if (x_dtype == BB_F32)
+      s = elim_prepare<float>(ctx->c, (const float*)X, n, d, y01, w, levels, (const float*)Xv, n_val, y01_val, w_val);
+    else if (x_dtype == BB_F64)
+      s = elim_prepare<double>(ctx->c, (const double*)X, n, d, y01, w, levels, (const double*)Xv, n_val, y01_val,
+                               w_val);
+    else
+      throw InvalidArg{"x_dtype must be BB_F32 or BB_F64"};
+    *out = new bb_elim{s};
+  });
+}
+
+int bb_elim_fit(bb_ctx* ctx, const bb_elim* e, const int32_t* cols, int32_t n_cols, const bb_fit_config* cfg,
+                double* out_auc, bb_fit_out* out) {
+  return guarded([&] {
+    if (!ctx || !e || !cols || !cfg) throw InvalidArg{"null argument"};
+    if (cfg->n_trees < 1) throw InvalidArg{"n_trees must be >= 1"};
+    if (cfg->depth < 1 || cfg->depth > 15) throw InvalidArg{"depth must be in [1, 15]"};
+    if (!(cfg->shrinkage > 0.0 && cfg->shrinkage <= 1.0)) throw InvalidArg{"shrinkage must be in (0, 1]"};
+    if (!(cfg->subsample > 0.0 && cfg->subsample <= 1.0)) throw InvalidArg{"subsample must be in (0, 1]"};
+    std::lock_guard<std::mutex> lock(ctx->c.mu);
+    BB_CUDA(cudaSetDevice(ctx->c.device));
+    if (e->s->device != ctx->c.device) throw InvalidArg{"session and context are on different devices"};
+    elim_fit(ctx->c, *e->s, cols, n_cols, *cfg, out_auc, out);
+  });
+}
+
+int bb_elim_destroy(bb_elim* e) {
+  return guarded([&] {
+    if (!e) return;
+    delete e->s;
+    delete e;
+  });
+}

@@ -312,12 +312,46 @@ def gen_huge(which):
         print("cfg4 forest done", flush=True)
 
 
+def gen_analysis(out):
+    """roc_auc on tied / weighted scores and a small elimination_importance
+    run (analysis.py:45-70, 104-173) by the unmodified reference."""
+    from binboost.analysis import elimination_importance, roc_auc
+
+    rng = np.random.default_rng(17)
+    arrs = {}
+    for k, (n, ties, weighted) in enumerate([(1000, False, False), (5000, True, True), (20000, True, False),
+                                            (777, False, True)]):
+        s = rng.normal(size=n)
+        if ties:
+            s = np.round(s * 4) / 4
+        lab = (rng.random(n) < 0.4).astype(np.int64)
+        w = rng.uniform(0.1, 3.0, n) if weighted else None
+        arrs[f"auc{k}_scores"] = s
+        arrs[f"auc{k}_labels"] = lab
+        if w is not None:
+            arrs[f"auc{k}_w"] = w
+        arrs[f"auc{k}_value"] = np.float64(roc_auc(s, lab, w))
+    X, y, w, _ = make_config("cfg2", n=6000)
+    X = X[:, [0, 5, 20, 25, 30, 35]]
+    cfg = FitConfig(n_trees=12, depth=3, shrinkage=0.2, subsample=0.5, binning_levels=6, seed=9)
+    rep = elimination_importance(X, y, w, cfg)
+    arrs.update(elim_X=X, elim_y=y, elim_w=w, elim_scores=rep.scores, elim_order=np.array(rep.order),
+                elim_step_aucs=np.array(rep.step_aucs), elim_n_fits=np.int64(rep.n_fits),
+                elim_config=np.array([cfg.n_trees, cfg.depth, cfg.shrinkage, cfg.subsample, cfg.binning_levels,
+                                      cfg.seed]))
+    np.savez_compressed(out, **arrs)
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--analysis", action="store_true", help="only the roc_auc / elimination goldens")
     ap.add_argument("--big", action="store_true", help="also the cfg2 slice and cfg3 proxy (minutes)")
     ap.add_argument("--huge", nargs="*", default=None,
                     help="only the full-size runs: any of cfg2 cfg3 cfg4 cfg5 (default all; ~30 min)")
     args = ap.parse_args()
+    if args.analysis:
+        gen_analysis(os.path.join(HERE, "analysis.npz"))
+        return
     if args.huge is not None:
         gen_huge(set(args.huge or ["cfg2", "cfg3", "cfg4", "cfg5"]))
         return

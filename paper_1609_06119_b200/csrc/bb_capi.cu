@@ -619,7 +619,20 @@ static SegPlan build_seg_plan(int n, long long slack) {
   while (seg_geom(n - 1, off, kSegTail, &t, 2 * slack)) {
     t.rec_off = P.n_rec;
     const int ns = t.nA + t.nB;
-    for (int q = 0; q < ns; q += kSubPerCta) P.tasks.push_back(int2{(int)P.tab.size(), q});
+    // phase-1 tasks (kernels_seg.cuh): one warp per piece whose window is a
+    // small share of its band (few ambiguous draws), else one warp per
+    // 512-state sub-window
+    auto piece = [&](int pl, int ph, int np, int code, int j0) {
+      if (np <= 0) return;
+      const double band = (double)smear_host((unsigned)ph) + 1.0;
+      if ((double)(ph - pl + 1 + kSub) * 64.0 <= band) {
+        P.tasks.push_back(int2{(int)P.tab.size(), code});
+      } else {
+        for (int j = 0; j < np; ++j) P.tasks.push_back(int2{(int)P.tab.size(), j0 + j});
+      }
+    };
+    piece(t.loA, t.hiA, t.nA, -1, 0);
+    piece(t.loB, t.hiB, t.nB, -2, t.nA);
     P.n_rec += ns;
     P.tab.push_back(t);
     off += t.len;
@@ -732,7 +745,7 @@ struct MaskGen {
       smax = std::max(smax, S[cc]);
       rmax = std::max(rmax, P.n_rec);
       if (getenv("BB_PARSE_PROFILE"))
-        fprintf(stderr, "seg plan n=%d: %d segments, %d phase-1 CTAs, %d records\n", n[cc], S[cc], n_tasks[cc], P.n_rec);
+        fprintf(stderr, "seg plan n=%d: %d segments, %d phase-1 pieces, %d records\n", n[cc], S[cc], n_tasks[cc], P.n_rec);
     }
     for (int q = 0; q < 2; ++q) {
       rec[q] = A.alloc<SegRec>((size_t)rmax);
@@ -871,7 +884,8 @@ struct MaskGen {
         SegArgs a = args(jj);
         a.func = job;
         a.emit = SegJob{};
-        k_seg_pass<<<job.n_tasks, kSegThreads, kSegPassSmem, sb>>>(a, job.n_tasks);
+        const int nbf = (int)ceil_div(job.n_tasks, kSubPerCta);
+        k_seg_pass<<<nbf, kSegThreads, kSegPassSmem, sb>>>(a, nbf);
         BB_LAUNCH_CHECK();
         launches += 1;
       }

@@ -230,7 +230,9 @@ struct SegArgs {
   long long* prof;
 };
 
-constexpr int kSegPassSmem = kSegMaxLen * 4;
+constexpr int kPieceWords = kSegMaxSub * 16;  // rank-mask words per piece (max)
+constexpr int kPieceSmemPerWarp = 2 * kPieceWords * 4;  // words + exclusive popcount prefix
+constexpr int kSegPassSmem = kSubPerCta * kPieceSmemPerWarp;  // phase 1: per-warp piece masks
 constexpr int kTabChunk = 64, kTabChunks = 4;  // table entries streamed into k_seg_compose
 #ifndef BB_CHAIN_SMEM_KB
 #define BB_CHAIN_SMEM_KB 0
@@ -262,6 +264,7 @@ __device__ __forceinline__ void seg_stage_cta(const SegArgs& a, const RngState& 
 // bitmask has 16 words; lane l < 16 owns word l (in a register, mirrored in
 // smem) and keeps `incl` = set bits in words <= l up to date, so a merge
 // finds its word with one ballot.
+template <bool kGlobalDraws>
 __device__ void seg_sub(const unsigned int* sd, int len, int lo, int W, unsigned int M, SegRec* out, int lane) {
   unsigned int wv = 0;
   if (lane < 16) wv = (lane == 0) ? 0xfffffffeu : 0xffffffffu;  // rank 0 is the base; ranks >= W sentinels
@@ -283,7 +286,7 @@ __device__ void seg_sub(const unsigned int* sd, int len, int lo, int W, unsigned
     for (int u = 0; u < kRows; ++u) {
       const int r = 32 * u + lane;
       const bool in = pos + r < len;
-      const int x = in ? (int)(sd[pos + r] & M) : 0x7fffffff;
+      const int x = in ? (int)((kGlobalDraws ? __ldg(sd + pos + r) : sd[pos + r]) & M) : 0x7fffffff;
       xs[u] = x;
       const bool acc = in && x <= a0 - r;
       sa[u] = __ballot_sync(0xffffffffu, acc);
@@ -364,6 +367,150 @@ __device__ __forceinline__ void seg_sub_geom(const SegTab& t, int j, int& lo, in
     lo = t.loB + kSub * (j - t.nA);
     W = min(kSub, t.hiB - lo + 1);
     M = smear((unsigned)t.hiB);
+  }
+}
+
+// Phase 1 over a whole piece (A or B) of a segment by ONE warp: the window
+// [lo, lo + W) of distinct start states is one interval [a, b] (the same
+// transfer-function bookkeeping as seg_sub), its rank bitmask (nsub * 512
+// ranks) in the warp's shared-memory words.  A draw is ambiguous only if it
+// falls inside the whole window (not once per 512-state sub-window), so the
+// piece costs one pass over the segment instead of nsub passes.  The result
+// is written as the piece's nsub sub-window records (SegRec format, read by
+// the chain unchanged): record j's base end = a_end + set bits of ranks
+// (0, 512 j], its own rank-0 bit cleared.
+__device__ void seg_piece(const SegArgs& ar, const RngState& r0, long long base, int len, int lo, int W, unsigned int M,
+                          int nsub, SegRec* out, unsigned int* sw, int lane) {
+  const unsigned FULL = 0xffffffffu;
+  const int NWp = nsub * 16;
+  const int K = (NWp + 31) >> 5;  // words per lane (contiguous)
+  const int w0 = lane * K, w1 = min(NWp, w0 + K);
+  int cnt = 0;
+  for (int w = w0; w < w1; ++w) {
+    const unsigned int v = (w == 0) ? 0xfffffffeu : 0xffffffffu;  // rank 0 is the base; ranks >= W sentinels
+    sw[w] = v;
+    cnt += __popc(v);
+  }
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __syncwarp();
+  const bool in_buf = base + len <= ar.n_draws;
+  int a = lo, b = lo + W - 1;
+  // the next 512-draw chunk is loaded while this one is classified
+  unsigned int nxt[kRows];
+  auto load = [&](int pos) {
+#pragma unroll
+    for (int u = 0; u < kRows; ++u) {
+      const int r = 32 * u + lane;
+      nxt[u] = (pos + r < len && in_buf) ? __ldg(ar.draws + base + pos + r) : 0u;
+    }
+    if (!in_buf)  // past the draw buffer (never for the configured sizes): jump-ahead per draw
+      for (int u = 0; u < kRows; ++u) {
+        const int r = 32 * u + lane;
+        if (pos + r < len) nxt[u] = seg_get(ar, r0, base + pos + r);
+      }
+  };
+  load(0);
+  for (int pos = 0; pos < len; pos += 32 * kRows) {
+    const int a0 = a, b0 = b;
+    unsigned sa[kRows], am[kRows];
+    int xs[kRows];
+    unsigned int cur[kRows];
+#pragma unroll
+    for (int u = 0; u < kRows; ++u) cur[u] = nxt[u];
+    if (pos + 32 * kRows < len) load(pos + 32 * kRows);
+#pragma unroll
+    for (int u = 0; u < kRows; ++u) {
+      const int r = 32 * u + lane;
+      const bool in = pos + r < len;
+      const int x = in ? (int)(cur[u] & M) : 0x7fffffff;
+      xs[u] = x;
+      const bool acc = in && x <= a0 - r;
+      sa[u] = __ballot_sync(FULL, acc);
+      am[u] = __ballot_sync(FULL, in && !acc && x <= b0);
+    }
+    unsigned amany = 0;
+    int tot = 0;
+#pragma unroll
+    for (int u = 0; u < kRows; ++u) {
+      amany |= am[u];
+      tot += __popc(sa[u]);
+    }
+    if (amany == 0) {
+      a -= tot;
+      b -= tot;
+      continue;
+    }
+#pragma unroll
+    for (int u = 0; u < kRows; ++u) {
+      unsigned acc = sa[u];
+      int mrow = 0;
+      unsigned rem = am[u];
+      while (rem) {
+        const int f = __ffs(rem) - 1;
+        rem &= rem - 1u;
+        const int nb = __popc(acc & ((1u << f) - 1u));
+        const int ac = a - nb, bc = b - nb - mrow;
+        const int xf = __shfl_sync(FULL, xs[u], f);
+        if (xf <= ac) {
+          acc |= 1u << f;
+        } else if (xf <= bc) {
+          // the groups at offsets xf - ac - 1 and xf - ac merge: clear the
+          // t-th set bit (1-based) of the rank mask
+          const int t = xf - ac;
+          const unsigned own = __ballot_sync(FULL, incl >= t);
+          const int ow = __ffs(own) - 1;
+          if (lane == ow) {
+            int tt = t - (incl - cnt);
+            for (int w = w0; w < w1; ++w) {
+              unsigned int m = sw[w];
+              const int pc = __popc(m);
+              if (tt <= pc) {
+                for (int z = 1; z < tt; ++z) m &= m - 1u;
+                sw[w] &= ~(m & (0u - m));
+                break;
+              }
+              tt -= pc;
+            }
+            --cnt;
+          }
+          if (lane >= ow) --incl;
+          ++mrow;
+        }
+      }
+      const int na = __popc(acc);
+      a -= na;
+      b -= na + mrow;
+    }
+  }
+  __syncwarp();
+  // exclusive popcount prefix of the words, then the sub-window records
+  unsigned int* pre = sw + kPieceWords;
+  {
+    int run = incl - cnt;
+    for (int w = w0; w < w1; ++w) {
+      pre[w] = (unsigned int)run;
+      run += __popc(sw[w]);
+    }
+  }
+  __syncwarp();
+  for (int j = 0; j < nsub; ++j) {
+    const int wb = 16 * j;
+    const unsigned int first = sw[wb];
+    const unsigned int bit0 = first & 1u;
+    if (lane < 16) {
+      const unsigned int wv = lane == 0 ? (first & ~1u) : sw[wb + lane];
+      out[j].words[lane] = wv;
+      out[j].pref[lane] = (unsigned short)(pre[wb + lane] - pre[wb] - (lane > 0 ? bit0 : 0u));
+    }
+    if (lane == 0) {
+      out[j].a_end = a + (int)(pre[wb] + bit0);
+      out[j].h = (int)(M >> 1);
+    }
   }
 }
 
@@ -598,23 +745,37 @@ __global__ void __launch_bounds__(kSegThreads) k_seg_pass(SegArgs a, int nb_func
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const RngState r0 = *a.rng0;
   if ((int)blockIdx.x < nb_func) {
+    // phase 1: one warp per piece (task = (segment, piece A / B))
     const SegJob& jb = a.func;
-    const int2 task = jb.tasks[blockIdx.x];
-    const SegTab t = jb.tab[task.x];
-    const long long p0 = *jb.anchor_in;
-    const long long c0 = clock64();
-    seg_stage_cta(a, r0, p0 + t.off, t.len, sd);
-    const int j = task.y + warp;
-    if (j < t.nA + t.nB) {
-      int lo, W;
-      unsigned int M;
-      seg_sub_geom(t, j, lo, W, M);
-      seg_sub(sd, t.len, lo, W, M, a.rec + t.rec_off + j, lane);
-    }
-    if (a.prof && lane == 0) {
-      atomicAdd((unsigned long long*)&a.prof[7], 1ull);
-      atomicAdd((unsigned long long*)&a.prof[8], (unsigned long long)(clock64() - c0));
-      atomicMax((unsigned long long*)&a.prof[9], (unsigned long long)(clock64() - c0));
+    const int task_i = (int)blockIdx.x * kSubPerCta + warp;
+    if (task_i < jb.n_tasks) {
+      const int2 task = jb.tasks[task_i];
+      const SegTab t = jb.tab[task.x];
+      const long long p0 = *jb.anchor_in;
+      const long long c0 = clock64();
+      unsigned int* sw = reinterpret_cast<unsigned int*>(ps_sm) + warp * (kPieceSmemPerWarp / 4);
+      if (task.y == -1) {
+        seg_piece(a, r0, p0 + t.off, t.len, t.loA, t.hiA - t.loA + 1, smear((unsigned)t.hiA), t.nA, a.rec + t.rec_off,
+                  sw, lane);
+      } else if (task.y == -2) {
+        seg_piece(a, r0, p0 + t.off, t.len, t.loB, t.hiB - t.loB + 1, smear((unsigned)t.hiB), t.nB,
+                  a.rec + t.rec_off + t.nA, sw, lane);
+      } else {
+        // a window that is a large share of its band: one warp per 512-state
+        // sub-window (dense ambiguous draws are cheaper in narrow windows)
+        int lo, W;
+        unsigned int M;
+        seg_sub_geom(t, task.y, lo, W, M);
+        if (p0 + t.off + t.len <= a.n_draws)
+          seg_sub<true>(a.draws + p0 + t.off, t.len, lo, W, M, a.rec + t.rec_off + task.y, lane);
+        else
+          seg_piece(a, r0, p0 + t.off, t.len, lo, W, M, 1, a.rec + t.rec_off + task.y, sw, lane);
+      }
+      if (a.prof && lane == 0) {
+        atomicAdd((unsigned long long*)&a.prof[7], 1ull);
+        atomicAdd((unsigned long long*)&a.prof[8], (unsigned long long)(clock64() - c0));
+        atomicMax((unsigned long long*)&a.prof[9], (unsigned long long)(clock64() - c0));
+      }
     }
   } else {
     const SegJob& jb = a.emit;

@@ -169,6 +169,15 @@ int bb_subsample_masks(int64_t n_sig, int64_t n_bkg, double rate, int32_t n_tree
                        uint32_t* out_bits);
 double bb_pairwise_sum(const double* a, int64_t n);
 
+/* Virtual shards: a group of `world` contexts of this process whose
+ * all-reduces go through host memory (rank-order sums) instead of NCCL, so
+ * the row-sharded fit runs with several shards on one GPU (parity tests;
+ * one thread per shard).  Bind each context with bb_ctx_init_virtual. */
+typedef struct bb_vgroup bb_vgroup;
+int bb_vgroup_create(int32_t world, bb_vgroup** out);
+int bb_vgroup_destroy(bb_vgroup* group);
+int bb_ctx_init_virtual(bb_ctx* ctx, int32_t rank, bb_vgroup* group);
+
 /* Analysis ------------------------------------------------------------ */
 
 /* Weighted ROC AUC of host scores (labels y01 > 0 = signal; w may be NULL).

@@ -2038,12 +2038,37 @@ int bb_ctx_init_comm(bb_ctx* ctx, int32_t rank, int32_t world, const uint8_t* un
   });
 }
 
+int bb_vgroup_create(int32_t world, bb_vgroup** out) {
+  return guarded([&] {
+    if (!out || world < 1) throw InvalidArg{"world must be >= 1"};
+    auto* g = new VirtualGroup();
+    g->world = world;
+    *out = reinterpret_cast<bb_vgroup*>(g);
+  });
+}
+
+int bb_vgroup_destroy(bb_vgroup* g) {
+  return guarded([&] { delete reinterpret_cast<VirtualGroup*>(g); });
+}
+
+int bb_ctx_init_virtual(bb_ctx* ctx, int32_t rank, bb_vgroup* g) {
+  return guarded([&] {
+    if (!ctx || !g) throw InvalidArg{"null argument"};
+    auto* vg = reinterpret_cast<VirtualGroup*>(g);
+    if (rank < 0 || rank >= vg->world) throw InvalidArg{"rank must be in [0, world)"};
+    std::lock_guard<std::mutex> lock(ctx->c.mu);
+    ctx->c.comm.init_virtual(rank, vg);
+  });
+}
+
 int bb_fit(bb_ctx* ctx, const void* X, int32_t x_dtype, int32_t x_on_device, int64_t n, int32_t d,
            const int8_t* y01, int32_t y_on_device, const double* w, int32_t w_on_device,
            const bb_fit_config* cfg, const bb_forced_cut* forced, int32_t n_forced, bb_fit_out* out) {
   return guarded([&] {
     if (!ctx || !cfg || !out) throw InvalidArg{"null argument"};
-    if (n < 2 || d < 1) throw InvalidArg{"need at least 2 rows and 1 feature"};
+    // a shard of a row-sharded fit may hold a single row (the class check
+    // runs on the global counts)
+    if (n < (ctx->c.comm.active() ? 1 : 2) || d < 1) throw InvalidArg{"need at least 2 rows and 1 feature"};
     if (n >= (int64_t)1 << 31) throw InvalidArg{"at most 2^31-1 rows per device"};
     if (cfg->n_trees < 1) throw InvalidArg{"n_trees must be >= 1"};
     if (cfg->depth < 1 || cfg->depth > 15) throw InvalidArg{"depth must be in [1, 15]"};

@@ -55,14 +55,76 @@ void NcclComm::init(int r, int w, const unsigned char* id) {
   check(lib().init(&comm, w, u, r), "ncclCommInitRank");
 }
 
+void VirtualGroup::barrier() {
+  std::unique_lock<std::mutex> lk(mu);
+  const long long g = generation;
+  if (++arrived == world) {
+    arrived = 0;
+    ++generation;
+    cv.notify_all();
+  } else {
+    cv.wait(lk, [&] { return generation != g; });
+  }
+}
+
+void NcclComm::init_virtual(int r, VirtualGroup* g) {
+  destroy();
+  rank = r;
+  world = g->world;
+  vgroup = g;
+}
+
+template <typename T>
+static void reduce_into(std::vector<std::vector<unsigned char>>& stage, size_t count, NcclOp op, T* out) {
+  for (size_t i = 0; i < count; ++i) {
+    T acc = reinterpret_cast<const T*>(stage[0].data())[i];
+    for (size_t r = 1; r < stage.size(); ++r) {
+      const T v = reinterpret_cast<const T*>(stage[r].data())[i];
+      acc = op == kNcclMax ? (v > acc ? v : acc) : (T)(acc + v);
+    }
+    out[i] = acc;
+  }
+}
+
 void NcclComm::all_reduce(void* buf, size_t count, NcclType t, NcclOp op, cudaStream_t st) {
   if (!active() || count == 0) return;
+  if (vgroup) {
+    const size_t es = (t == kNcclU32) ? 4 : 8;
+    VirtualGroup& g = *vgroup;
+    if (cudaStreamSynchronize(st) != cudaSuccess) throw std::runtime_error("virtual all_reduce: stream error");
+    {
+      std::lock_guard<std::mutex> lk(g.mu);
+      if (g.stage.size() != (size_t)g.world) g.stage.resize(g.world);
+    }
+    g.stage[rank].resize(count * es);
+    if (cudaMemcpyAsync(g.stage[rank].data(), buf, count * es, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      throw std::runtime_error("virtual all_reduce: copy");
+    g.barrier();  // every rank's contribution staged
+    std::vector<unsigned char> res(count * es);
+    switch (t) {
+      case kNcclU32: reduce_into<unsigned int>(g.stage, count, op, reinterpret_cast<unsigned int*>(res.data())); break;
+      case kNcclI64: reduce_into<long long>(g.stage, count, op, reinterpret_cast<long long*>(res.data())); break;
+      case kNcclU64:
+        reduce_into<unsigned long long>(g.stage, count, op, reinterpret_cast<unsigned long long*>(res.data()));
+        break;
+      case kNcclF64: reduce_into<double>(g.stage, count, op, reinterpret_cast<double*>(res.data())); break;
+    }
+    g.barrier();  // every rank has read the stage
+    // ordered on the fit's stream (a pageable cudaMemcpy may return before
+    // its DMA lands, and the fit's stream does not wait for the legacy one)
+    if (cudaMemcpyAsync(buf, res.data(), count * es, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      throw std::runtime_error("virtual all_reduce: copy back");
+    return;
+  }
   check(lib().all_reduce(buf, buf, count, (int)t, (int)op, comm, st), "ncclAllReduce");
 }
 
 void NcclComm::destroy() {
   if (comm) lib().destroy(comm);
   comm = nullptr;
+  vgroup = nullptr;
 }
 
 }  // namespace bb

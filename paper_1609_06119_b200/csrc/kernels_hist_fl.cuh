@@ -368,7 +368,7 @@ __device__ __forceinline__ void fl_run(int code_off, const NodeT* __restrict__ n
         bulk_reduce_add_u64(grow(nd, sub, f), st + rl * pitch, (unsigned)B * 8u);
       }
     }
-    asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+    asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
     __syncthreads();
   }
 }

@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
           bulk_reduce_add_u64(hist + (((size_t)sg.w * nodes + sg.z) * d + ff) * B, stg + (size_t)threadIdx.x * pitch,
                               (unsigned)B * 8u);
       }
-      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
       __syncthreads();
     }
     if (p1 < r_end) {

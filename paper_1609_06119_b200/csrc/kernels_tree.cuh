@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kHistWThreads, 1)
         bulk_reduce_add_u64(hist + (((int64_t)cls * p.nodes + ln) * d + (f0 + j)) * B, st + (size_t)rl * B,
                             (unsigned)B * 8u);
       }
-      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
       __syncthreads();
     }
     return;

@@ -32,7 +32,7 @@ import numpy as np
 from . import _lib
 from .engine import FitConfig, Forest, _as_features, _fit_native
 
-__all__ = ["sharded_prior", "comm_context", "fit_forest_sharded"]
+__all__ = ["sharded_prior", "comm_context", "fit_forest_sharded", "fit_forest_virtual_shards"]
 
 _comm_ctx: dict = {}
 _comm_lock = threading.Lock()
@@ -130,3 +130,64 @@ def fit_forest_sharded(X, y, weights=None, config: FitConfig | None = None, *, g
     ctx = comm_context(device, group)
     return _fit_native(X, xdt, False, n, d, y01, False, w, False, cfg, return_leaves=return_leaves,
                        return_scores=return_scores, device=device, ctx=ctx, f0_override=f0)
+
+
+def fit_forest_virtual_shards(shards, config: FitConfig | None = None, *, device: int = 0,
+                              return_leaves: bool = False) -> list:
+    """The row-sharded fit with ``len(shards)`` shards in ONE process (and on
+    one GPU): shard g = (X_g, y_g, w_g or None) is rank g's rows.  Each shard
+    runs bb_fit in its own thread on its own context; the contexts share a
+    virtual group whose all-reduces sum in host memory (bb_vgroup_*), so the
+    library executes exactly the sharded code path (global binning from
+    exchanged radix histograms, class offsets, global masks sliced to the
+    local rows, per-layer histogram and node-sum reductions) without NCCL.
+    Returns every shard's Forest (identical trees)."""
+    cfg = config or FitConfig()
+    G = len(shards)
+    lib = _lib.lib()
+    prep = []
+    for X, y, w in shards:
+        Xa, xdt = _as_features(X)
+        y01 = np.ascontiguousarray(np.asarray(y) > 0, dtype=np.int8)
+        wa = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
+        prep.append((Xa, xdt, y01, wa))
+    # the reference prior over the concatenated class blocks (boosting.py:76-83)
+    f0 = math.nan
+    if prep[0][3] is not None:
+        ws = np.concatenate([p[3][p[2] > 0] for p in prep])
+        wb = np.concatenate([p[3][p[2] <= 0] for p in prep])
+        s_sig, s_bkg = float(np.sum(ws)), float(np.sum(wb))
+        f0 = 0.0 if (s_sig <= 0.0 or s_bkg <= 0.0) else 0.5 * math.log(s_sig / s_bkg)
+    grp = C.c_void_p()
+    _lib.check(lib.bb_vgroup_create(G, C.byref(grp)))
+    ctxs = []
+    try:
+        for g in range(G):
+            h = C.c_void_p()
+            _lib.check(lib.bb_ctx_create(device, C.byref(h)))
+            ctxs.append(h)
+            _lib.check(lib.bb_ctx_init_virtual(h, g, grp))
+        out = [None] * G
+        err = [None] * G
+
+        def run(g):
+            Xa, xdt, y01, wa = prep[g]
+            try:
+                out[g] = _fit_native(Xa, xdt, False, Xa.shape[0], Xa.shape[1], y01, False, wa, False, cfg,
+                                     return_leaves=return_leaves, device=device, ctx=ctxs[g], f0_override=f0)
+            except Exception as e:  # noqa: BLE001 - re-raised below
+                err[g] = e
+
+        th = [threading.Thread(target=run, args=(g,)) for g in range(G)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for e in err:
+            if e is not None:
+                raise e
+        return out
+    finally:
+        for h in ctxs:
+            lib.bb_ctx_destroy(h)
+        lib.bb_vgroup_destroy(grp)

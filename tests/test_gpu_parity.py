@@ -722,3 +722,43 @@ def test_elimination_refit_equals_direct_fit():
 
     ref_auc = roc_auc(predict_batch(direct, X[:1000][:, cols]), y[:1000], w[:1000])
     assert abs(auc - ref_auc) <= 1e-12
+
+
+# ------------------------------------------------------------ virtual shards
+@pytest.mark.parametrize("G,weighted,name,n,D", [(2, False, "cfg1", 40_000, 3), (4, True, "cfg2", 60_000, 4),
+                                                 (8, True, "cfg3", 90_000, 5), (3, False, "cfg5", 30_000, 6)])
+def test_virtual_shards_match_single(G, weighted, name, n, D):
+    """SURVEY.md §4's G-shard harness: the row-sharded library path with G
+    shard contexts on one GPU (in-process rank-order sums instead of NCCL)
+    gives the single-device forest bit-for-bit: global binning from the
+    exchanged radix histograms, class-count offsets, the global subsample
+    mask sliced per shard (k_mask_slice), the layer histograms and node sums
+    (sample.py:112-116, 128-132)."""
+    from paper_1609_06119_b200.distributed import fit_forest_virtual_shards
+    from paper_1609_06119_b200.sharding import shard_rows
+
+    X, y, w, kw = make_config(name, n=n)
+    if not weighted:
+        w = None
+    cfg = FitConfig(n_trees=5, depth=D, shrinkage=0.1, subsample=0.5, binning_levels=kw["binning_levels"], seed=7)
+    ref = fit_forest(X, y, w, cfg, return_leaves=True)
+    parts = [shard_rows(y, g, G) for g in range(G)]
+    got = fit_forest_virtual_shards([(X[i], y[i], None if w is None else w[i]) for i in parts], cfg,
+                                    return_leaves=True)
+    for f in got:
+        assert f.f0 == ref.f0
+        for a, b in zip(f.binnings, ref.binnings):
+            np.testing.assert_array_equal(a.boundaries, b.boundaries)
+        for ta, tb in zip(f.trees, ref.trees):
+            np.testing.assert_array_equal(ta.valid, tb.valid)
+            np.testing.assert_array_equal(ta.feature, tb.feature)
+            np.testing.assert_array_equal(ta.cut_bin, tb.cut_bin)
+            np.testing.assert_array_equal(ta.node_weight, tb.node_weight)
+    # per-shard leaves (class-block order of the shard) = the single fit's
+    # leaves of those rows: signal shards then background shards
+    n_sig = int((y > 0).sum())
+    lv = ref.fit_info["leaves"]
+    sig_parts = [got[g].fit_info["leaves"][:, :int((y[parts[g]] > 0).sum())] for g in range(G)]
+    bkg_parts = [got[g].fit_info["leaves"][:, int((y[parts[g]] > 0).sum()):] for g in range(G)]
+    np.testing.assert_array_equal(np.concatenate(sig_parts, axis=1), lv[:, :n_sig])
+    np.testing.assert_array_equal(np.concatenate(bkg_parts, axis=1), lv[:, n_sig:])

@@ -31,8 +31,11 @@ bins); the metric is fit rows*trees/s.
   forest of seed 1 over 256-bin equal-frequency boundaries of all rows) with
   its own e2e and a host-cores CPU baseline.
 
-Multi-GPU (N > 1): every rank runs an independent full fit (replicas, weak
-scaling).
+Multi-GPU (N > 1): one row-sharded fit of the whole workload (strong
+scaling): rank g holds its class-block shard of the rows (sharding.py), the
+library exchanges binning histograms, class counts, layer histograms and
+node sums over NCCL; value = all rows x trees / the
+max over ranks of the fit time.  The apply leg runs one replica per rank.
 """
 
 from __future__ import annotations
@@ -164,7 +167,7 @@ def workload_config(name, spec, n, d, world):
     """The `config` dict both arms print (identical keys and values)."""
     return {"workload": f"{name} fit", "rows": n, "features": d, "trees": spec["trees"], "depth": spec["depth"],
             "bins": 1 << spec["binning_levels"], "subsample": spec["subsample"], "shrinkage": spec["shrinkage"],
-            "parallelism": "single" if world == 1 else f"replicas{world}",
+            "parallelism": "single" if world == 1 else f"rows{world}",
             "l2": "inputs exceed L2; 256 MiB L2 flush between device steps"}
 
 
@@ -227,7 +230,8 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": "fit rows*trees/s", "value": value, "unit": "rows*trees/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * statistics.mean(secs), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * statistics.mean(secs), "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args.config, spec, n, d, world),
         "cpu_baseline": {"value": value, "unit": "rows*trees/s", "cores": 1, "kind": "port", "sample": sample,
@@ -337,10 +341,21 @@ def run_b200(args, rank, world, local):
     spec = dict(CONFIGS[args.config])
     cfg = fit_config(spec)
     X, y, w, _ = make_config(args.config)
-    n, d = X.shape
+    n, d = X.shape  # the workload's (global) rows
     T = spec["trees"]
+    ctx, f0 = None, float("nan")
+    if world > 1:
+        # row-sharded fit: this rank's class-block shard
+        from paper_1609_06119_b200.distributed import comm_context, sharded_prior
+        from paper_1609_06119_b200.sharding import shard_rows
+
+        rows = shard_rows(y, rank, world)
+        X, y, w = np.ascontiguousarray(X[rows]), y[rows], (None if w is None else w[rows])
+        ctx = comm_context(local)
+        f0 = sharded_prior(w, (y > 0).astype(np.int8))
+    n_loc = X.shape[0]
     Xd = torch.from_numpy(X).cuda()
-    yd = torch.from_numpy(y.astype(np.int8)).cuda()
+    yd = torch.from_numpy((y > 0).astype(np.int8)).cuda()
     wd = torch.from_numpy(w).cuda() if w is not None else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -351,8 +366,17 @@ def run_b200(args, rank, world, local):
             torch.cuda.synchronize()
 
     def device_fit(profile):
-        return fit_forest_device(Xd.data_ptr(), "float32", n, d, yd.data_ptr(),
-                                 None if wd is None else wd.data_ptr(), cfg, profile=profile, device=local)
+        if ctx is None:
+            return fit_forest_device(Xd.data_ptr(), "float32", n_loc, d, yd.data_ptr(),
+                                     None if wd is None else wd.data_ptr(), cfg, profile=profile, device=local)
+        import ctypes as C
+
+        from paper_1609_06119_b200 import _lib
+        from paper_1609_06119_b200.engine import _fit_native
+
+        return _fit_native(C.c_void_p(Xd.data_ptr()), _lib.BB_F32, True, n_loc, d, C.c_void_p(yd.data_ptr()), True,
+                           None if wd is None else C.c_void_p(wd.data_ptr()), True, cfg, profile=profile,
+                           device=local, ctx=ctx, f0_override=f0)
 
     for _ in range(args.warmup):
         device_fit(False)
@@ -377,10 +401,10 @@ def run_b200(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = world * n * T / (ms_per_step / 1e3)
+    value = n * T / (ms_per_step / 1e3)  # all rows of the workload (sharded across ranks)
 
     # roofline of the layer-histogram kernel
-    n_active = int(cfg.subsample * int((y > 0).sum())) + int(cfg.subsample * int((y <= 0).sum()))
+    n_active = int(cfg.subsample * int((y > 0).sum())) + int(cfg.subsample * int((y <= 0).sum()))  # this rank's
     per_launch_bytes = hist_algorithmic_bytes(n_active, d, spec["binning_levels"], spec["depth"]) / spec["depth"]
     avg_launch_ms = hist_ms / max(1, hist_launches)
     achieved = per_launch_bytes / (avg_launch_ms / 1e3) / 1e9 if avg_launch_ms > 0 else None
@@ -392,14 +416,22 @@ def run_b200(args, rank, world, local):
     # e2e through the public API from pageable numpy arrays (host wall clock)
     e2e = None
     if not args.no_e2e:
-        fit_forest(X, y, w, cfg)  # warm
+        if world > 1:
+            from paper_1609_06119_b200.distributed import fit_forest_sharded
+
+            def api_fit():
+                return fit_forest_sharded(X, y, w, cfg, device=local)
+        else:
+            def api_fit():
+                return fit_forest(X, y, w, cfg)
+        api_fit()  # warm
         barrier()
         e2e_s = []
         for _ in range(args.steps):
             flush.fill_(1)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            f = fit_forest(X, y, w, cfg)
+            api_fit()
             e2e_s.append(time.perf_counter() - t0)
         barrier()
         tot = sum(e2e_s)
@@ -409,10 +441,11 @@ def run_b200(args, rank, world, local):
             tot = float(t.item())
         I, N = (1 << spec["depth"]) - 1, (1 << (spec["depth"] + 1)) - 1
         d2h = T * I * (4 + 4 + 1 + 8 + 8) + T * N * 16 + d * ((1 << spec["binning_levels"]) - 1) * 8
-        e2e = {"value": world * n * T / (tot / args.steps), "unit": "rows*trees/s",
+        e2e = {"value": n * T / (tot / args.steps), "unit": "rows*trees/s",
                "h2d_bytes_per_step": int(X.nbytes + y.nbytes + (0 if w is None else w.nbytes)),
                "d2h_bytes_per_step": int(d2h),
-               "timing": "host wall clock around engine.fit_forest (pageable numpy inputs)"}
+               "timing": "host wall clock around engine.fit_forest (pageable numpy inputs)" if world == 1 else
+                         "host wall clock around distributed.fit_forest_sharded per rank (pageable), max over ranks"}
 
     apply = None if args.no_apply else run_apply(args, rank, world, local, torch, dist)
 
@@ -426,8 +459,8 @@ def run_b200(args, rank, world, local):
         line = {
             "metric": "fit rows*trees/s", "value": value, "unit": "rows*trees/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
-            "config": workload_config(args.config, spec, n, d, world),
+            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "int64+f64",
+            "data": "synthetic", "config": workload_config(args.config, spec, n, d, world),
             "roofline": {"bound": "hbm", "kernel": hist_kernel, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": None,

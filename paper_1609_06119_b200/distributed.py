@@ -46,23 +46,124 @@ def _dist():
     return dist
 
 
+def _pw_leaves(off: int, n: int, out: list) -> None:
+    """numpy's pairwise-sum recursion (PW_BLOCKSIZE 128, 8-way unroll): the
+    (offset, length) leaves in recursion order (bb_capi.cu pw_leaves)."""
+    if n <= 128:
+        out.append((off, n))
+        return
+    n2 = n // 2
+    n2 -= n2 % 8
+    _pw_leaves(off, n2, out)
+    _pw_leaves(off + n2, n - n2, out)
+
+
+def _leaf_sums(a: np.ndarray, leaves) -> np.ndarray:
+    """numpy's sum of each <= 128-element leaf (8 accumulators, then the
+    remainder in order), vectorised over leaves of equal length."""
+    out = np.empty(len(leaves))
+    by_len: dict = {}
+    for k, (o, n) in enumerate(leaves):
+        by_len.setdefault(n, []).append((k, o))
+    for n, items in by_len.items():
+        ks = np.array([k for k, _ in items])
+        offs = np.array([o for _, o in items])
+        blk = a[offs[:, None] + np.arange(n)[None, :]]
+        if n < 8:
+            res = np.zeros(len(items))
+            for i in range(n):
+                res = res + blk[:, i]
+        else:
+            r = blk[:, :8].copy()
+            m = n - n % 8
+            for i in range(8, m, 8):
+                r += blk[:, i:i + 8]
+            res = ((r[:, 0] + r[:, 1]) + (r[:, 2] + r[:, 3])) + ((r[:, 4] + r[:, 5]) + (r[:, 6] + r[:, 7]))
+            for i in range(m, n):
+                res = res + blk[:, i]
+        out[ks] = res
+    return out
+
+
+def _pw_combine(n: int, leaf: np.ndarray, k: list) -> float:
+    if n <= 128:
+        v = float(leaf[k[0]])
+        k[0] += 1
+        return v
+    n2 = n // 2
+    n2 -= n2 % 8
+    a = _pw_combine(n2, leaf, k)
+    b = _pw_combine(n - n2, leaf, k)
+    return a + b
+
+
+def _global_pairwise(dist, group, a_local: np.ndarray) -> float:
+    """np.sum (pairwise) of the concatenation of every rank's ``a_local`` in
+    rank order, bit-exact, exchanging only each rank's <= 128-element head and
+    tail and its sums of the recursion leaves that lie inside it (not the
+    vectors: ~1/128 of the data)."""
+    W = dist.get_world_size(group)
+    info = [None] * W
+    head, tail = a_local[:128].copy(), a_local[-128:].copy() if a_local.size else a_local[:0].copy()
+    dist.all_gather_object(info, (int(a_local.size), head, tail), group=group)
+    sizes = [x[0] for x in info]
+    starts = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    n = int(starts[-1])
+    if n == 0:
+        return 0.0
+    leaves = []
+    _pw_leaves(0, n, leaves)
+    me = dist.get_rank(group)
+    s0, s1 = int(starts[me]), int(starts[me + 1])
+    inside = [k for k, (o, m) in enumerate(leaves) if o >= s0 and o + m <= s1]
+    mine = _leaf_sums(a_local, [(leaves[k][0] - s0, leaves[k][1]) for k in inside]) if inside else np.empty(0)
+    parts = [None] * W
+    dist.all_gather_object(parts, (inside, mine), group=group)
+    leaf = np.full(len(leaves), np.nan)
+    for ks, vs in parts:
+        if len(ks):
+            leaf[np.asarray(ks)] = vs
+    # leaves crossing a rank boundary: every element is within 128 of a slice
+    # end, so the gathered heads / tails hold it
+    for k in np.flatnonzero(np.isnan(leaf)):
+        o, m = leaves[k]
+        vals = np.empty(m)
+        for j in range(m):
+            p = o + j
+            r = int(np.searchsorted(starts, p, side="right") - 1)
+            q = p - int(starts[r])
+            h, t = info[r][1], info[r][2]
+            vals[j] = h[q] if q < h.size else t[q - (sizes[r] - t.size)]
+        leaf[k] = _leaf_sums(vals, [(0, m)])[0]
+    return _pw_combine(n, leaf, [0])
+
+
 def sharded_prior(w_local: np.ndarray | None, y01_local: np.ndarray, group=None) -> float:
     """The reference prior over the concatenated rows (boosting.py:76-83):
     0.5*log(sum w_sig / sum w_bkg) with numpy's pairwise sums taken over the
-    GLOBAL class blocks in rank order (so the value is bit-identical to a
-    single-process fit).  NaN for unit weights: the library's exact count
-    ratio is used then."""
+    GLOBAL class blocks in rank order, bit-identical to a single-process fit.
+    NaN for unit weights: the library's exact count ratio is used then."""
     if w_local is None:
         return math.nan
     dist = _dist()
     sig = y01_local > 0
-    parts = [None] * dist.get_world_size(group)
-    dist.all_gather_object(parts, (np.asarray(w_local[sig]), np.asarray(w_local[~sig])), group=group)
-    w_sig = float(np.sum(np.concatenate([p[0] for p in parts])))
-    w_bkg = float(np.sum(np.concatenate([p[1] for p in parts])))
+    w_sig = _global_pairwise(dist, group, np.ascontiguousarray(w_local[sig], dtype=np.float64))
+    w_bkg = _global_pairwise(dist, group, np.ascontiguousarray(w_local[~sig], dtype=np.float64))
     if w_sig <= 0.0 or w_bkg <= 0.0:
         return 0.0
     return 0.5 * math.log(w_sig / w_bkg)
+
+
+def _agree(dist, group, err: str | None) -> None:
+    """Every rank validates its own rows, then all ranks learn whether any
+    failed before the first collective of the fit, so a bad shard raises on
+    every rank instead of leaving the others blocked in a collective."""
+    flags = [None] * dist.get_world_size(group)
+    dist.all_gather_object(flags, err, group=group)
+    bad = [(r, e) for r, e in enumerate(flags) if e is not None]
+    if bad:
+        r, e = bad[0]
+        raise ValueError(e if r == dist.get_rank(group) else f"rank {r} rejected its rows: {e}")
 
 
 def _unique_id(dist, group) -> bytes:
@@ -111,21 +212,29 @@ def fit_forest_sharded(X, y, weights=None, config: FitConfig | None = None, *, g
 
         device = torch.cuda.current_device()
     cfg = config or FitConfig()
+    err = None
     X, xdt = _as_features(X)
-    if X.ndim != 2:
-        raise ValueError("X must be 2-d (n_events, n_features)")
-    n, d = X.shape
-    y = np.asarray(y)
-    if y.shape != (n,):
-        raise ValueError(f"y has shape {y.shape}, expected ({n},)")
-    y01 = np.ascontiguousarray(y > 0, dtype=np.int8)
-    w = None
-    if weights is not None:
-        w = np.ascontiguousarray(weights, dtype=np.float64)
-        if w.shape != (n,):
-            raise ValueError(f"weights has shape {w.shape}, expected ({n},)")
-        if not np.all(np.isfinite(w)):
-            raise ValueError("user weights must be finite")
+    n = d = 0
+    y01 = w = None
+    try:
+        if X.ndim != 2:
+            raise ValueError("X must be 2-d (n_events, n_features)")
+        n, d = X.shape
+        if n < 1:
+            raise ValueError("every rank needs at least one row")
+        y = np.asarray(y)
+        if y.shape != (n,):
+            raise ValueError(f"y has shape {y.shape}, expected ({n},)")
+        y01 = np.ascontiguousarray(y > 0, dtype=np.int8)
+        if weights is not None:
+            w = np.ascontiguousarray(weights, dtype=np.float64)
+            if w.shape != (n,):
+                raise ValueError(f"weights has shape {w.shape}, expected ({n},)")
+            if not np.all(np.isfinite(w)):
+                raise ValueError("user weights must be finite")
+    except ValueError as e:
+        err = str(e)
+    _agree(dist, group, err)
     f0 = sharded_prior(w, y01, group)
     ctx = comm_context(device, group)
     return _fit_native(X, xdt, False, n, d, y01, False, w, False, cfg, return_leaves=return_leaves,

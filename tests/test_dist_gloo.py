@@ -123,3 +123,56 @@ def test_sharded_prior_and_unique_id_broadcast():
         assert p.exitcode == 0
     assert got[0][0] == want and got[1][0] == want
     assert len(got[0][1]) == 128 and got[0][1] == got[1][1]
+
+
+def _pairwise_worker(rank, world, port, sizes, out_q):
+    from paper_1609_06119_b200.distributed import _agree, _global_pairwise
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = []
+    for k, sz in enumerate(sizes):
+        rng = np.random.default_rng(100 + k)
+        full = rng.normal(size=sum(sz)) * 10.0 ** rng.integers(-3, 4, sum(sz))
+        s0 = sum(sz[:rank])
+        res.append(_global_pairwise(dist, None, full[s0:s0 + sz[rank]]))
+    # a bad shard raises on EVERY rank (no rank left waiting in a collective)
+    err = None
+    try:
+        _agree(dist, None, "weights shape (3,) does not match labels shape (4,)" if rank == 1 else None)
+    except ValueError as e:
+        err = str(e)
+    out_q.put((rank, res, err))
+    dist.destroy_process_group()
+
+
+def test_global_pairwise_sum_and_rank_agreement():
+    """The sharded prior's exchange: numpy's pairwise sum of the rank-ordered
+    concatenation from per-rank leaf sums plus the <= 128-element heads and
+    tails (leaves crossing shard boundaries, shards shorter than a leaf),
+    bit-identical to np.sum; and argument errors agreed across ranks."""
+    world = 3
+    sizes = [(1000, 1000, 1000), (5, 300, 2), (127, 129, 1), (0, 4000, 77), (128, 128, 128), (3, 0, 0)]
+    want = []
+    for k, sz in enumerate(sizes):
+        rng = np.random.default_rng(100 + k)
+        full = rng.normal(size=sum(sz)) * 10.0 ** rng.integers(-3, 4, sum(sz))
+        want.append(float(np.sum(full)))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_pairwise_worker, args=(r, world, port, sizes, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(world):
+        r, res, err = q.get(timeout=180)
+        got[r] = (res, err)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert got[r][0] == want, r
+        assert got[r][1] is not None and "does not match" in got[r][1]

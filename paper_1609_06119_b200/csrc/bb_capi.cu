@@ -310,7 +310,10 @@ static HistPlan plan_layer(int layer, const FitShape& s, int sm_count, bool sib_
     p.ngs -= 1;
     p.n_ng = (int)ceil_div(built, p.ngs);
   }
-  if (need(p.fg) > kSmemMax) throw InvalidArg{"histogram stage does not fit in shared memory"};
+  if (need(p.fg) > kSmemMax) {
+    if (s.B <= 2048) throw InvalidArg{"histogram stage does not fit in shared memory"};
+    p.global_only = 1;  // binning_levels 12..15: the global-atomic kernel
+  }
   p.tile = tile;
   p.smem = (int)need(p.fg);
   p.tiles_sig0 = 0;
@@ -556,7 +559,7 @@ static void launch_layer_hist(const HistPlan& p, const FlPlan& fl, int sm_count,
       k_layer_hist_fl<CodeT, NodeT><<<fl_grid(fl), kFlThreads, fl.smem, st>>>(code_off, node, q, n, n_sig, d, B, fl,
                                                                              hist);
     }
-  } else if (path == 4 || (path == 0 && p.n_fg * p.n_ng > hist_global_groups())) {
+  } else if (path == 4 || p.global_only || (path == 0 && p.n_fg * p.n_ng > hist_global_groups())) {
     k_layer_hist_g<CodeT, NodeT><<<8 * sm_count, 256, 0, st>>>(codes, code_off, node, q, n, n_sig, d, B, p, hist);
   } else if (path == 2 || (path != 3 && hist_warp_mode())) {
     k_layer_hist_w<CodeT, NodeT><<<hist_grid(p), kHistWThreads, p.smem, st>>>(codes, code_off, node, q, n, n_sig, d, B,
@@ -1580,8 +1583,9 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
     if (n % kTile)
       BB_CUDA(cudaMemsetAsync(codes + (size_t)(ceil_div(n, kTile) - 1) * d * kTile, 0, (size_t)d * kTile * sizeof(CodeT),
                               st));
+    BB_CUDA(cudaFuncSetAttribute(k_codes<K, CodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     k_codes<K, CodeT><<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256 * 4), 4 * c.sm_count / d + 1)), d),
-                        256, (size_t)nt * sizeof(K), st>>>(keys, n, nt, bkeys, pos, codes, stride, off, d, 1);
+                        256, codes_smem<K>(nt), st>>>(keys, n, nt, bkeys, pos, codes, stride, off, d, 1);
     BB_LAUNCH_CHECK();
   };
   auto after_codes = [&]() {
@@ -1831,13 +1835,15 @@ static ElimSession* elim_prepare(Ctx& c, const T* X, int64_t n, int d, const int
     if (s.code_bytes == 1) {
       if (rows % kTile)
         BB_CUDA(cudaMemsetAsync((uint8_t*)out + (size_t)(ceil_div(rows, kTile) - 1) * d * kTile, 0, (size_t)d * kTile, st));
-      k_codes<K, uint8_t><<<g, 256, (size_t)nt * sizeof(K), st>>>(kk, rows, nt, bkeys, pp, (uint8_t*)out, str,
+      BB_CUDA(cudaFuncSetAttribute(k_codes<K, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      k_codes<K, uint8_t><<<g, 256, codes_smem<K>(nt), st>>>(kk, rows, nt, bkeys, pp, (uint8_t*)out, str,
                                                                   s.code_off, d, 1);
     } else {
       if (rows % kTile)
         BB_CUDA(cudaMemsetAsync((uint16_t*)out + (size_t)(ceil_div(rows, kTile) - 1) * d * kTile, 0,
                                 (size_t)d * kTile * 2, st));
-      k_codes<K, uint16_t><<<g, 256, (size_t)nt * sizeof(K), st>>>(kk, rows, nt, bkeys, pp, (uint16_t*)out, str,
+      BB_CUDA(cudaFuncSetAttribute(k_codes<K, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      k_codes<K, uint16_t><<<g, 256, codes_smem<K>(nt), st>>>(kk, rows, nt, bkeys, pp, (uint16_t*)out, str,
                                                                    s.code_off, d, 1);
     }
     BB_LAUNCH_CHECK();
@@ -2072,8 +2078,8 @@ int bb_fit(bb_ctx* ctx, const void* X, int32_t x_dtype, int32_t x_on_device, int
     if (n >= (int64_t)1 << 31) throw InvalidArg{"at most 2^31-1 rows per device"};
     if (cfg->n_trees < 1) throw InvalidArg{"n_trees must be >= 1"};
     if (cfg->depth < 1 || cfg->depth > 15) throw InvalidArg{"depth must be in [1, 15]"};
-    if (cfg->binning_levels < 1 || cfg->binning_levels > 11)
-      throw InvalidArg{"binning_levels must be in [1, 11] on the GPU path"};
+    if (cfg->binning_levels < 1 || cfg->binning_levels > 15)
+      throw InvalidArg{"binning_levels must be in [1, 15] on the GPU path (uint16 codes)"};
     if (!(cfg->shrinkage > 0.0 && cfg->shrinkage <= 1.0)) throw InvalidArg{"shrinkage must be in (0, 1]"};
     if (!(cfg->subsample > 0.0 && cfg->subsample <= 1.0)) throw InvalidArg{"subsample must be in (0, 1]"};
     const int64_t hist_bytes = (int64_t)2 * (1 << (cfg->depth - 1)) * d * (1 << cfg->binning_levels) * 8;
@@ -2250,7 +2256,7 @@ int bb_bin(bb_ctx* ctx, const void* X, int32_t x_dtype, int64_t n, int32_t d, in
            int16_t* out_codes) {
   return guarded([&] {
     if (!ctx) throw InvalidArg{"null argument"};
-    if (levels < 1 || levels > 11) throw InvalidArg{"levels must be in [1, 11]"};
+    if (levels < 1 || levels > 15) throw InvalidArg{"levels must be in [1, 15]"};
     std::lock_guard<std::mutex> lock(ctx->c.mu);
     Ctx& c = ctx->c;
     BB_CUDA(cudaSetDevice(c.device));
@@ -2274,7 +2280,8 @@ int bb_bin(bb_ctx* ctx, const void* X, int32_t x_dtype, int64_t n, int32_t d, in
         k_iota<<<grid_for(n, 256, c.sm_count), 256, 0, st>>>(pos, n);
         BB_LAUNCH_CHECK();
         uint16_t* codes = A.alloc<uint16_t>((size_t)d * n);
-        k_codes<K, uint16_t><<<dim3((unsigned)std::max<int64_t>(1, ceil_div(n, 1024)), d), 256, (size_t)nt * sizeof(K),
+        BB_CUDA(cudaFuncSetAttribute(k_codes<K, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        k_codes<K, uint16_t><<<dim3((unsigned)std::max<int64_t>(1, ceil_div(n, 1024)), d), 256, codes_smem<K>(nt),
                                st>>>(keys, n, nt, bkeys, pos, codes, n, 0, d, 0);
         BB_LAUNCH_CHECK();
         BB_CUDA(cudaMemcpyAsync(out_codes, codes, (size_t)d * n * 2, cudaMemcpyDeviceToHost, st));
@@ -2291,7 +2298,7 @@ int bb_layer_hist(bb_ctx* ctx, const uint16_t* codes, const uint16_t* node, cons
                   int32_t d, int32_t levels, int32_t layer, int64_t* out_hist) {
   return guarded([&] {
     if (!ctx) throw InvalidArg{"null argument"};
-    if (layer < 1 || layer > 15 || levels < 1 || levels > 11) throw InvalidArg{"bad layer/levels"};
+    if (layer < 1 || layer > 15 || levels < 1 || levels > 15) throw InvalidArg{"bad layer/levels"};
     std::lock_guard<std::mutex> lock(ctx->c.mu);
     Ctx& c = ctx->c;
     BB_CUDA(cudaSetDevice(c.device));
@@ -2416,7 +2423,7 @@ int bb_split(bb_ctx* ctx, const int64_t* hist, int32_t d, int32_t levels, int32_
              double* out_gain, double* out_threshold) {
   return guarded([&] {
     if (!ctx) throw InvalidArg{"null argument"};
-    if (layer < 1 || layer > 15 || levels < 1 || levels > 11) throw InvalidArg{"bad layer/levels"};
+    if (layer < 1 || layer > 15 || levels < 1 || levels > 15) throw InvalidArg{"bad layer/levels"};
     std::lock_guard<std::mutex> lock(ctx->c.mu);
     Ctx& c = ctx->c;
     BB_CUDA(cudaSetDevice(c.device));
@@ -2534,7 +2541,7 @@ int bb_elim_create(bb_ctx* ctx, const void* X, int32_t x_dtype, int64_t n, int32
     if (!ctx || !X || !y01 || !out) throw InvalidArg{"null argument"};
     if (n < 2 || d < 1) throw InvalidArg{"need at least 2 rows and 1 feature"};
     if (n >= (int64_t)1 << 31 || n_val >= (int64_t)1 << 31) throw InvalidArg{"at most 2^31-1 rows per device"};
-    if (levels < 1 || levels > 11) throw InvalidArg{"binning_levels must be in [1, 11] on the GPU path"};
+    if (levels < 1 || levels > 15) throw InvalidArg{"binning_levels must be in [1, 15] on the GPU path (uint16 codes)"};
     if (n_val > 0 && (!Xv || !y01_val)) throw InvalidArg{"null validation argument"};
     std::lock_guard<std::mutex> lock(ctx->c.mu);
     BB_CUDA(cudaSetDevice(ctx->c.device));

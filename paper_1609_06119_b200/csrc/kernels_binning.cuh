@@ -407,17 +407,29 @@ __global__ void k_class_positions(const int8_t* __restrict__ y, int64_t n, const
 // codes[code_index(pos[i], f)] = stored code; stored = code - code_off
 // (code_off = 1 only for NaN-free data at B = 256 with u8 storage).
 // tiled = 0 writes plain column-major [f][code_stride] (bb_bin parity entry).
+constexpr int64_t kCodesSmemMax = 200 * 1024;
+template <typename K>
+__host__ inline size_t codes_smem(int nt) {
+  const int64_t b = (int64_t)nt * (int64_t)sizeof(K);
+  return b <= kCodesSmemMax ? (size_t)b : 0;
+}
+
 template <typename K, typename CodeT>
 __global__ void __launch_bounds__(256) k_codes(const K* __restrict__ keys, int64_t n, int nt,
                                                const K* __restrict__ bkeys, const int* __restrict__ pos,
                                                CodeT* __restrict__ codes, int64_t code_stride, int code_off,
                                                int d, int tiled) {
   extern __shared__ unsigned char s_raw[];
-  K* sb = reinterpret_cast<K*>(s_raw);
   const int f = blockIdx.y;
   const K* bk = bkeys + (int64_t)f * nt;
-  for (int t = threadIdx.x; t < nt; t += blockDim.x) sb[t] = bk[t];
-  __syncthreads();
+  // boundary keys in shared memory, or (binning_levels 15 with f64 keys:
+  // 256 KB) searched in global memory through the cache
+  const bool in_smem = (int64_t)nt * (int64_t)sizeof(K) <= kCodesSmemMax;
+  K* sb = in_smem ? reinterpret_cast<K*>(s_raw) : const_cast<K*>(bk);
+  if (in_smem) {
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) sb[t] = bk[t];
+    __syncthreads();
+  }
   const K* col = keys + (int64_t)f * n;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const K k = col[i];

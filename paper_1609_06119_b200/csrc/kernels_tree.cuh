@@ -171,6 +171,7 @@ struct HistPlan {
   int smem;                  // dynamic shared memory bytes
   int prof;                  // debug (BB_HIST_PROFILE=1): thread 0's per-phase cycles into g_hist_prof
   int sib;                   // 1: build left children only (right = parent - left in k_split)
+  int global_only;           // bins too wide for any shared-memory plan (levels 12..15)
 };
 
 __device__ unsigned long long g_hist_prof[8];
@@ -642,7 +643,105 @@ __global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restric
   const bool right = sib && (node & 1);
   const int pnode = node >> 1, pnodes = nodes >> 1;
   const bool pvalid = right && ta.valid[(int64_t)tree * n_internal + ((start - 1) >> 1) + pnode] != 0;
-  for (int f = fbeg; f < fend; ++f) {
+  if (per > 8) {
+    // wide bins (B > 8 * THREADS, binning_levels 12..15): two passes per
+    // feature, node totals first, then chunks of 8 * THREADS codes with the
+    // CPH prefix carried across chunks (same gains, same first-max order)
+    constexpr int CH = 8 * THREADS;
+    __shared__ long long s_red[2][THREADS / 32];
+    for (int f = fbeg; f < fend; ++f) {
+      long long* hs = hist + ((int64_t)node * d + f) * B;
+      long long* hb = hist + (((int64_t)nodes + node) * d + f) * B;
+      long long* ls = right ? hist + ((int64_t)(node - 1) * d + f) * B : nullptr;
+      long long* lb = right ? hist + (((int64_t)nodes + node - 1) * d + f) * B : nullptr;
+      long long* ps = right ? par + ((int64_t)pnode * d + f) * B : nullptr;
+      long long* pb = right ? par + (((int64_t)pnodes + pnode) * d + f) * B : nullptr;
+      auto val = [&](int c, long long& a, long long& b) {
+        if (right) {
+          a = pvalid ? ps[c] - ls[c] : 0;
+          b = pvalid ? pb[c] - lb[c] : 0;
+        } else {
+          a = hs[c];
+          b = hb[c];
+        }
+      };
+      long long ts = 0, tb = 0;
+      for (int c = threadIdx.x; c < B; c += THREADS) {
+        long long a, b;
+        val(c, a, b);
+        ts += a;
+        tb += b;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        ts += __shfl_xor_sync(0xffffffffu, ts, o);
+        tb += __shfl_xor_sync(0xffffffffu, tb, o);
+      }
+      if (lane == 0) { s_red[0][warp] = ts; s_red[1][warp] = tb; }
+      __syncthreads();
+      long long tot_s = 0, tot_b = 0;
+      for (int w = 0; w < THREADS / 32; ++w) { tot_s += s_red[0][w]; tot_b += s_red[1][w]; }
+      __syncthreads();
+      long long carry_s = 0, carry_b = 0;
+      for (int ch0 = 0; ch0 < B; ch0 += CH) {
+        long long vs[8], vb[8];
+        long long qs = 0, qb = 0;
+        const int c0 = ch0 + threadIdx.x * 8;
+        for (int j = 0; j < 8; ++j) {
+          const int c = c0 + j;
+          vs[j] = 0;
+          vb[j] = 0;
+          if (c < B) {
+            val(c, vs[j], vb[j]);
+            if (right) {
+              if (!final_layer) { hs[c] = vs[j]; hb[c] = vb[j]; }
+              ps[c] = 0;
+              pb[c] = 0;
+            }
+          }
+          qs += vs[j];
+          qb += vb[j];
+        }
+        long long is = qs, ib = qb;
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long us = __shfl_up_sync(0xffffffffu, is, o);
+          const long long ub = __shfl_up_sync(0xffffffffu, ib, o);
+          if (lane >= o) { is += us; ib += ub; }
+        }
+        if (lane == 31) { s_ws[warp] = is; s_wb[warp] = ib; }
+        __syncthreads();
+        long long off_s = 0, off_b = 0, ch_s = 0, ch_b = 0;
+        for (int w = 0; w < THREADS / 32; ++w) {
+          if (w < warp) { off_s += s_ws[w]; off_b += s_wb[w]; }
+          ch_s += s_ws[w];
+          ch_b += s_wb[w];
+        }
+        __syncthreads();
+        long long cs = carry_s + off_s + is - qs, cb = carry_b + off_b + ib - qb;
+        for (int j = 0; j < 8; ++j) {
+          const int c = c0 + j;
+          cs += vs[j];
+          cb += vb[j];
+          if (c >= B - 1) break;
+          const long long rs = tot_s - cs, rb = tot_b - cb;
+          double g = -INFINITY;
+          if (cs + cb > 0 && rs + rb > 0)
+            g = __dsub_rn(__dadd_rn(g_term(cs, cb, scale), g_term(rs, rb, scale)), g_term(tot_s, tot_b, scale));
+          const int flat = f * (B - 1) + c;
+          if (better(g, flat, best_g, best_flat)) { best_g = g; best_flat = flat; }
+          if (fc >= 0 && (fc >> 16) == f && (fc & 0xffff) == c + 1) sc.forced_gain[node] = g;
+        }
+        if (!sib && !keep) {
+          for (int j = 0; j < 8; ++j) {
+            const int c = c0 + j;
+            if (c < B) { hs[c] = 0; hb[c] = 0; }
+          }
+        }
+        carry_s += ch_s;
+        carry_b += ch_b;
+      }
+    }
+  }
+  for (int f = fbeg; f < fend && per <= 8; ++f) {
     long long* hs = hist + ((int64_t)node * d + f) * B;
     long long* hb = hist + (((int64_t)nodes + node) * d + f) * B;
     long long vs[8], vb[8];

@@ -762,3 +762,43 @@ def test_virtual_shards_match_single(G, weighted, name, n, D):
     bkg_parts = [got[g].fit_info["leaves"][:, int((y[parts[g]] > 0).sum()):] for g in range(G)]
     np.testing.assert_array_equal(np.concatenate(sig_parts, axis=1), lv[:, :n_sig])
     np.testing.assert_array_equal(np.concatenate(bkg_parts, axis=1), lv[:, n_sig:])
+
+
+# ------------------------------------------------------------ wide bins (levels 12..15)
+@pytest.mark.parametrize("levels", [12, 13, 15])
+def test_binning_wide_levels_vs_oracle(levels):
+    """binning_levels 12..15 (uint16 codes, sample.py:22-24): boundaries and
+    codes bit-exact, f32 and f64 keys (levels 15 with f64 keys searches the
+    boundary keys in global memory)."""
+    rng = np.random.default_rng(levels)
+    X = rng.standard_t(3, size=(120_000, 3))
+    X[rng.random(X.shape) < 0.02] = np.nan
+    X[:, 2] = np.round(X[:, 2] * 3)  # ties
+    for arr in (X.astype(np.float32), X):
+        b, c = gpu_bin(arr, levels)
+        for j in range(X.shape[1]):
+            ref_b = oracle.fit_boundaries(arr[:, j], levels)
+            np.testing.assert_array_equal(b[j], ref_b)
+            np.testing.assert_array_equal(c[j].astype(np.uint16), oracle.bin_codes(ref_b, arr[:, j]).astype(np.uint16))
+
+
+@pytest.mark.parametrize("levels,nan", [(12, False), (15, True)])
+def test_fit_wide_levels_vs_fixed_point_oracle(levels, nan):
+    """Fits with 4096 / 32768 bins (global-atomic histograms, the chunked
+    CPH split) exact against the fixed-point oracle."""
+    X, y, w, _ = make_config("cfg2", n=30_000)
+    X = X[:, :4].copy()
+    if nan:
+        X[np.random.default_rng(1).random(X.shape) < 0.03] = np.nan
+    kw = dict(n_trees=4, depth=3, shrinkage=0.1, subsample=0.5, levels=levels, seed=2)
+    forest = fit_forest(X, y, w, FitConfig(n_trees=4, depth=3, shrinkage=0.1, subsample=0.5, binning_levels=levels,
+                                           seed=2), return_leaves=True)
+    ref = oracle.fit_forest(X, y, w, fixed_point=True, record_leaves=True, **kw)
+    np.testing.assert_array_equal(np.stack([b.boundaries for b in forest.binnings]), ref.boundaries)
+    for t in range(4):
+        tr = forest.trees[t]
+        np.testing.assert_array_equal(tr.valid, ref.valid[t])
+        np.testing.assert_array_equal(tr.feature, ref.feature[t])
+        np.testing.assert_array_equal(tr.cut_bin, ref.cut_bin[t])
+        np.testing.assert_array_equal(forest.fit_info["leaves"][t], ref.leaves[t].astype(np.uint16))
+        np.testing.assert_allclose(tr.node_weight, ref.node_weight[t], rtol=1e-12, atol=1e-15)

@@ -4,6 +4,8 @@ model-file interop with the reference format, sharding arithmetic."""
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -87,3 +89,26 @@ def test_class_block_shard_partition():
     assert sorted(np.concatenate(parts).tolist()) == list(range(7))
     ms, mb = np.array([1, 0, 1, 1], bool), np.array([0, 1, 1], bool)
     assert np.concatenate([slice_mask(ms, mb, r, 2) for r in range(2)]).sum() == ms.sum() + mb.sum()
+
+
+def test_gpu_written_model_loads_in_reference(golden_dir):
+    """A model file written by the GPU binding on a B200
+    (tests/golden/gpu_model.json, tools/gen_gpu_model.py) loads through the
+    reference's own model_io.load_forest (model_io.py:111-237) and the
+    reference's predict_batch reproduces the GPU predictions.  Needs the
+    reference tree (build container only)."""
+    import sys
+
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference not present")
+    sys.path.insert(0, ref)
+    try:
+        from binboost.boosting import predict_batch as ref_predict
+        from binboost.model_io import load_forest as ref_load
+    finally:
+        sys.path.remove(ref)
+    f = ref_load(os.path.join(golden_dir, "gpu_model.json"))
+    z = np.load(os.path.join(golden_dir, "gpu_model_inputs.npz"))
+    assert len(f.trees) == int(z["trees"])
+    np.testing.assert_allclose(ref_predict(f, z["X"]), z["pred"], rtol=0, atol=1e-15)

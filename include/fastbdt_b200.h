@@ -178,6 +178,23 @@ int bb_vgroup_create(int32_t world, bb_vgroup** out);
 int bb_vgroup_destroy(bb_vgroup* group);
 int bb_ctx_init_virtual(bb_ctx* ctx, int32_t rank, bb_vgroup* group);
 
+/* CSV ingestion (replaces the csv/float() loop of binboost.dataset.load_csv
+ * / load_matrix, pkg/src/binboost/dataset.py:31-137): host-side, threaded.
+ * bb_csv_open reads the file and delimits its records (excel dialect);
+ * bb_csv_parse parses the chosen columns of every data record as float64
+ * (Python float() grammar) into out[records][n_cols]; finite_col (or -1)
+ * must hold finite values.  On BB_EINVAL bb_csv_error gives the first error
+ * in record order: kind 1 = cell count, 2 = not a number, 3 = non-finite. */
+typedef struct bb_csv bb_csv;
+int bb_csv_open(const char* path, bb_csv** out);
+int32_t bb_csv_n_header(const bb_csv* h);
+int64_t bb_csv_n_records(const bb_csv* h);
+const char* bb_csv_header(const bb_csv* h, int32_t j, int64_t* len);
+int bb_csv_parse(bb_csv* h, const int32_t* cols, int32_t n_cols, int32_t finite_col, int32_t n_threads, double* out);
+int bb_csv_error(const bb_csv* h, int64_t* row, int32_t* kind, int32_t* col, int32_t* cells, const char** cell,
+                 int64_t* cell_len, double* value);
+int bb_csv_close(bb_csv* h);
+
 /* Analysis ------------------------------------------------------------ */
 
 /* Weighted ROC AUC of host scores (labels y01 > 0 = signal; w may be NULL).

@@ -103,6 +103,15 @@ _SIGS = {
     "bb_subsample_masks_gpu": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_int32,
                                          C.POINTER(FitConfigC), C.c_void_p]),
     "bb_pairwise_sum": (C.c_double, [C.c_void_p, C.c_int64]),
+    "bb_csv_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "bb_csv_n_header": (C.c_int32, [C.c_void_p]),
+    "bb_csv_n_records": (C.c_int64, [C.c_void_p]),
+    "bb_csv_header": (C.c_void_p, [C.c_void_p, C.c_int32, C.POINTER(C.c_int64)]),
+    "bb_csv_parse": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
+    "bb_csv_error": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                               C.POINTER(C.c_int32), C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
+                               C.POINTER(C.c_double)]),
+    "bb_csv_close": (C.c_int, [C.c_void_p]),
     "bb_vgroup_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
     "bb_vgroup_destroy": (C.c_int, [C.c_void_p]),
     "bb_ctx_init_virtual": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),

@@ -16,7 +16,9 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfastbdt_b200.so")
+# BB_LIB_VARIANT=check loads the device-bounds-check build (make -C csrc check)
+LIB_PATH = os.path.join(_HERE, "libfastbdt_b200_check.so" if os.environ.get("BB_LIB_VARIANT") == "check"
+                        else "libfastbdt_b200.so")
 
 BB_OK, BB_EINVAL, BB_ECUDA, BB_ESTATE = 0, 1, 2, 3
 BB_F32, BB_F64 = 0, 1

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/fastbdt_b200.h"
 #include "bb_mask.h"
@@ -35,6 +36,13 @@
 namespace bb {
 
 static thread_local std::string g_err;
+
+// NVTX ranges (header-only nvtx3: free unless a profiler attaches) around
+// the fit's phases, every tree and every layer
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 void set_error(const std::string& msg) { g_err = msg; }
 
 // numpy's pairwise float64 summation (numpy/_core/src/umath/loops_utils.h
@@ -1226,7 +1234,14 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
 
   // node-partitioned row lists + row-major codes (kernels_hist_list.cuh):
   // u8 codes, d <= 64, every built (node, class) list gets a CTA
-  const int lh_nw = s.d <= 32 ? 8 : 16;
+  // rows of 33..64 features: one 64-feature CTA per SM; BB_LH_GROUPS=1 runs
+  // two 32-feature groups of the NW = 8 kernel (two CTAs per SM) instead,
+  // measured slower at cfg3 (240 vs 180 us at layer 1: a group's 32-byte
+  // half-row reads cost a 64-byte DRAM access each)
+  static const bool lh_nw16 = !(getenv("BB_LH_GROUPS") && atoi(getenv("BB_LH_GROUPS")) != 0);
+  const int lh_nw = (s.d <= 32 || !lh_nw16) ? 8 : 16;
+  const int lh_pitch = s.d <= 32 ? 8 : 16;  // words per row of rc
+  const int lh_groups = lh_nw == 8 && s.d > 32 ? 2 : 1;
   const int lh_grid = lh_nw == 8 ? 2 * (c.sm_count - hist_reserve()) : c.sm_count - hist_reserve();
   const int hp_env = hist_path_env();
   const bool lists = sizeof(CodeT) == 1 && s.d <= 64 && s.depth <= 8 && (hp_env == 0 || hp_env == 5) &&
@@ -1236,7 +1251,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   long long* lq[2] = {nullptr, nullptr};
   int* cnt = nullptr;
   if (lists) {
-    rc = A.alloc<uint32_t>((size_t)npad * lh_nw);
+    rc = A.alloc<uint32_t>((size_t)npad * lh_pitch);
     for (int b = 0; b < 2; ++b) {
       lrow[b] = A.alloc<int>(npad);
       lq[b] = A.alloc<long long>(npad);
@@ -1248,7 +1263,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
     BB_CUDA(cudaFuncSetAttribute(k_hist_list<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lh_smem_bytes<16>()));
     BB_CUDA(cudaFuncSetAttribute(k_rowcodes<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * kTile));
     BB_CUDA(cudaFuncSetAttribute(k_rowcodes<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * kTile));
-    if (lh_nw == 8) k_rowcodes<8><<<tiles, 256, (size_t)s.d * kTile, st>>>(c8, n, s.d, rc);
+    if (lh_pitch == 8) k_rowcodes<8><<<tiles, 256, (size_t)s.d * kTile, st>>>(c8, n, s.d, rc);
     else k_rowcodes<16><<<tiles, 256, (size_t)s.d * kTile, st>>>(c8, n, s.d, rc);
     BB_LAUNCH_CHECK();
   }
@@ -1289,6 +1304,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
     const bool tl_on = getenv("BB_TIMELINE") != nullptr;  // debug: main-stream waits for masks
     std::vector<cudaEvent_t> tl;
     for (int t = 0; t < s.T; ++t) {
+      NvtxRange tree_range("tree");
       feed.ahead(t);
       const int slot = t % kSlots;
       unsigned int* mask = feed.bits(t);
@@ -1310,6 +1326,10 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
       BB_LAUNCH_CHECK();
       stats.launches += 1;
       for (int layer = 1; layer <= s.depth; ++layer) {
+        static const char* kLayerNames[] = {"layer 0", "layer 1", "layer 2", "layer 3", "layer 4", "layer 5", "layer 6",
+                                            "layer 7", "layer 8", "layer 9", "layer 10", "layer 11", "layer 12",
+                                            "layer 13", "layer 14", "layer 15"};
+        NvtxRange layer_range(kLayerNames[layer]);
         const HistPlan& p = plans[layer];
         unsigned long long* hist = hbuf[layer & 1];
         unsigned long long* par = hbuf[(layer - 1) & 1];
@@ -1318,10 +1338,12 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
           const int lb = (layer - 1) & 1;
           if (lh_nw == 8)
             k_hist_list<8><<<lh_grid, kLhThreads, lh_smem_bytes<8>(), st>>>(rc, lrow[lb], lq[lb], cnt, layer, p.sib,
-                                                                          s.n_sig, s.d, s.B, code_off, p.nodes, hist);
+                                                                          s.n_sig, s.d, s.B, code_off, p.nodes, hist,
+                                                                          lh_pitch, lh_groups);
           else
             k_hist_list<16><<<lh_grid, kLhThreads, lh_smem_bytes<16>(), st>>>(rc, lrow[lb], lq[lb], cnt, layer, p.sib,
-                                                                            s.n_sig, s.d, s.B, code_off, p.nodes, hist);
+                                                                            s.n_sig, s.d, s.B, code_off, p.nodes, hist,
+                                                                            16, 1);
           BB_LAUNCH_CHECK();
         } else {
           launch_layer_hist<CodeT, NodeT>(p, fl_plans[layer], c.sm_count, codes, code_off, node, q, n, s.n_sig, s.d,
@@ -1430,6 +1452,7 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   } evg{ev0, ev1};
   Arena A(st);
   const int levels = cfg.binning_levels, B = 1 << levels, nt = B - 1;
+  NvtxRange fit_range("bb_fit");
   // ---- upload
   auto t_up = std::chrono::steady_clock::now();
   const T* Xd = reinterpret_cast<const T*>(Xv);
@@ -1529,6 +1552,7 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
     BB_CUDA(cudaStreamSynchronize(st));  // host vectors pw_off / pw_len go out of use
   }
   // ---- binning
+  NvtxRange bin_range("binning");
   std::vector<unsigned long long> finite, nans;
   unsigned long long* finite_dev = nullptr;
   K* keys = make_keys<T>(c, A, Xd, n, d, finite, nans, &finite_dev, dist);
@@ -2311,7 +2335,9 @@ int bb_layer_hist(bb_ctx* ctx, const uint16_t* codes, const uint16_t* node, cons
       // with the fit's region rule (full layer: both children listed)
       if (B > 256 || d > 64) throw InvalidArg{"list histogram: needs B <= 256 and d <= 64"};
       const int code_off = B == 256 ? 1 : 0;
-      const int NW = d <= 32 ? 8 : 16;
+      const int NW = d <= 32 ? 8 : 16;  // row words
+      const bool nw16 = !(getenv("BB_LH_GROUPS") && atoi(getenv("BB_LH_GROUPS")) != 0);
+      const int groups = (NW == 16 && !nw16) ? 2 : 1;
       std::vector<uint32_t> rch((size_t)npad * NW, 0u);
       for (int f = 0; f < d; ++f)
         for (int64_t i = 0; i < n; ++i) {
@@ -2375,15 +2401,16 @@ int bb_layer_hist(bb_ctx* ctx, const uint16_t* codes, const uint16_t* node, cons
       const size_t hsz = (size_t)2 * nodes * d * B;
       unsigned long long* hist = A.alloc<unsigned long long>(hsz);
       BB_CUDA(cudaMemsetAsync(hist, 0, hsz * 8, st));
-      const int grid = NW == 8 ? 2 * c.sm_count : c.sm_count;
-      if (NW == 8) {
+      const bool k8 = NW == 8 || groups == 2;
+      const int grid = k8 ? 2 * c.sm_count : c.sm_count;
+      if (k8) {
         BB_CUDA(cudaFuncSetAttribute(k_hist_list<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, lh_smem_bytes<8>()));
         k_hist_list<8><<<grid, kLhThreads, lh_smem_bytes<8>(), st>>>(rcd, lrd, lqd, cd, layer, 0, n_sig, d, B, code_off,
-                                                                     nodes, hist);
+                                                                     nodes, hist, NW, groups);
       } else {
         BB_CUDA(cudaFuncSetAttribute(k_hist_list<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lh_smem_bytes<16>()));
         k_hist_list<16><<<grid, kLhThreads, lh_smem_bytes<16>(), st>>>(rcd, lrd, lqd, cd, layer, 0, n_sig, d, B,
-                                                                       code_off, nodes, hist);
+                                                                       code_off, nodes, hist, 16, 1);
       }
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaStreamSynchronize(st));

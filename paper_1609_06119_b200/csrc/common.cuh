@@ -37,6 +37,24 @@ struct InvalidArg {
   std::string msg;
 };
 
+// Device-side bounds checks of the check build (make check: -DBB_DEVICE_CHECKS,
+// libfastbdt_b200_check.so, loaded with BB_LIB_VARIANT=check); no code in
+// the release build.  A failed check prints its location and traps.
+#ifdef BB_DEVICE_CHECKS
+#define BB_DCHECK(cond)                                                                              \
+  do {                                                                                               \
+    if (!(cond)) {                                                                                   \
+      printf("BB_DCHECK failed: %s at %s:%d block %d thread %d\n", #cond, __FILE__, __LINE__,        \
+             (int)blockIdx.x, (int)threadIdx.x);                                                     \
+      __trap();                                                                                      \
+    }                                                                                                \
+  } while (0)
+#else
+#define BB_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------- keys
 // Order-preserving unsigned keys for IEEE floats.  -0.0 is canonicalised to
 // +0.0 so equal-comparing values share a key (np.sort/np.searchsorted treat

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kAucThreads) k_radix_scatter(const unsigned lo
 #pragma unroll
     for (int q = 0; q < kAucDigits; ++q)
       if (dg == q) pos = base[q]++;
+    BB_DCHECK(pos < (unsigned int)n);
     kout[pos] = kk[j];
     vout[pos] = vin[i];
   }

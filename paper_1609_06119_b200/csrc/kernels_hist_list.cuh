@@ -105,7 +105,16 @@ template <int NW>
 __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
     k_hist_list(const uint32_t* __restrict__ rc, const int* __restrict__ lrow, const long long* __restrict__ lq,
                 const int* __restrict__ cnt, int layer, int sib, long long n_sig, int d, int B, int code_off,
-                int nodes, unsigned long long* __restrict__ hist) {
+                int nodes, unsigned long long* __restrict__ hist, int pitch, int ngroups) {
+  // pitch: row words of rc; ngroups > 1 (NW = 8 over 16-word rows): CTA
+  // b takes feature group b % ngroups (features 32 g ..) of the rows it
+  // gathers, so two 64 KB-histogram CTAs fit per SM and twice the warps
+  // keep gathers in flight (same bytes: each group reads its 32-byte half)
+  const int fgrp = (int)blockIdx.x % ngroups, cta = (int)blockIdx.x / ngroups, nctas = (int)gridDim.x / ngroups;
+  const int fbase = 32 * fgrp * (NW == 8 ? 1 : 0);
+  const uint32_t* rcg = rc + (NW == 8 ? 8 * fgrp : 0);
+  const int dtot = d;
+  d = min(d - fbase, NW * 4);  // features of this group
   extern __shared__ __align__(16) unsigned char lh_sm[];
   unsigned char* hb = lh_sm;                                             // histogram limbs
   uint32_t* bufs = reinterpret_cast<uint32_t*>(lh_sm + lh_hist_bytes<NW>());  // [warp][2][32 rows][NW]
@@ -123,14 +132,14 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
       R += segs[s].y;
       E += segs[s].y > 0;
     }
-    const int G = gridDim.x, Gp = G > E ? G - E : 0;
+    const int G = nctas, Gp = G > E ? G - E : 0;
     int cum = 0, seg = -1;
     long long r0 = 0, r1 = 0;
     for (int s = 0; s < ns && seg < 0; ++s) {
       if (segs[s].y == 0) continue;
       const int k = 1 + (int)((long long)Gp * segs[s].y / (R > 0 ? R : 1));
-      if ((int)blockIdx.x < cum + k) {
-        const int j = (int)blockIdx.x - cum;
+      if (cta < cum + k) {
+        const int j = cta - cum;
         seg = s;
         r0 = (long long)segs[s].y * j / k;
         r1 = (long long)segs[s].y * (j + 1) / k;
@@ -147,6 +156,7 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
   __syncthreads();
   if (s_seg < 0) return;
   const int4 sg = segs[s_seg];
+  BB_DCHECK(sg.x >= 0 && sg.y >= 0 && sg.z >= 0 && sg.z < nodes && (sg.w == 0 || sg.w == 1));
   const int r_begin = s_r0, r_end = s_r1;
   const int* lr = lrow + sg.x;
   const long long* lqs = lq + sg.x;
@@ -184,6 +194,7 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
       if (sl < nsl && e < p1) {
         row = __ldg(lr + e);
         qq = __ldg(lqs + e);
+        BB_DCHECK(row >= 0);
       }
     };
     auto fetch = [&](int row_of_lane, uint4 (&x)[CPR]) {  // lane loads chunk (lane % CPR) of rows lane / CPR + (32 / CPR) t
@@ -191,7 +202,7 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
       for (int t = 0; t < CPR; ++t) {
         const int rr = lane / CPR + (32 / CPR) * t;
         const int srow = __shfl_sync(0xffffffffu, row_of_lane, rr);
-        x[t] = srow >= 0 ? __ldg(reinterpret_cast<const uint4*>(rc + (size_t)srow * NW) + (lane % CPR))
+        x[t] = srow >= 0 ? __ldg(reinterpret_cast<const uint4*>(rcg + (size_t)srow * pitch) + (lane % CPR))
                          : make_uint4(0u, 0u, 0u, 0u);
       }
     };
@@ -215,6 +226,7 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const uint32_t off = __byte_perm(word, g4 + cb[b], 0x5504u | ((uint32_t)b << 4));
+          BB_DCHECK(off + (NW == 16 ? 65536u : 128u) + 4u <= (uint32_t)lh_hist_bytes<NW>());
           atomicAdd(reinterpret_cast<uint32_t*>(hb + off), qlo);
           atomicAdd(reinterpret_cast<uint32_t*>(hb + off + (NW == 16 ? 65536u : 128u)), qhi);
         }
@@ -223,25 +235,29 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
     const int nj = nsl > warp ? (nsl - warp + kLhWarps - 1) / kLhWarps : 0;  // this warp's slices
     // kLhPf slices in flight in registers (register-file capacity, not shared
     // memory, bounds the bytes in flight: 16 warps x kLhPf x 32 rows x NW words)
-    int rr_;
-    long long qv[kLhPf];
-    uint4 xv[kLhPf][CPR];
+    // row ids (and q) are loaded one round before the gathers that need them
+    constexpr int PF = NW == 8 ? 3 : kLhPf;  // NW = 8 runs 2 CTAs / SM: 64 registers
+    long long qv[PF], qn[PF];
+    int rn[PF];
+    uint4 xv[PF][CPR];
 #pragma unroll
-    for (int u = 0; u < kLhPf; ++u) {
-      entry(u, rr_, qv[u]);
-      fetch(rr_, xv[u]);
+    for (int u = 0; u < PF; ++u) {
+      int r0;
+      entry(u, r0, qv[u]);
+      fetch(r0, xv[u]);
+      entry(u + PF, rn[u], qn[u]);
     }
-    for (int j = 0; j < nj; j += kLhPf) {
+    for (int j = 0; j < nj; j += PF) {
 #pragma unroll
-      for (int u = 0; u < kLhPf; ++u) {
+      for (int u = 0; u < PF; ++u) {
         if (j + u < nj) {
           store(xv[u]);
           __syncwarp();
-          long long qn;
-          entry(j + u + kLhPf, rr_, qn);
-          fetch(rr_, xv[u]);
-          accumulate(qv[u]);
-          qv[u] = qn;
+          fetch(rn[u], xv[u]);  // slice j + u + PF (ids from the previous round)
+          const long long qq = qv[u];
+          qv[u] = qn[u];
+          entry(j + u + 2 * PF, rn[u], qn[u]);
+          accumulate(qq);
           __syncwarp();
         }
       }
@@ -254,7 +270,7 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
     // layer histogram with one bulk reduction per row
     const uint32_t* lo = reinterpret_cast<const uint32_t*>(hb);
     long long* stg = reinterpret_cast<long long*>(bufs);
-    const int pitch = B + 2;
+    const int spitch = B + 2;
     // NW = 16: 2 rounds of 32 feature rows, warps take bins; NW = 8 (2 CTAs
     // per SM, half the staging): 2 rounds of 16 rows, half-warps take bins
     constexpr int RPR = NW == 16 ? 32 : 16;  // staged rows per round
@@ -272,7 +288,7 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
             if (NW == 16) val = (long long)(int)lo[16384 + v * 64 + wa] * 65536ll + (long long)lo[v * 64 + wa];
             else val = (long long)(int)lo[v * 64 + 32 + wa] * 65536ll + (long long)lo[v * 64 + wa];
           }
-          stg[(size_t)srow * pitch + bin] = val;
+          stg[(size_t)srow * spitch + bin] = val;
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -280,8 +296,8 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
       if (threadIdx.x < RPR) {
         const int ff = NW == 16 ? 4 * (threadIdx.x & 15) + 2 * (threadIdx.x >> 4) + round : threadIdx.x + 16 * round;
         if (ff < d)
-          bulk_reduce_add_u64(hist + (((size_t)sg.w * nodes + sg.z) * d + ff) * B, stg + (size_t)threadIdx.x * pitch,
-                              (unsigned)B * 8u);
+          bulk_reduce_add_u64(hist + (((size_t)sg.w * nodes + sg.z) * dtot + fbase + ff) * B,
+                              stg + (size_t)threadIdx.x * spitch, (unsigned)B * 8u);
       }
       asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
       __syncthreads();

@@ -464,8 +464,10 @@ __device__ void seg_piece(const SegArgs& ar, const RngState& r0, long long base,
           const int t = xf - ac;
           const unsigned own = __ballot_sync(FULL, incl >= t);
           const int ow = __ffs(own) - 1;
+          BB_DCHECK(ow >= 0 && ow < 32);
           if (lane == ow) {
             int tt = t - (incl - cnt);
+            BB_DCHECK(tt >= 1 && tt <= cnt);
             for (int w = w0; w < w1; ++w) {
               unsigned int m = sw[w];
               const int pc = __popc(m);

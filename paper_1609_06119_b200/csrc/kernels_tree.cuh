@@ -62,11 +62,10 @@ __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, i
                                                                 const double* __restrict__ nw_prev, double two_s,
                                                                 int* __restrict__ cnt, int* __restrict__ lrow,
                                                                 long long* __restrict__ lq) {
-  __shared__ int s_cnt[2], s_base[2];
+  __shared__ int s_base[2];
   constexpr int R = kListTileRows / kListThreads;
+  __shared__ int s_wc[2 * R * (kListThreads / 32)];  // per (class, row group, warp): count, then rank base
   for (int64_t t0 = (int64_t)blockIdx.x * kListTileRows; t0 < n; t0 += (int64_t)gridDim.x * kListTileRows) {
-    if (lrow && threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
-    if (lrow) __syncthreads();
     int loc[R];
     long long qs[R];
     double fr[R], wr[R];
@@ -106,31 +105,45 @@ __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, i
         if (lrow && act) loc[k] = i < n_sig ? 0 : 1;  // class, ranked below
       }
       // layer-1 row lists (kernels_hist_list.cuh): class regions [0, n_sig),
-      // [n_sig, n); one shared atomic per warp and class
+      // [n_sig, n).  Ranks follow the row order inside the tile (per (row
+      // group k, warp) counts, scanned in that order), so a list is sorted
+      // by row within each tile block and the histogram's row gathers stream
       if (lrow) {
-        const int lane = threadIdx.x & 31, cls = loc[k];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, cls = loc[k];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const unsigned m = __ballot_sync(0xffffffffu, cls == c);
-          if (!m) continue;
-          const int leader = __ffs(m) - 1;
-          int b0 = 0;
-          if (lane == leader) b0 = atomicAdd(&s_cnt[c], __popc(m));
-          b0 = __shfl_sync(0xffffffffu, b0, leader);
-          if (cls == c) loc[k] = (c << 30) | (b0 + __popc(m & ((1u << lane) - 1u)));
+          if (lane == 0) s_wc[(c * R + k) * (kListThreads / 32) + warp] = __popc(m);
+          if (cls == c) loc[k] = (c << 30) | __popc(m & ((1u << lane) - 1u));
         }
       }
     }
     if (!lrow) continue;
     __syncthreads();
-    if (threadIdx.x < 2) s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(cnt + threadIdx.x, s_cnt[threadIdx.x]) : 0;
+    if (threadIdx.x < 2) {  // exclusive scan of class c's (k, warp) counts in row order
+      const int c = threadIdx.x;
+      int run = 0;
+      for (int e = 0; e < R * (kListThreads / 32); ++e) {
+        const int x = s_wc[c * R * (kListThreads / 32) + e];
+        s_wc[c * R * (kListThreads / 32) + e] = run;
+        run += x;
+      }
+      s_base[c] = run ? atomicAdd(cnt + c, run) : 0;
+    }
     __syncthreads();
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (loc[k] >= 0) {
+        const int c = loc[k] >> 30;
+        loc[k] += s_wc[(c * R + k) * (kListThreads / 32) + (threadIdx.x >> 5)];
+      }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       if (loc[k] < 0) continue;
       const int64_t i = t0 + k * kListThreads + threadIdx.x;
       const int c = loc[k] >> 30;
       const int64_t pos = (c ? n_sig : 0) + s_base[c] + (loc[k] & 0x3fffffff);
+      BB_DCHECK(pos >= 0 && pos < (c ? n : n_sig));
       lrow[pos] = (int)i;
       lq[pos] = qs[k];
     }
@@ -1000,6 +1013,7 @@ __global__ void __launch_bounds__(kListThreads, 4) k_advance(const CodeT* __rest
       const int reg = s_reg[cls * nodes + (par - start)];
       const int pos = left ? reg + old : reg + cnt[2 * par + cls] - 1 - old;
       const int64_t i = t0 + k * kListThreads + threadIdx.x;
+      BB_DCHECK(pos >= 0 && pos < n && old < cnt[2 * par + cls]);
       lrow[pos] = (int)i;
       lq[pos] = q[i];
     }

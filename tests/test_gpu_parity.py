@@ -154,15 +154,17 @@ def _oracle_hist(codes, node, q, n_sig, d, levels, layer):
     return out
 
 
-@pytest.fixture(params=["list", "fl", "fl_partials", "warp", "cta", "global"])
+@pytest.fixture(params=["list", "list_groups", "fl", "fl_partials", "warp", "cta", "global"])
 def hist_path(request, monkeypatch):
     """Every histogram kernel: the node-partitioned row-list one (default for
     u8 codes and d <= 64), the feature-lane one (TMA bulk reductions into the
     histogram, or with BB_FL_PARTIALS=1 per-CTA partial rows summed by
     k_fl_reduce), the warp-independent shared-memory one, the CTA-barrier one
     and the global-atomic one (BB_HIST_PATH = list | fl | w | cta | g)."""
-    monkeypatch.setenv("BB_HIST_PATH", {"list": "list", "fl": "fl", "fl_partials": "fl", "warp": "w", "cta": "cta",
-                                        "global": "g"}[request.param])
+    monkeypatch.setenv("BB_HIST_PATH", {"list": "list", "list_groups": "list", "fl": "fl", "fl_partials": "fl",
+                                        "warp": "w", "cta": "cta", "global": "g"}[request.param])
+    if request.param == "list_groups":  # rows of 33..64 features as two 32-feature groups
+        monkeypatch.setenv("BB_LH_GROUPS", "1")
     if request.param == "fl_partials":
         monkeypatch.setenv("BB_FL_PARTIALS", "1")
     return request.param
@@ -171,12 +173,12 @@ def hist_path(request, monkeypatch):
 @pytest.mark.parametrize("levels,layer,d", [(8, 1, 10), (8, 3, 40), (8, 5, 7), (10, 6, 3), (3, 2, 5), (1, 1, 2),
                                              (8, 2, 50), (8, 4, 33), (6, 3, 17), (8, 2, 70), (4, 3, 100)])
 def test_layer_hist_exact(levels, layer, d, hist_path):
-    if hist_path == "list" and (d > 64 or levels > 8):
+    if hist_path.startswith("list") and (d > 64 or levels > 8):
         pytest.skip("row-list kernel: u8 codes, d <= 64 (other shapes take the other kernels)")
     rng = np.random.default_rng(levels * 100 + layer)
     n, n_sig = 60_000, 23_456
     # u8 codes with B = 256 hold no NaN bin (the fit stores code - 1)
-    nan_rate = 0.0 if (hist_path == "list" and levels == 8) else 0.05
+    nan_rate = 0.0 if (hist_path.startswith("list") and levels == 8) else 0.05
     codes, node, q = _random_layer(rng, n, n_sig, d, levels, layer, nan_rate=nan_rate)
     B = 1 << levels
     nodes = 1 << (layer - 1)

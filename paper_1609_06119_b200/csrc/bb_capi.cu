@@ -1296,9 +1296,10 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
     BB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kListThreads, smem));
     return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kListTileRows), (int64_t)std::max(1, per) * c.sm_count));
   };
-  const int gridR = resident(k_update_refresh<NodeT>, 0);
+  const int gridR = resident(k_update_refresh<NodeT, CodeT>, 0);
   const int gridL = resident(k_advance<CodeT, NodeT>, 0);
   const int gridLL = resident(k_advance<CodeT, NodeT>, (size_t)32 * s.n_nodes);
+  const int gridAL = std::max(2 * (1 << std::max(0, s.depth - 1)), resident(k_advance_list<CodeT>, 0));
   const auto t0 = std::chrono::steady_clock::now();
   try {
     const bool tl_on = getenv("BB_TIMELINE") != nullptr;  // debug: main-stream waits for masks
@@ -1320,9 +1321,9 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         BB_CUDA(cudaEventRecord(tl.back(), st));  // ... and tree t's mask ready
       }
       if (lists) BB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)2 * s.n_nodes * 4, st));
-      k_update_refresh<NodeT><<<gridR, kListThreads, 0, st>>>(n, s.n_sig, F, node, w_cb, q, mask,
-                                                      t > 0 ? ta.nw + (size_t)(t - 1) * s.n_nodes : nullptr, two_s,
-                                                      cnt, lrow[0], lq[0]);
+      k_update_refresh<NodeT, CodeT><<<gridR, kListThreads, 0, st>>>(
+          n, s.n_sig, F, node, w_cb, q, mask, t > 0 ? ta.nw + (size_t)(t - 1) * s.n_nodes : nullptr, two_s, cnt,
+          lrow[0], lq[0], codes, s.d, code_off, ta, (lists && t > 0) ? t - 1 : -1, s.n_internal, s.depth);
       BB_LAUNCH_CHECK();
       stats.launches += 1;
       for (int layer = 1; layer <= s.depth; ++layer) {
@@ -1364,10 +1365,16 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         BB_LAUNCH_CHECK();
         const bool last = layer == s.depth;
         if (last && p.sib) BB_CUDA(cudaMemsetAsync(hist, 0, (size_t)2 * nodes * s.d * s.B * 8, st));
-        k_advance<CodeT, NodeT><<<last ? gridLL : gridL, kListThreads, last ? (size_t)32 * s.n_nodes : 0, st>>>(
-            codes, s.d, code_off, node, n, s.n_sig, p.start, t, s.n_internal, ta, last ? 1 : 0, s.n_nodes, q, mask,
-            F, w_cb, two_s, sums, cnt, lists ? lrow[layer & 1] : nullptr, lists ? lq[layer & 1] : nullptr,
-            (layer < s.depth && plans[layer + 1].sib) ? 1 : 0);
+        if (lists) {
+          // the layer's listed active rows only (kernels_hist_list.cuh)
+          k_advance_list<CodeT><<<gridAL, kListThreads, 0, st>>>(
+              codes, s.d, code_off, lrow[(layer - 1) & 1], lq[(layer - 1) & 1], cnt, lrow[layer & 1], lq[layer & 1],
+              layer, t, s.n_internal, ta, last ? 1 : 0, s.n_sig, sums, s.n_nodes, F, w_cb, two_s);
+        } else {
+          k_advance<CodeT, NodeT><<<last ? gridLL : gridL, kListThreads, last ? (size_t)32 * s.n_nodes : 0, st>>>(
+              codes, s.d, code_off, node, n, s.n_sig, p.start, t, s.n_internal, ta, last ? 1 : 0, s.n_nodes, q, mask,
+              F, w_cb, two_s, sums, nullptr, nullptr, nullptr, 0);
+        }
         BB_LAUNCH_CHECK();
       }
       BB_CUDA(cudaEventRecord(feed.freed[slot], st));
@@ -1377,6 +1384,11 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
       BB_LAUNCH_CHECK();
       stats.launches += 1;
       if (out->leaves) {
+        if (lists) {  // no per-row node ids in row-list fits: walk the tree
+          k_walk_leaves<CodeT, NodeT><<<gridN, 256, 0, st>>>(codes, s.d, code_off, n, ta, t, s.n_internal, s.depth,
+                                                              node);
+          BB_LAUNCH_CHECK();
+        }
         leaf_tmp.resize(n);
         BB_CUDA(cudaMemcpyAsync(leaf_tmp.data(), node, (size_t)n * sizeof(NodeT), cudaMemcpyDeviceToHost, st));
         BB_CUDA(cudaStreamSynchronize(st));
@@ -1385,6 +1397,9 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
       }
     }
     if (out->scores) {
+      if (lists)
+        k_walk_leaves<CodeT, NodeT><<<gridN, 256, 0, st>>>(codes, s.d, code_off, n, ta, s.T - 1, s.n_internal, s.depth,
+                                                            node);
       k_update_scores<NodeT><<<gridN, 256, 0, st>>>(n, F, node, ta.nw + (size_t)(s.T - 1) * s.n_nodes);
       BB_LAUNCH_CHECK();
       BB_CUDA(cudaMemcpyAsync(out->scores, F, (size_t)n * 8, cudaMemcpyDeviceToHost, st));

@@ -33,6 +33,7 @@
 // added to the global layer histogram by TMA bulk reductions.
 #pragma once
 #include "common.cuh"
+#include "kernels_tree.cuh"
 
 namespace bb {
 
@@ -307,6 +308,166 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
         reinterpret_cast<uint4*>(hb)[i] = make_uint4(0u, 0u, 0u, 0u);
       __syncthreads();
     }
+  }
+}
+
+// Advance over the row lists (row-list fits; replaces the all-rows k_advance):
+// every listed active row of the layer moves to its child (code of the
+// node's cut feature > cut bin -> right; trees.py:207-228).  CTAs take
+// contiguous pieces of the (node, class) segments, so a CTA's rows share one
+// node: its cut is uniform, children are two keys.  Both children are listed
+// for the next layer in the node's region (left from its start, right from
+// its end; ranks in list order within a tile, one global atomic per tile and
+// child).  A row that parks (invalid cut, missing code) leaves the lists and
+// adds its (eff, resp) fixed-point sums to its node; on the last layer every
+// row adds them to its leaf (trees.py:231-244).  Per-row node ids are not
+// kept: the next tree's refresh walks this tree for every row.
+template <typename CodeT>
+__global__ void __launch_bounds__(kListThreads) k_advance_list(
+    const CodeT* __restrict__ codes, int d, int code_off, const int* __restrict__ lrow_in,
+    const long long* __restrict__ lq_in, int* __restrict__ cnt, int* __restrict__ lrow_out,
+    long long* __restrict__ lq_out, int layer, int tree, int n_internal, TreeArrays ta, int last_layer,
+    long long n_sig, unsigned long long* __restrict__ sums, int n_nodes, const double* __restrict__ F,
+    const double* __restrict__ w, double two_s) {
+  constexpr int R = kListTileRows / kListThreads;
+  constexpr int NWARP = kListThreads / 32;
+  __shared__ int4 segs[kLhMaxSegs];
+  __shared__ int s_seg, s_r0, s_r1;
+  __shared__ int s_reg[2 * kAdvMaxNodes];
+  __shared__ int s_wc[2 * R * NWARP];  // per (child side, row group, warp): count, then rank base
+  __shared__ int s_base[2];
+  __shared__ unsigned long long s_sum[3][2];  // (node, left, right) x (eff, resp), two's complement sums
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int start = (1 << (layer - 1)) - 1, nodes = start + 1;
+  if (threadIdx.x == 0) {
+    const int ns = lh_segments(cnt, layer, 0, n_sig, segs);
+    long long Rt = 0;
+    int E = 0;
+    for (int q = 0; q < ns; ++q) {
+      Rt += segs[q].y;
+      E += segs[q].y > 0;
+    }
+    const int G = gridDim.x, Gp = G > E ? G - E : 0;
+    int cum = 0, seg = -1;
+    long long r0 = 0, r1 = 0;
+    for (int q = 0; q < ns && seg < 0; ++q) {
+      if (segs[q].y == 0) continue;
+      const int k = 1 + (int)((long long)Gp * segs[q].y / (Rt > 0 ? Rt : 1));
+      if ((int)blockIdx.x < cum + k) {
+        const int j = (int)blockIdx.x - cum;
+        seg = q;
+        r0 = (long long)segs[q].y * j / k;
+        r1 = (long long)segs[q].y * (j + 1) / k;
+      }
+      cum += k;
+    }
+    s_seg = seg;
+    s_r0 = (int)r0;
+    s_r1 = (int)r1;
+    if (!last_layer) {  // regions of the next layer's lists: class-major prefix of this layer's counts
+      int off = 0;
+      for (int k = 0; k < 2; ++k)
+        for (int p = 0; p < nodes; ++p) {
+          s_reg[k * nodes + p] = off;
+          off += __ldcg(cnt + 2 * (start + p) + k);
+        }
+    }
+  }
+  if (threadIdx.x < 6) s_sum[threadIdx.x >> 1][threadIdx.x & 1] = 0ull;
+  __syncthreads();
+  if (s_seg < 0) return;
+  const int4 sg = segs[s_seg];
+  const int c = start + sg.z, cls = sg.w;
+  const int64_t e_tc = (int64_t)tree * n_internal + c;
+  const bool vld = ta.valid[e_tc] != 0;
+  const int f = vld ? ta.feature[e_tc] : 0;
+  const int cut = vld ? ta.cut[e_tc] : 0;
+  const int* lr = lrow_in + sg.x;
+  const long long* lqs = lq_in + sg.x;
+  const int cnt_c = __ldcg(cnt + 2 * c + cls);
+  const int reg = last_layer ? 0 : s_reg[cls * nodes + sg.z];
+  long long acc_e[3] = {0, 0, 0}, acc_r[3] = {0, 0, 0};  // per thread: (node, left, right)
+  for (int t0 = s_r0; t0 < s_r1; t0 += kListTileRows) {
+    int rowv[R], side[R];  // side: 0 left, 1 right, 2 parked, -1 none
+    long long qv[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int e = t0 + k * kListThreads + threadIdx.x;
+      rowv[k] = e < s_r1 ? __ldg(lr + e) : -1;
+      qv[k] = e < s_r1 ? __ldg(lqs + e) : 0;
+    }
+    int cv[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      cv[k] = (rowv[k] >= 0 && vld) ? (int)codes[code_index(rowv[k], f, d)] + code_off : 0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      side[k] = rowv[k] < 0 ? -1 : (cv[k] == 0 ? 2 : (cv[k] > cut ? 1 : 0));
+      if (side[k] == 2 || (last_layer && side[k] >= 0)) {
+        // fixed-point (eff, resp) of the row at its final node (k_advance's last-layer rule)
+        const int64_t i = rowv[k];
+        const int lab = row_label(i, n_sig);
+        const double r = residual_of(F[i], lab);
+        const double wi = w ? w[i] : 1.0;
+        const long long qr = __double2ll_rn(__dmul_rn(__dmul_rn(wi, r), two_s));
+        const int slot = side[k] == 2 ? 0 : 1 + side[k];
+        acc_e[slot] += qv[k];
+        acc_r[slot] += qr;
+      }
+    }
+    if (!last_layer) {
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+#pragma unroll
+        for (int sd = 0; sd < 2; ++sd) {
+          const unsigned m = __ballot_sync(0xffffffffu, side[k] == sd);
+          if (lane == 0) s_wc[(sd * R + k) * NWARP + warp] = __popc(m);
+          if (side[k] == sd) rowv[k] = (rowv[k] & 0x7fffffff), side[k] = sd + 4 * __popc(m & ((1u << lane) - 1u));
+        }
+      __syncthreads();
+      if (threadIdx.x < 2) {
+        const int sd = threadIdx.x;
+        int run = 0;
+        for (int e = 0; e < R * NWARP; ++e) {
+          const int x = s_wc[sd * R * NWARP + e];
+          s_wc[sd * R * NWARP + e] = run;
+          run += x;
+        }
+        s_base[sd] = run ? atomicAdd(cnt + 2 * (2 * c + 1 + sd) + cls, run) : 0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if (rowv[k] < 0 || (side[k] & 3) > 1) continue;
+        const int sd = side[k] & 3;
+        const int old = s_base[sd] + s_wc[(sd * R + k) * NWARP + warp] + (side[k] >> 2);
+        const int pos = sd == 0 ? reg + old : reg + cnt_c - 1 - old;
+        BB_DCHECK(old < cnt_c && pos >= 0);
+        lrow_out[pos] = rowv[k];
+        lq_out[pos] = qv[k];
+      }
+      __syncthreads();
+    }
+  }
+  // node sums of this CTA's rows: (parked at c, left child, right child)
+#pragma unroll
+  for (int s3 = 0; s3 < 3; ++s3) {
+    long long e = acc_e[s3], r = acc_r[s3];
+    for (int o = 16; o > 0; o >>= 1) {
+      e += __shfl_xor_sync(0xffffffffu, e, o);
+      r += __shfl_xor_sync(0xffffffffu, r, o);
+    }
+    if (lane == 0 && (e != 0 || r != 0)) {
+      atomicAdd(&s_sum[s3][0], as_ull(e));
+      atomicAdd(&s_sum[s3][1], as_ull(r));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int s3 = threadIdx.x >> 1, kind = threadIdx.x & 1;
+    const unsigned long long v = s_sum[s3][kind];
+    const int nd = s3 == 0 ? c : 2 * c + s3;
+    if (v != 0ull && nd < n_nodes) atomicAdd(&sums[((int64_t)cls * n_nodes + nd) * 2 + kind], v);
   }
 }
 

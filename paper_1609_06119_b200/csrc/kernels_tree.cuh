@@ -54,14 +54,43 @@ __global__ void k_iota(int* __restrict__ a, int64_t n) {
 constexpr int kListTileRows = 2048;  // rows per CTA tile (512 threads x 4)
 constexpr int kListThreads = 512;
 
-template <typename NodeT>
+// Leaf of row i in tree `tree` over its bin codes (trees.py:318-330): an
+// invalid node or a missing code stops the walk.
+template <typename CodeT>
+__device__ __forceinline__ int walk_leaf(const CodeT* __restrict__ codes, int d, int code_off, int64_t i,
+                                         const TreeArrays& ta, int tree, int n_internal, int depth) {
+  int nd = 0;
+  for (int l = 0; l < depth; ++l) {
+    const int64_t e = (int64_t)tree * n_internal + nd;
+    if (!__ldg(&ta.valid[e])) break;
+    const int c = (int)codes[code_index(i, __ldg(&ta.feature[e]), d)] + code_off;
+    if (c == 0) break;
+    nd = 2 * nd + 1 + (c > __ldg(&ta.cut[e]) ? 1 : 0);
+  }
+  return nd;
+}
+
+template <typename CodeT, typename NodeT>
+__global__ void k_walk_leaves(const CodeT* __restrict__ codes, int d, int code_off, int64_t n, TreeArrays ta, int tree,
+                              int n_internal, int depth, NodeT* __restrict__ node) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    node[i] = (NodeT)walk_leaf(codes, d, code_off, i, ta, tree, n_internal, depth);
+}
+
+// walk_tree >= 0 (row-list fits): the previous tree's leaf of every row is
+// found by walking that tree over the codes (no per-row node ids are kept);
+// otherwise it is node[i].
+template <typename NodeT, typename CodeT>
 __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, int64_t n_sig, double* __restrict__ F,
                                                                 NodeT* __restrict__ node, const double* __restrict__ w,
                                                                 long long* __restrict__ q,
                                                                 const unsigned int* __restrict__ mask,
                                                                 const double* __restrict__ nw_prev, double two_s,
                                                                 int* __restrict__ cnt, int* __restrict__ lrow,
-                                                                long long* __restrict__ lq) {
+                                                                long long* __restrict__ lq,
+                                                                const CodeT* __restrict__ codes, int d, int code_off,
+                                                                TreeArrays ta, int walk_tree, int n_internal,
+                                                                int depth) {
   __shared__ int s_base[2];
   constexpr int R = kListTileRows / kListThreads;
   __shared__ int s_wc[2 * R * (kListThreads / 32)];  // per (class, row group, warp): count, then rank base
@@ -78,7 +107,36 @@ __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, i
       wr[k] = (in && w) ? w[i] : 1.0;
       mw[k] = in ? mask[i >> 5] : 0u;
     }
-    if (nw_prev) {
+    if (nw_prev && walk_tree >= 0) {
+      // the R rows' walks in lockstep: independent gather chains overlap
+      int nd[R];
+      bool live[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        nd[k] = 0;
+        live[k] = t0 + k * kListThreads + threadIdx.x < n;
+      }
+      for (int l = 0; l < depth; ++l) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          if (!live[k]) continue;
+          const int64_t i = t0 + k * kListThreads + threadIdx.x;
+          const int64_t e = (int64_t)walk_tree * n_internal + nd[k];
+          if (!__ldg(&ta.valid[e])) { live[k] = false; continue; }
+          const int c = (int)codes[code_index(i, __ldg(&ta.feature[e]), d)] + code_off;
+          if (c == 0) { live[k] = false; continue; }
+          nd[k] = 2 * nd[k] + 1 + (c > __ldg(&ta.cut[e]) ? 1 : 0);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int64_t i = t0 + k * kListThreads + threadIdx.x;
+        if (i < n) {
+          fr[k] = __dadd_rn(fr[k], nw_prev[nd[k]]);
+          F[i] = fr[k];
+        }
+      }
+    } else if (nw_prev) {
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         const int64_t i = t0 + k * kListThreads + threadIdx.x;
@@ -100,7 +158,7 @@ __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, i
         const bool act = (mw[k] >> (i & 31)) & 1u;
         const long long qv = act ? __double2ll_rn(__dmul_rn(__dmul_rn(wr[k], bw), two_s)) : 0ll;
         q[i] = qv;
-        node[i] = 0;
+        if (walk_tree < 0) node[i] = 0;
         qs[k] = qv;
         if (lrow && act) loc[k] = i < n_sig ? 0 : 1;  // class, ranked below
       }

@@ -636,7 +636,8 @@ static SegPlan build_seg_plan(int n, long long slack) {
     auto piece = [&](int pl, int ph, int np, int code, int j0) {
       if (np <= 0) return;
       const double band = (double)smear_host((unsigned)ph) + 1.0;
-      if ((double)(ph - pl + 1 + kSub) * 64.0 <= band) {
+      static const double ratio = getenv("BB_PIECE_RATIO") ? atof(getenv("BB_PIECE_RATIO")) : 64.0;
+      if ((double)(ph - pl + 1 + kSub) * ratio <= band) {
         P.tasks.push_back(int2{(int)P.tab.size(), code});
       } else {
         for (int j = 0; j < np; ++j) P.tasks.push_back(int2{(int)P.tab.size(), j0 + j});
@@ -1014,6 +1015,16 @@ struct MaskGen {
         // k == 0: nothing is active (position 0 is never a step target)
         if (kk == 0 || nn <= 1 || kk >= nn) {
           BB_CUDA(cudaMemsetAsync(removed[cc], kk == 0 ? 1 : 0, (size_t)std::max(1, nn), st));
+          continue;
+        }
+        const bool buckets = getenv("BB_MASK_BUCKETS") && atoi(getenv("BB_MASK_BUCKETS")) != 0;  // per call: tests
+        if (!buckets) {
+          // sort-free resolution (kernels_mask.cuh k_up_min / k_resolve_values)
+          BB_CUDA(cudaMemsetAsync(cnt, 0x7f, (size_t)nn * 4, st));  // up[] = 0x7f7f7f7f (no step)
+          k_up_min<<<grid_for(nn - kk, 256, sm), 256, 0, st>>>(Jt, kk, nn, cnt);
+          k_resolve_values<<<grid_for(nn, 256, sm), 256, 0, st>>>(Jt, kk, nn, cnt, removed[cc]);
+          BB_LAUNCH_CHECK();
+          launches += 2;
           continue;
         }
         BB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)nn * 4, st));  // fill and removed: cleared by k_scan_apply

@@ -168,6 +168,43 @@ __global__ void k_resolve(const int* __restrict__ J, int k, int n, const int* __
   }
 }
 
+// Sort-free resolution (replaces the bucket pipeline below on the fit path).
+// Follow a value instead of a step: value v starts at position v; while it
+// sits at position p it is hit (moved to a final position >= k, i.e.
+// removed) iff a step t targets p while it is there, and it leaves p at step
+// p (to J[p]) if p >= k.  Steps run downward, so v sits at p from the step
+// that brought it there (prev) down to p, and a hit exists iff
+// up[p] = min{t > p : J[t] = p} < prev.  J[p] == p keeps v at p until p
+// is final: removed.  A value that reaches p < k unhit stays active.
+// (Equal to the chain rule of k_resolve on every case of
+// tests/test_gpu_parity.py; derivation in DESIGN.md §Kernels.)
+constexpr int kUpNone = 0x7f7f7f7f;  // up[] initial value (memset 0x7f): no step targets the position
+
+__global__ void k_up_min(const int* __restrict__ J, int k, int n, int* __restrict__ up) {
+  const int t0 = k > 1 ? k : 1;
+  for (int t = t0 + blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int p = J[t];
+    if (p != t) atomicMin(&up[p], t);
+  }
+}
+
+__global__ void k_resolve_values(const int* __restrict__ J, int k, int n, const int* __restrict__ up,
+                                 unsigned char* __restrict__ removed) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int p = v, prev = kUpNone;  // no step before the first position: up[p] < kUpNone iff some step targets p
+    unsigned char rem = 0;
+    for (;;) {
+      if (__ldg(&up[p]) < prev) { rem = 1; break; }
+      if (p < k) break;
+      const int j = __ldg(&J[p]);
+      if (j == p) { rem = 1; break; }
+      prev = p;
+      p = j;
+    }
+    removed[v] = rem;
+  }
+}
+
 // active bits, class-block order: bit g < n_sig -> signal value g, else
 // background value g - n_sig
 __global__ void k_mask_bits(const unsigned char* __restrict__ rem_sig, const unsigned char* __restrict__ rem_bkg,

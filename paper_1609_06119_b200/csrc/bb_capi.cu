@@ -2151,6 +2151,12 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
     if (!ctx || !fo) throw InvalidArg{"null argument"};
     if (d != fo->n_features)
       throw InvalidArg{"model expects " + std::to_string(fo->n_features) + " features, rows have " + std::to_string(d)};
+    if (fo->n_trees < 0 || fo->depth < 1 || fo->depth > 20) throw InvalidArg{"invalid forest shape"};
+    // cut features index the row in shared memory: reject out-of-range ones
+    for (size_t e = 0, te = (size_t)fo->n_trees * ((1 << fo->depth) - 1); e < te; ++e)
+      if (fo->valid[e] && (fo->feature[e] < 0 || fo->feature[e] >= d))
+        throw InvalidArg{"cut feature " + std::to_string(fo->feature[e]) + " out of range for " + std::to_string(d) +
+                         " features"};
     if (n == 0) return;
     std::lock_guard<std::mutex> lock(ctx->c.mu);
     Ctx& c = ctx->c;
@@ -2230,7 +2236,7 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
       // each continuing F in tree order
       // (2 levels measured best: cfg4 889 M rows/s; 3 levels need two launches
       // for 1000 trees and a 4-way select: 583 M)
-      const int PL = getenv("BB_APPLY_PARAM_LEVELS") ? std::max(0, std::min(3, atoi(getenv("BB_APPLY_PARAM_LEVELS"))))
+      const int PL = getenv("BB_APPLY_PARAM_LEVELS") ? std::max(0, std::min(std::min(3, D), atoi(getenv("BB_APPLY_PARAM_LEVELS"))))
                                                      : std::min(D, 2);
       const int RP = (1 << PL) - 1;
       const int per_launch = RP ? kApplyParamRecs / RP : fo->n_trees;

@@ -82,25 +82,36 @@ __device__ __forceinline__ unsigned int draw_at(const PcgJump& J, const RngState
 constexpr int kDrawChunk = 64;  // PCG outputs per thread
 
 // draws [j_lo, j_hi) of the buffer (a chunk's draws are generated in two
-// parts: the first jobs' range on the critical stream, the rest overlapped)
+// parts: the first jobs' range on the critical stream, the rest overlapped).
+// A warp owns 32 * kDrawChunk consecutive outputs, lane l the outputs
+// l, l + 32, ...: one jump to its first output, then the 32-step LCG map
+// (A_32, C_32) per output, so each warp-wide store covers 256 contiguous
+// bytes of the buffer.
 __global__ void k_pcg_draws(const PcgJump* __restrict__ Jp, const RngState* __restrict__ rs,
                             unsigned int* __restrict__ draws, long long j_lo, long long j_hi) {
   const RngState r = *rs;
   const long long h = r.has_uint32 ? 1 : 0;
   const long long out_lo = j_lo > h ? (j_lo - h) / 2 : 0;   // first output touching [j_lo, j_hi)
   const long long out_hi = (j_hi - h + 1) / 2;              // outputs before this cover j < j_hi
-  const long long q0 = out_lo + ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kDrawChunk;
-  if (q0 >= out_hi) return;
-  if (q0 == 0 && h && j_lo == 0) draws[0] = r.uinteger;
-  U128 s = pcg_jump(*Jp, r.s, (unsigned long long)q0);  // state before output q0
-  const U128 a = Jp->A[0], c = Jp->C[0];
-  const long long q1 = min(out_hi, q0 + kDrawChunk);
-  for (long long qq = q0; qq < q1; ++qq) {
-    s = u128_add(u128_mul(a, s), c);
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const long long wbase = out_lo + (gt >> 5) * 32 * kDrawChunk;
+  if (wbase >= out_hi) return;
+  if (wbase == 0 && lane == 0 && h && j_lo == 0) draws[0] = r.uinteger;
+  const long long q0 = wbase + lane;
+  U128 s = pcg_jump(*Jp, r.s, (unsigned long long)q0 + 1ull);  // state after output q0
+  const U128 a = Jp->A[5], c = Jp->C[5];                       // 32 steps
+  const long long q1 = min(out_hi, wbase + 32 * kDrawChunk);
+  for (long long qq = q0; qq < q1; qq += 32) {
     const unsigned long long o = xsl_rr(s);
     const long long j = h + 2 * qq;
-    if (j >= j_lo && j < j_hi) draws[j] = (unsigned int)o;
-    if (j + 1 >= j_lo && j + 1 < j_hi) draws[j + 1] = (unsigned int)(o >> 32);
+    if (j >= j_lo && j + 1 < j_hi && !h) {
+      *reinterpret_cast<uint2*>(draws + j) = make_uint2((unsigned int)o, (unsigned int)(o >> 32));
+    } else {
+      if (j >= j_lo && j < j_hi) draws[j] = (unsigned int)o;
+      if (j + 1 >= j_lo && j + 1 < j_hi) draws[j + 1] = (unsigned int)(o >> 32);
+    }
+    s = u128_add(u128_mul(a, s), c);
   }
 }
 

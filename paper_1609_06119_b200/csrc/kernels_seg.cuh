@@ -44,9 +44,10 @@
 namespace bb {
 
 #ifndef BB_SEG_MAXLEN
-#define BB_SEG_MAXLEN 8192
+#define BB_SEG_MAXLEN 32768
 #endif
 constexpr int kSegMaxLen = BB_SEG_MAXLEN;   // draws per segment (max)
+constexpr int kWalkStage = 8192;            // draws per shared-memory stage of an exact walk
 constexpr int kSegCrossLen = 1024; // draws per segment in band-crossing zones
 constexpr int kAnchorSlackMin = 512;   // a job's segments start at its predicted first draw + a slack of
 constexpr int kAnchorSlackMax = 4000;  // 5 sd of a job's draw count, clamped to this range
@@ -240,7 +241,7 @@ constexpr int kTabChunk = 64, kTabChunks = 4;  // table entries streamed into k_
 // dynamic shared memory of the chain kernel; BB_CHAIN_SMEM_KB pads it so that
 // no other CTA can share the chain's SM (its single-warp dependent chains
 // lose issue slots to co-resident phase-1 warps)
-constexpr int kSegComposeSmemUsed = kSegRing * kSegMaxSub * 128 + kTabChunk * kTabChunks * 48 + (kSegMaxLen + 16) * 4;
+constexpr int kSegComposeSmemUsed = kSegRing * kSegMaxSub * 128 + kTabChunk * kTabChunks * 48 + (kWalkStage + 16) * 4;
 constexpr int kSegComposeSmem =
     kSegComposeSmemUsed > BB_CHAIN_SMEM_KB * 1024 ? kSegComposeSmemUsed : BB_CHAIN_SMEM_KB * 1024;
 
@@ -810,7 +811,7 @@ __device__ __forceinline__ void cp_async16_seg(void* dst, const void* src) {
 // Exact walk by one warp over draws staged in shared memory by bulk copies
 // (16-byte aligned source: copy from base & ~3, walk from base & 3).
 struct StageWalk {
-  unsigned int* sd;  // kSegMaxLen + 16 draws
+  unsigned int* sd;  // kWalkStage + 16 draws
   uint64_t* bar;
   unsigned phase;
   __device__ int operator()(const SegArgs& a, const RngState& r0, long long base, long long len, int i, int k, int* J,
@@ -818,9 +819,9 @@ struct StageWalk {
     long long done = 0;
     while (done < len && i >= 1) {
       const long long b = base + done;
-      const int n = (int)min((long long)kSegMaxLen, len - done);
+      const int n = (int)min((long long)kWalkStage, len - done);
       if (lane == 0 && len - done > n)
-        seg_prefetch_l2(a.draws, b + n, min((long long)kSegMaxLen, len - done - n), a.n_draws);
+        seg_prefetch_l2(a.draws, b + n, min((long long)kWalkStage, len - done - n), a.n_draws);
       int u;
       if (b + n + 4 <= a.n_draws) {
         const long long ab = b & ~3ll;
@@ -1005,7 +1006,7 @@ __global__ void __launch_bounds__(64) k_seg_chain(SegArgs a) {
 
 // phase 2b: one warp walks the tail (states below kSegTail) to the job's
 // last draw, writing J for steps >= k; the next draw is the next job's first.
-constexpr int kSegTailSmem = (kSegMaxLen + 16) * 4;
+constexpr int kSegTailSmem = (kWalkStage + 16) * 4;
 // phase 2b: walk the tail (states below kSegTail) from (p, i) to the job's
 // last draw, writing J for steps >= k; the next draw is the next job's first.
 __device__ void seg_tail_walk(const SegArgs& a, const RngState& r0, StageWalk& walk, long long p, int i, int lane) {
@@ -1014,7 +1015,7 @@ __device__ void seg_tail_walk(const SegArgs& a, const RngState& r0, StageWalk& w
   long long tail = 0;
   while (i >= 1) {
     long long used;
-    i = walk(a, r0, p, 8 * kSegMaxLen, i, jb.k, jb.J, lane, &used, kLeanTail);
+    i = walk(a, r0, p, 8 * kWalkStage, i, jb.k, jb.J, lane, &used, kLeanTail);
     p += used;
     tail += used;
   }
@@ -1055,7 +1056,7 @@ __device__ void seg_tail_walk(const SegArgs& a, const RngState& r0, StageWalk& w
 }
 
 __global__ void __launch_bounds__(32) k_seg_tail(SegArgs a) {
-  extern __shared__ __align__(16) unsigned int sd[];  // kSegMaxLen + 16 draws
+  extern __shared__ __align__(16) unsigned int sd[];  // kWalkStage + 16 draws
   __shared__ __align__(8) uint64_t st_bar;
   const int lane = threadIdx.x;
   const RngState r0 = *a.rng0;

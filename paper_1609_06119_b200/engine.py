@@ -250,15 +250,33 @@ def _fit_native(X, xdt, x_dev, n, d, y01, y_dev, w, w_dev, cfg, *, forced_cuts=N
                   fit_info=info)
 
 
+def _pad(a: np.ndarray, size: int, fill) -> np.ndarray:
+    out = np.full(size, fill, dtype=a.dtype)
+    out[: a.shape[0]] = a
+    return out
+
+
 def _forest_struct(forest: Forest):
+    """Packs the forest for bb_predict.  Trees of a mixed-depth forest (the
+    model format allows it, model_io.py:185-191) are padded to the deepest
+    tree: a shallow tree's leaves become invalid internal nodes, where the
+    traversal stops (trees.py:333-346), so its predictions are unchanged."""
     T = len(forest.trees)
-    depth = forest.trees[0].depth if T else 1
+    depth = max(t.depth for t in forest.trees) if T else 1
     I, N = (1 << depth) - 1, (1 << (depth + 1)) - 1
     if T:
-        feat = np.ascontiguousarray(np.stack([np.where(t.valid, t.feature, 0) for t in forest.trees]), dtype=np.int32)
-        valid = np.ascontiguousarray(np.stack([t.valid for t in forest.trees]), dtype=np.uint8)
-        thr = np.ascontiguousarray(np.stack([t.threshold for t in forest.trees]), dtype=np.float64)
-        nw = np.ascontiguousarray(np.stack([t.node_weight for t in forest.trees]), dtype=np.float64)
+        for k, t in enumerate(forest.trees):
+            fv = np.asarray(t.feature)[np.asarray(t.valid, dtype=bool)]
+            if fv.size and (fv.min() < 0 or fv.max() >= forest.n_features):
+                raise ValueError(f"tree {k}: cut feature out of range for a model with {forest.n_features} features")
+        feat = np.ascontiguousarray(np.stack([_pad(np.where(t.valid, t.feature, 0), I, 0) for t in forest.trees]),
+                                    dtype=np.int32)
+        valid = np.ascontiguousarray(np.stack([_pad(np.asarray(t.valid, dtype=np.uint8), I, 0) for t in forest.trees]),
+                                     dtype=np.uint8)
+        thr = np.ascontiguousarray(np.stack([_pad(np.asarray(t.threshold, dtype=np.float64), I, 0.0)
+                                             for t in forest.trees]), dtype=np.float64)
+        nw = np.ascontiguousarray(np.stack([_pad(np.asarray(t.node_weight, dtype=np.float64), N, 0.0)
+                                            for t in forest.trees]), dtype=np.float64)
     else:
         feat = np.zeros((0, I), np.int32)
         valid = np.zeros((0, I), np.uint8)

@@ -35,6 +35,18 @@ def test_engine_input_validation():
         fit_forest(np.zeros((4, 2)), np.array([0, 1, 0, 1]), np.array([1, np.inf, 1, 1]))
 
 
+def test_predict_rejects_out_of_range_cut_feature():
+    """bb_predict indexes the row by cut feature: a hand-built forest with a
+    feature >= n_features is rejected before anything reaches the GPU."""
+    from paper_1609_06119_b200.engine import FeatureBinning, Forest, Tree, predict_batch
+
+    t = Tree(depth=1, feature=np.array([3]), cut_bin=np.array([1]), threshold=np.array([0.0]), gain=np.zeros(1),
+             valid=np.array([True]), node_weight=np.zeros(3), node_purity=np.zeros(3))
+    forest = Forest(f0=0.0, trees=[t], binnings=[FeatureBinning(np.array([0.0]), 1)] * 2)
+    with pytest.raises(ValueError, match="out of range"):
+        predict_batch(forest, np.zeros((4, 2)))
+
+
 def test_bridge_validation_messages():
     with pytest.raises(ValueError, match="features must be a 2-d matrix"):
         bridge.fit(np.zeros(4), [0, 1, 0, 1])

@@ -419,6 +419,36 @@ def test_apply_large_forest_multi_launch():
         np.testing.assert_array_equal(F, ref)
 
 
+def test_apply_mixed_depth_forest():
+    """A forest whose trees have different depths (allowed by the model file,
+    model_io.py:185-191): shallow trees are padded with invalid nodes, so each
+    tree's prediction is its own traversal (trees.py:333-346)."""
+    from paper_1609_06119_b200.engine import FeatureBinning, Forest, Tree
+
+    rng = np.random.default_rng(21)
+    d = 5
+    X = rng.normal(size=(4000, d))
+    X[rng.random(X.shape) < 0.05] = np.nan
+    trees = []
+    for t, D in enumerate([1, 3, 2, 5, 4, 3]):
+        I, N = (1 << D) - 1, (1 << (D + 1)) - 1
+        valid = rng.random(I) > 0.1
+        feature = np.where(valid, rng.integers(0, d, I), -1)
+        thr = np.where(valid, rng.normal(size=I), np.nan)
+        nw = rng.uniform(-1, 1, N)
+        trees.append(Tree(depth=D, feature=feature, cut_bin=np.where(valid, 1, 0), threshold=thr, gain=np.zeros(I),
+                          valid=valid, node_weight=nw, node_purity=np.zeros(N)))
+    forest = Forest(f0=0.1, trees=trees, binnings=[FeatureBinning(np.sort(rng.normal(size=7)), 3) for _ in range(d)])
+    for dt in (np.float64, np.float32):
+        Xc = X.astype(dt)
+        ref = np.full(X.shape[0], 0.1)
+        for t in trees:
+            ref += oracle.predict_scores(0.0, t.valid[None], t.feature[None], t.threshold[None], t.node_weight[None],
+                                         t.depth, Xc)
+        _, F = predict_batch(forest, Xc, return_scores=True)
+        np.testing.assert_allclose(F, ref, rtol=0, atol=1e-12)
+
+
 # ------------------------------------------------------------------ bridge
 def test_bridge_fit_predict_and_concurrency():
     X, y, w, _ = make_config("cfg1", n=20_000)

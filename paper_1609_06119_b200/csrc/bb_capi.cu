@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -23,6 +24,7 @@
 #include "../../include/fastbdt_b200.h"
 #include "bb_mask.h"
 #include "bb_nccl.h"
+#include "bb_stage.h"
 #include "common.cuh"
 #include "kernels_apply.cuh"
 #include "kernels_binning.cuh"
@@ -85,6 +87,7 @@ struct Ctx {
   int sm_count = 148;
   std::mutex mu;
   NcclComm comm;  // world > 1: row-sharded fits
+  HostStager stage;  // pinned staging of pageable host buffers (bb_stage.h)
 };
 
 // class-block layout of this rank's rows inside the global blocks
@@ -1479,28 +1482,24 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   Arena A(st);
   const int levels = cfg.binning_levels, B = 1 << levels, nt = B - 1;
   NvtxRange fit_range("bb_fit");
-  // ---- upload
+  // ---- upload: labels and weights first (the class-block kernels and the
+  // subsample masks need only these), the rows after the first mask chunk
+  // has been queued, so its parse overlaps the row upload as well
   auto t_up = std::chrono::steady_clock::now();
   const T* Xd = reinterpret_cast<const T*>(Xv);
-  if (!x_dev) {
-    T* p = A.alloc<T>((size_t)n * d);
-    BB_CUDA(cudaMemcpyAsync(p, Xv, (size_t)n * d * sizeof(T), cudaMemcpyHostToDevice, st));
-    Xd = p;
-  }
   const int8_t* yd = y;
   if (!y_dev) {
     int8_t* p = A.alloc<int8_t>(n);
-    BB_CUDA(cudaMemcpyAsync(p, y, (size_t)n, cudaMemcpyHostToDevice, st));
+    c.stage.h2d(p, y, (size_t)n, st);
     yd = p;
   }
   const double* wd = w;
   if (w && !w_dev) {
     double* p = A.alloc<double>(n);
-    BB_CUDA(cudaMemcpyAsync(p, w, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    c.stage.h2d(p, w, (size_t)n * 8, st);
     wd = p;
   }
-  BB_CUDA(cudaStreamSynchronize(st));
-  const double ms_up = elapsed_ms(t_up);
+  double ms_up = elapsed_ms(t_up);
   // ---- class blocks (sample.py:112-116)
   auto t_bin = std::chrono::steady_clock::now();
   const bool dist = c.comm.active();  // row-sharded fit: every rank holds a slice of the rows
@@ -1551,6 +1550,13 @@ static void fit_impl(Ctx& c, const void* Xv, bool x_dev, int64_t n, int d, const
   MaskFeed feed;
   feed.init(c, A, n, n_sig, cfg, shard, &stats);
   feed.ahead(0);
+  if (!x_dev) {
+    t_up = std::chrono::steady_clock::now();
+    T* p = A.alloc<T>((size_t)n * d);
+    c.stage.h2d(p, Xv, (size_t)n * d * sizeof(T), st);
+    Xd = p;
+    ms_up += elapsed_ms(t_up);
+  }
   // user weights: per-class pairwise-sum leaves and max |w| on the device
   // (read back after the binning kernels are queued)
   std::vector<long long> pw_off;
@@ -1830,12 +1836,12 @@ static ElimSession* elim_prepare(Ctx& c, const T* X, int64_t n, int d, const int
   Arena A(st);
   T* Xd = A.alloc<T>((size_t)n * d);
   int8_t* yd = A.alloc<int8_t>(n);
-  BB_CUDA(cudaMemcpyAsync(Xd, X, (size_t)n * d * sizeof(T), cudaMemcpyHostToDevice, st));
-  BB_CUDA(cudaMemcpyAsync(yd, y, (size_t)n, cudaMemcpyHostToDevice, st));
+  c.stage.h2d(Xd, X, (size_t)n * d * sizeof(T), st);
+  c.stage.h2d(yd, y, (size_t)n, st);
   double* wd = nullptr;
   if (w) {
     wd = A.alloc<double>(n);
-    BB_CUDA(cudaMemcpyAsync(wd, w, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    c.stage.h2d(wd, w, (size_t)n * 8, st);
   }
   // class blocks (sample.py:112-116)
   const int n_tiles = (int)ceil_div(n, CLS_TILE);
@@ -1903,7 +1909,7 @@ static ElimSession* elim_prepare(Ctx& c, const T* X, int64_t n, int d, const int
   // validation rows: keys, codes with the training boundaries, input order
   if (nv > 0) {
     T* Xvd = A.alloc<T>((size_t)nv * d);
-    BB_CUDA(cudaMemcpyAsync(Xvd, Xv, (size_t)nv * d * sizeof(T), cudaMemcpyHostToDevice, st));
+    c.stage.h2d(Xvd, Xv, (size_t)nv * d * sizeof(T), st);
     std::vector<unsigned long long> f2, n2;
     unsigned long long* fd2 = nullptr;
     K* vkeys = make_keys<T>(c, A, Xvd, nv, d, f2, n2, &fd2);
@@ -2010,6 +2016,29 @@ static void elim_fit(Ctx& c, const ElimSession& s, const int* cols, int nc, cons
 }  // namespace bb
 
 using namespace bb;
+
+// two copy streams and K + 1 events of a row pipeline (bb_predict)
+struct PipeStreams {
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev[PinnedRing::kBufs + 1] = {};
+  explicit PipeStreams(int) {
+    BB_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+    BB_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+    for (auto& e : ev) BB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  ~PipeStreams() {
+    if (s_in) {
+      cudaStreamSynchronize(s_in);
+      cudaStreamDestroy(s_in);
+    }
+    if (s_out) {
+      cudaStreamSynchronize(s_out);
+      cudaStreamDestroy(s_out);
+    }
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
 
 struct bb_ctx {
   Ctx c;
@@ -2177,10 +2206,15 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
     }
     ApplyForest af{fo->n_trees, fo->depth, I, N, feat, vld, thr, nw, fo->f0};
     const size_t es = x_dtype == BB_F32 ? 4 : 8;
+    const size_t row_bytes = (size_t)d * es;
+    // host rows: uploaded and scored in row chunks through pinned staging
+    // (bb_stage.h), the chunk's DMA, kernels and result read-back overlapping
+    const bool pipe = !x_on_device && !out_on_device && (size_t)n * row_bytes >= HostStager::kMinStaged &&
+                      !host_pointer_is_pinned(X) && !getenv("BB_NO_STAGING");
     const void* Xd = X;
     if (!x_on_device) {
-      void* p = A.alloc<unsigned char>((size_t)n * d * es);
-      BB_CUDA(cudaMemcpyAsync(p, X, (size_t)n * d * es, cudaMemcpyHostToDevice, st));
+      void* p = A.alloc<unsigned char>((size_t)n * row_bytes);
+      if (!pipe) c.stage.h2d(p, X, (size_t)n * row_bytes, st);
       Xd = p;
     }
     double* pd = out_prob;
@@ -2189,16 +2223,24 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
       pd = out_prob ? A.alloc<double>(n) : nullptr;
       fd = out_score ? A.alloc<double>(n) : nullptr;
     }
-    const unsigned grid = (unsigned)ceil_div(n, APPLY_ROWS);
     const size_t smem = (size_t)APPLY_ROWS * (d + 1) * es;
     const size_t smem32 = ((size_t)kApplyRows * (d + 1) * 4 + 15) / 16 * 16 + (size_t)kApplyTB * (N * 8 + I * 8);
     const int D = fo->depth;
     const size_t smemD = ((size_t)kApplyDRows * (d + 1) * 4 + 15) / 16 * 16 +
                          (size_t)kApplyDTB * (((size_t)1 << D) * 8 + (size_t)I * 8);
+    // launch_rows(r0, nr): score rows [r0, r0 + nr) on st.  The host staging
+    // vectors of the chosen kernel live until the final synchronisation.
+    std::function<void(int64_t, int64_t)> launch_rows;
+    std::vector<int2> hr, hn;
+    std::vector<double> hl;
+    std::unique_ptr<ApplyRoots> roots;
+    auto rows_at = [&](int64_t r0) { return (const void*)((const char*)Xd + (size_t)r0 * row_bytes); };
+    auto at = [](double* p, int64_t r0) { return p ? p + r0 : nullptr; };
     if (x_dtype == BB_F32 && D >= 1 && D <= 6 && smemD <= 200 * 1024) {
       // fixed-depth walk over leaf tables with the invalid-node stops folded in
-      std::vector<int2> hr(TI), hn(TI);
-      std::vector<double> hl((size_t)fo->n_trees << D);
+      hr.resize(TI);
+      hn.resize(TI);
+      hl.resize((size_t)fo->n_trees << D);
       for (int t = 0; t < fo->n_trees; ++t) {
         for (int k = 0; k < I; ++k) {
           const size_t e = (size_t)t * I + k;
@@ -2243,18 +2285,19 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
       const int n_launch = fo->n_trees > 0 ? (int)ceil_div(fo->n_trees, per_launch) : 1;
       double* fa = fd;
       if (n_launch > 1 && !fa) fa = A.alloc<double>(n);  // F between launches
-      const unsigned gd = (unsigned)ceil_div(n, kApplyDRows);
-      auto roots = std::make_unique<ApplyRoots>();  // host staging; each launch copies its parameters
-      for (int li = 0; li < n_launch; ++li) {
-        const int t0 = li * per_launch, t1 = std::min(fo->n_trees, t0 + per_launch);
-        for (int t = t0; t < t1; ++t)
-          for (int k = 0; k < RP; ++k) roots->r[(t - t0) * RP + k] = hr[(size_t)t * I + k];
-        ApplyD ad{fo->n_trees, t0, t1, li == 0 ? 1 : 0, li == n_launch - 1 ? 1 : 0, rd, ld, nd2, nw, fo->f0};
-        auto launch = [&](auto kern) {
-          BB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-          kern<<<gd, kApplyDRows, smemD, st>>>((const float*)Xd, n, d, ad, pd, fa, *roots);
-          BB_LAUNCH_CHECK();
-        };
+      roots = std::make_unique<ApplyRoots>();  // host staging; each launch copies its parameters
+      launch_rows = [=, &roots, &hr](int64_t r0, int64_t nr) {
+        const unsigned gd = (unsigned)ceil_div(nr, kApplyDRows);
+        for (int li = 0; li < n_launch; ++li) {
+          const int t0 = li * per_launch, t1 = std::min(fo->n_trees, t0 + per_launch);
+          for (int t = t0; t < t1; ++t)
+            for (int k = 0; k < RP; ++k) roots->r[(t - t0) * RP + k] = hr[(size_t)t * I + k];
+          ApplyD ad{fo->n_trees, t0, t1, li == 0 ? 1 : 0, li == n_launch - 1 ? 1 : 0, rd, ld, nd2, nw, fo->f0};
+          auto launch = [&](auto kern) {
+            BB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            kern<<<gd, kApplyDRows, smemD, st>>>((const float*)rows_at(r0), nr, d, ad, at(pd, r0), at(fa, r0), *roots);
+            BB_LAUNCH_CHECK();
+          };
 #define BB_APPLY_D(DD)                                      \
   do {                                                      \
     if (PL >= 3 && DD >= 3) launch(k_apply_d<DD, 3>);       \
@@ -2262,21 +2305,20 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
     else if (PL >= 1) launch(k_apply_d<DD, 1>);             \
     else launch(k_apply_d<DD, 0>);                          \
   } while (0)
-        switch (D) {
-          case 1: BB_APPLY_D(1); break;
-          case 2: BB_APPLY_D(2); break;
-          case 3: BB_APPLY_D(3); break;
-          case 4: BB_APPLY_D(4); break;
-          case 5: BB_APPLY_D(5); break;
-          default: BB_APPLY_D(6); break;
-        }
-      }
+          switch (D) {
+            case 1: BB_APPLY_D(1); break;
+            case 2: BB_APPLY_D(2); break;
+            case 3: BB_APPLY_D(3); break;
+            case 4: BB_APPLY_D(4); break;
+            case 5: BB_APPLY_D(5); break;
+            default: BB_APPLY_D(6); break;
+          }
 #undef BB_APPLY_D
-      BB_LAUNCH_CHECK();
-      BB_CUDA(cudaStreamSynchronize(st));  // host staging vectors
+        }
+      };
     } else if (x_dtype == BB_F32 && smem32 <= 200 * 1024) {
       // packed node records with float-ceiling thresholds (exact for float rows)
-      std::vector<int2> hn(TI);
+      hn.resize(TI);
       for (size_t e = 0; e < TI; ++e) {
         const double t = fo->threshold[e];
         float tf = (float)t;  // round-to-nearest, then step up if below t
@@ -2289,21 +2331,90 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
       if (TI) BB_CUDA(cudaMemcpyAsync(nd, hn.data(), TI * sizeof(int2), cudaMemcpyHostToDevice, st));
       ApplyF32 a32{fo->n_trees, fo->depth, I, N, nd, nw, fo->f0};
       BB_CUDA(cudaFuncSetAttribute(k_apply_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      k_apply_f32<<<(unsigned)ceil_div(n, kApplyRows), kApplyRows, smem32, st>>>((const float*)Xd, n, d, a32, pd, fd);
-      BB_LAUNCH_CHECK();
-      BB_CUDA(cudaStreamSynchronize(st));  // host staging vector hn
+      launch_rows = [=](int64_t r0, int64_t nr) {
+        k_apply_f32<<<(unsigned)ceil_div(nr, kApplyRows), kApplyRows, smem32, st>>>((const float*)rows_at(r0), nr, d, a32,
+                                                                                  at(pd, r0), at(fd, r0));
+        BB_LAUNCH_CHECK();
+      };
     } else if (x_dtype == BB_F32) {
       BB_CUDA(cudaFuncSetAttribute(k_apply<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      k_apply<float><<<grid, APPLY_ROWS, smem, st>>>((const float*)Xd, n, d, af, pd, fd);
+      launch_rows = [=](int64_t r0, int64_t nr) {
+        k_apply<float><<<(unsigned)ceil_div(nr, APPLY_ROWS), APPLY_ROWS, smem, st>>>((const float*)rows_at(r0), nr, d, af,
+                                                                                   at(pd, r0), at(fd, r0));
+        BB_LAUNCH_CHECK();
+      };
     } else {
       BB_CUDA(cudaFuncSetAttribute(k_apply<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      k_apply<double><<<grid, APPLY_ROWS, smem, st>>>((const double*)Xd, n, d, af, pd, fd);
+      launch_rows = [=](int64_t r0, int64_t nr) {
+        k_apply<double><<<(unsigned)ceil_div(nr, APPLY_ROWS), APPLY_ROWS, smem, st>>>((const double*)rows_at(r0), nr, d,
+                                                                                    af, at(pd, r0), at(fd, r0));
+        BB_LAUNCH_CHECK();
+      };
     }
-    BB_LAUNCH_CHECK();
-    if (!out_on_device) {
-      if (out_prob) BB_CUDA(cudaMemcpyAsync(out_prob, pd, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
-      if (out_score) BB_CUDA(cudaMemcpyAsync(out_score, fd, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    if (!pipe) {
+      launch_rows(0, n);
+      if (!out_on_device) {
+        if (out_prob) c.stage.d2h(out_prob, pd, (size_t)n * 8, st);
+        if (out_score) c.stage.d2h(out_score, fd, (size_t)n * 8, st);
+      }
+      BB_CUDA(cudaStreamSynchronize(st));
+      return;
     }
+    // ---- pipelined host rows: chunk i's upload (copy stream), kernels (st)
+    // and read-back (second copy stream) overlap chunks i+1 / i-1
+    constexpr int K = PinnedRing::kBufs;
+    const size_t out_chunk = HostStager::kChunk / 4;
+    int64_t rows_c = (int64_t)std::min(HostStager::kChunk / row_bytes, out_chunk / 8);
+    rows_c = std::max<int64_t>(1024, rows_c / 1024 * 1024);
+    HostStager& hs = c.stage;
+    hs.in.ensure(std::max(HostStager::kChunk, (size_t)rows_c * row_bytes));
+    if (out_prob) hs.out.ensure(std::max(HostStager::kChunk, (size_t)rows_c * 8));
+    if (out_score) hs.out2.ensure(std::max(HostStager::kChunk, (size_t)rows_c * 8));
+    PipeStreams ps(c.device);
+    const int64_t chunks = ceil_div(n, rows_c);
+    cudaEvent_t ev_k[K];
+    for (int b = 0; b < K; ++b) ev_k[b] = ps.ev[b];
+    auto drain = [&](int64_t j) {
+      const int b = (int)(j % K);
+      const int64_t r0 = j * rows_c, nr = std::min(rows_c, n - r0);
+      if (out_prob) {
+        BB_CUDA(cudaEventSynchronize(hs.out.ev(b)));
+        parallel_memcpy(out_prob + r0, hs.out.buf(b), (size_t)nr * 8);
+      }
+      if (out_score) {
+        BB_CUDA(cudaEventSynchronize(hs.out2.ev(b)));
+        parallel_memcpy(out_score + r0, hs.out2.buf(b), (size_t)nr * 8);
+      }
+    };
+    cudaEvent_t ev_setup = ps.ev[K];
+    BB_CUDA(cudaEventRecord(ev_setup, st));  // forest tables uploaded; Xd / pd allocated in stream order
+    BB_CUDA(cudaStreamWaitEvent(ps.s_in, ev_setup, 0));
+    BB_CUDA(cudaStreamWaitEvent(ps.s_out, ev_setup, 0));
+    for (int64_t i = 0; i < chunks; ++i) {
+      const int b = (int)(i % K);
+      const int64_t r0 = i * rows_c, nr = std::min(rows_c, n - r0);
+      if (i >= K) drain(i - K);  // frees out buffer b; in buffer b is guarded by its own event
+      BB_CUDA(cudaEventSynchronize(hs.in.ev(b)));
+      parallel_memcpy(hs.in.buf(b), (const char*)X + (size_t)r0 * row_bytes, (size_t)nr * row_bytes);
+      BB_CUDA(cudaMemcpyAsync((char*)Xd + (size_t)r0 * row_bytes, hs.in.buf(b), (size_t)nr * row_bytes,
+                              cudaMemcpyHostToDevice, ps.s_in));
+      BB_CUDA(cudaEventRecord(hs.in.ev(b), ps.s_in));
+      BB_CUDA(cudaStreamWaitEvent(st, hs.in.ev(b), 0));
+      launch_rows(r0, nr);
+      BB_CUDA(cudaEventRecord(ev_k[b], st));
+      BB_CUDA(cudaStreamWaitEvent(ps.s_out, ev_k[b], 0));
+      if (out_prob) {
+        BB_CUDA(cudaMemcpyAsync(hs.out.buf(b), pd + r0, (size_t)nr * 8, cudaMemcpyDeviceToHost, ps.s_out));
+        BB_CUDA(cudaEventRecord(hs.out.ev(b), ps.s_out));
+      }
+      if (out_score) {
+        BB_CUDA(cudaMemcpyAsync(hs.out2.buf(b), fd + r0, (size_t)nr * 8, cudaMemcpyDeviceToHost, ps.s_out));
+        BB_CUDA(cudaEventRecord(hs.out2.ev(b), ps.s_out));
+      }
+    }
+    for (int64_t j = std::max<int64_t>(0, chunks - K); j < chunks; ++j) drain(j);
+    BB_CUDA(cudaStreamSynchronize(ps.s_in));
+    BB_CUDA(cudaStreamSynchronize(ps.s_out));
     BB_CUDA(cudaStreamSynchronize(st));
   });
 }
@@ -2323,7 +2434,7 @@ int bb_bin(bb_ctx* ctx, const void* X, int32_t x_dtype, int64_t n, int32_t d, in
       using T = decltype(tag);
       using K = typename KeyOf<T>::K;
       T* Xd = A.alloc<T>((size_t)n * d);
-      BB_CUDA(cudaMemcpyAsync(Xd, X, (size_t)n * d * sizeof(T), cudaMemcpyHostToDevice, st));
+      c.stage.h2d(Xd, X, (size_t)n * d * sizeof(T), st);
       std::vector<unsigned long long> fin, nan_;
       unsigned long long* fdev = nullptr;
       K* keys = make_keys<T>(c, A, Xd, n, d, fin, nan_, &fdev);
@@ -2585,9 +2696,9 @@ int bb_roc_auc(bb_ctx* ctx, const double* scores, const int8_t* y01, const doubl
     double* p = A.alloc<double>(n);
     int8_t* y = A.alloc<int8_t>(n);
     double* wd = w ? A.alloc<double>(n) : nullptr;
-    BB_CUDA(cudaMemcpyAsync(p, scores, (size_t)n * 8, cudaMemcpyHostToDevice, c.stream));
+    c.stage.h2d(p, scores, (size_t)n * 8, c.stream);
     BB_CUDA(cudaMemcpyAsync(y, y01, (size_t)n, cudaMemcpyHostToDevice, c.stream));
-    if (w) BB_CUDA(cudaMemcpyAsync(wd, w, (size_t)n * 8, cudaMemcpyHostToDevice, c.stream));
+    if (w) c.stage.h2d(wd, w, (size_t)n * 8, c.stream);
     double ws, wb;
     *out_auc = auc_device(c, A, p, y, wd, n, &ws, &wb);
   });

@@ -164,8 +164,10 @@ def fit_forest(X, y, weights=None, config: FitConfig | None = None, *, forced_cu
         raise ValueError("X must be 2-d (n_events, n_features)")
     n, d = X.shape
     y = np.asarray(y)
-    labels = np.where(y > 0, 1, -1)
-    if not ((labels == 1).any() and (labels == -1).any()):
+    # labels = where(y > 0, 1, -1) (boosting.py:142-144) as one boolean pass
+    is_sig = y > 0
+    n_pos = int(np.count_nonzero(is_sig))
+    if not 0 < n_pos < is_sig.size:
         raise ValueError("training data must contain both classes")
     if y.shape != (n,):
         raise ValueError(f"y has shape {y.shape}, expected ({n},)")
@@ -178,7 +180,7 @@ def fit_forest(X, y, weights=None, config: FitConfig | None = None, *, forced_cu
             raise ValueError("user weights must be finite")
     if d == 0:
         raise ValueError("X must have at least one feature")
-    y01 = np.ascontiguousarray(labels > 0, dtype=np.int8)
+    y01 = np.ascontiguousarray(is_sig).view(np.int8)
 
     return _fit_native(X, xdt, False, n, d, y01, False, w, False, cfg, forced_cuts=forced_cuts,
                        return_leaves=return_leaves, return_scores=return_scores,

@@ -834,3 +834,41 @@ def test_fit_wide_levels_vs_fixed_point_oracle(levels, nan):
         np.testing.assert_array_equal(tr.cut_bin, ref.cut_bin[t])
         np.testing.assert_array_equal(forest.fit_info["leaves"][t], ref.leaves[t].astype(np.uint16))
         np.testing.assert_allclose(tr.node_weight, ref.node_weight[t], rtol=1e-12, atol=1e-15)
+
+
+# ------------------------------------------------------------------ host staging (csrc/bb_stage.cpp)
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_predict_pipelined_host_rows_match_plain_copy(dtype, monkeypatch):
+    """Pageable host rows go through the pinned-chunk pipeline (upload,
+    kernels and read-back per row chunk); the result must be identical to the
+    single plain copy (BB_NO_STAGING=1), including a ragged last chunk."""
+    rng = np.random.default_rng(11)
+    Xs = rng.normal(size=(20_000, 12))
+    y = (Xs[:, 0] + 0.5 * Xs[:, 3] + rng.normal(size=20_000) > 0).astype(int)
+    forest = fit_forest(Xs, y, None, FitConfig(n_trees=20, depth=3, binning_levels=6, seed=2))
+    n = 1_300_003  # several chunks of 349,184 (f32) / 174,080 (f64) rows + a ragged tail
+    X = rng.normal(size=(n, 12)).astype(dtype)
+    X[rng.random(n) < 0.01, 5] = np.nan
+    p1, F1 = predict_batch(forest, X, return_scores=True)
+    p1b = predict_batch(forest, X)
+    monkeypatch.setenv("BB_NO_STAGING", "1")
+    p0, F0 = predict_batch(forest, X, return_scores=True)
+    np.testing.assert_array_equal(F1, F0)
+    np.testing.assert_array_equal(p1, p0)
+    np.testing.assert_array_equal(p1b, p0)
+
+
+def test_fit_staged_upload_matches_plain_copy(monkeypatch):
+    """bb_fit uploads pageable rows/weights through the threaded pinned ring;
+    the forest must not depend on the transfer path."""
+    X, y, w, _ = make_config("cfg2", n=400_000)  # 400k x 40 f32 = 64 MB: 4 ring laps
+    cfg = FitConfig(n_trees=5, depth=3, binning_levels=8, seed=3)
+    a = fit_forest(X, y, w, cfg, return_scores=True)
+    monkeypatch.setenv("BB_NO_STAGING", "1")
+    b = fit_forest(X, y, w, cfg, return_scores=True)
+    assert a.f0 == b.f0
+    for ta, tb in zip(a.trees, b.trees):
+        np.testing.assert_array_equal(ta.feature, tb.feature)
+        np.testing.assert_array_equal(ta.cut_bin, tb.cut_bin)
+        np.testing.assert_array_equal(ta.node_weight, tb.node_weight)
+    np.testing.assert_array_equal(a.fit_info["scores"], b.fit_info["scores"])

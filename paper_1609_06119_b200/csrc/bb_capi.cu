@@ -625,12 +625,21 @@ static long long seg_slack(int n_prev) {
                              std::max<long long>(kAnchorSlackMin, (long long)std::ceil(k * seg_draws_sd(n_prev))));
 }
 
-static SegPlan build_seg_plan(int n, long long slack) {
+static SegPlan build_seg_plan(int n, long long slack, bool throughput_plan) {
   SegPlan P;
   if (n - 1 < kSegTail) return P;
   long long off = 0;
   SegTab t{};
-  while (seg_geom(n - 1, off, kSegTail, &t, 2 * slack)) {
+  // Plan shape.  Large fits (>= 4M rows) are bound by the tree kernels, which
+  // share the SMs with phase 1: shorter segments and 3-sd windows cut the
+  // phase-1 work (cfg3: 720 -> 663 ms per fit; a start outside its window only
+  // costs an exact walk of that segment).  Small fits are bound by the chain:
+  // long segments (fewer lookups) and 5-sd windows (no walks on the critical
+  // path; cfg2 at 3 sd: 101 -> 112 ms).  BB_SEG_LEN / BB_SEG_SD override.
+  const int max_len = getenv("BB_SEG_LEN") ? std::max(256, std::min(kSegMaxLen, atoi(getenv("BB_SEG_LEN"))))
+                                           : (throughput_plan ? 16384 : kSegMaxLen);
+  const double window_sd = getenv("BB_SEG_SD") ? atof(getenv("BB_SEG_SD")) : (throughput_plan ? 3.0 : (double)BB_SEG_WINDOW_SD);
+  while (seg_geom(n - 1, off, kSegTail, &t, 2 * slack, max_len, window_sd)) {
     t.rec_off = P.n_rec;
     const int ns = t.nA + t.nB;
     // phase-1 tasks (kernels_seg.cuh): one warp per piece whose window is a
@@ -748,7 +757,7 @@ struct MaskGen {
       // class cc's jobs follow jobs of the other class (sig, bkg alternate)
       slack[cc] = seg_slack(n[1 - cc]);
       exp_draws[cc] = n[cc] > 1 ? (long long)std::llround(seg_expected_draws(n[cc] - 1)) : 0;
-      const SegPlan P = build_seg_plan(n[cc], slack[cc]);
+      const SegPlan P = build_seg_plan(n[cc], slack[cc], (long long)n[0] + n[1] >= 4000000);
       S[cc] = (int)P.tab.size();
       n_tasks[cc] = (int)P.tasks.size();
       tab[cc] = A.alloc<SegTab>(std::max<size_t>(1, P.tab.size()));
@@ -775,7 +784,7 @@ struct MaskGen {
     BB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
     // BB_MASK_PRIO: 0 all mask streams high priority; 1 phase 1 high, emits /
     // resolution / draws normal; 2 all normal (the chain stream stays high)
-    static const int prio_mode = getenv("BB_MASK_PRIO") ? atoi(getenv("BB_MASK_PRIO")) : 0;
+    static const int prio_mode = getenv("BB_MASK_PRIO") ? atoi(getenv("BB_MASK_PRIO")) : 2;
     const int p_sb = prio_mode >= 2 ? lo_prio : hi_prio, p_rest = prio_mode >= 1 ? lo_prio : hi_prio;
     BB_CUDA(cudaStreamCreateWithPriority(&sb, cudaStreamNonBlocking, p_sb));
     BB_CUDA(cudaEventCreateWithFlags(&evA, cudaEventDisableTiming));
@@ -1310,7 +1319,19 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
     BB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kListThreads, smem));
     return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kListTileRows), (int64_t)std::max(1, per) * c.sm_count));
   };
-  const int gridR = resident(k_update_refresh<NodeT, CodeT>, 0);
+  // staged refresh walk (kernels_tree.cuh): the previous tree's distinct cut
+  // features' code columns in shared memory, 2048 rows per tile
+  static const bool stage_off = getenv("BB_REFRESH_STAGE") && atoi(getenv("BB_REFRESH_STAGE")) == 0;
+  int stage_slots = std::min(s.n_internal, s.d);
+  size_t stage_smem = (size_t)stage_slots * kListTileRows * sizeof(CodeT);
+  if (!lists || stage_off || s.n_internal > kStageNodes || stage_smem > 64 * 1024) {
+    stage_slots = 0;
+    stage_smem = 0;
+  }
+  if (stage_smem > 0)
+    BB_CUDA(cudaFuncSetAttribute(k_update_refresh<NodeT, CodeT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)stage_smem));
+  const int gridR = resident(k_update_refresh<NodeT, CodeT>, stage_smem);
   const int gridL = resident(k_advance<CodeT, NodeT>, 0);
   const int gridLL = resident(k_advance<CodeT, NodeT>, (size_t)32 * s.n_nodes);
   const int gridAL = std::max(2 * (1 << std::max(0, s.depth - 1)), resident(k_advance_list<CodeT>, 0));
@@ -1335,9 +1356,10 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         BB_CUDA(cudaEventRecord(tl.back(), st));  // ... and tree t's mask ready
       }
       if (lists) BB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)2 * s.n_nodes * 4, st));
-      k_update_refresh<NodeT, CodeT><<<gridR, kListThreads, 0, st>>>(
+      k_update_refresh<NodeT, CodeT><<<gridR, kListThreads, stage_smem, st>>>(
           n, s.n_sig, F, node, w_cb, q, mask, t > 0 ? ta.nw + (size_t)(t - 1) * s.n_nodes : nullptr, two_s, cnt,
-          lrow[0], lq[0], codes, s.d, code_off, ta, (lists && t > 0) ? t - 1 : -1, s.n_internal, s.depth);
+          lrow[0], lq[0], codes, s.d, code_off, ta, (lists && t > 0) ? t - 1 : -1, s.n_internal, s.depth,
+          stage_slots);
       BB_LAUNCH_CHECK();
       stats.launches += 1;
       for (int layer = 1; layer <= s.depth; ++layer) {
@@ -2083,7 +2105,16 @@ int bb_ctx_create(int32_t device, bb_ctx** out) {
     h->c.device = device;
     try {
       BB_CUDA(cudaSetDevice(device));
-      BB_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
+      // the fit's main stream runs above the mask streams (BB_MASK_PRIO=2
+      // default): the mask kernels backfill what the tree kernels leave, and a
+      // pending histogram CTA is not starved by queued phase-1 CTAs.
+      // cfg3: 728 -> 712 ms per fit; cfg2 unchanged (BB_MAIN_PRIO=0 BB_MASK_PRIO=0: the old order)
+      {
+        int lo_prio = 0, hi_prio = 0;
+        BB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+        const bool main_hi = !(getenv("BB_MAIN_PRIO") && atoi(getenv("BB_MAIN_PRIO")) == 0);
+        BB_CUDA(cudaStreamCreateWithPriority(&h->c.stream, cudaStreamNonBlocking, main_hi ? hi_prio : lo_prio));
+      }
       BB_CUDA(cudaDeviceGetAttribute(&h->c.sm_count, cudaDevAttrMultiProcessorCount, device));
       // keep freed stream-ordered allocations cached in the device pool: the
       // default threshold (0) returns them to the OS at every synchronisation,

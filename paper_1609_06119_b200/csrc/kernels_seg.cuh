@@ -127,8 +127,8 @@ __host__ __device__ inline double seg_expected_draws(int i0) {
 #ifndef BB_SEG_WINDOW_SD
 #define BB_SEG_WINDOW_SD 5.0
 #endif
-__host__ __device__ inline double seg_half_window(double p) {
-  return p <= 0.0 ? 0.0 : fmin(kSegHalfWindowCap, ceil(0.5 * BB_SEG_WINDOW_SD * sqrt(p)) + 16.0);
+__host__ __device__ inline double seg_half_window(double p, double window_sd = BB_SEG_WINDOW_SD) {
+  return p <= 0.0 ? 0.0 : fmin(kSegHalfWindowCap, ceil(0.5 * window_sd * sqrt(p)) + 16.0);
 }
 
 // Geometry of the segment at draw offset `off` of a stretch that starts at
@@ -137,12 +137,13 @@ __host__ __device__ inline double seg_half_window(double p) {
 // sub-window merge at most; kSegCrossLen draws where some start may reach
 // its band's last state, so the exact walk a crossing costs stays short).
 // Returns false once the window lies below floor_state.
-__host__ __device__ inline bool seg_geom(int i0, long long off, int floor_state, SegTab* t, long long slack = 0) {
+__host__ __device__ inline bool seg_geom(int i0, long long off, int floor_state, SegTab* t, long long slack = 0,
+                                         int max_len = kSegMaxLen, double window_sd = BB_SEG_WINDOW_SD) {
   // the job has consumed between off and off + slack draws at this segment
   const double pi = seg_pred_state(i0, (double)off);
   const double pl = seg_pred_state(i0, (double)(off + slack));
-  int lo = (int)fmax(1.0, floor(pl - seg_half_window((double)(off + slack))));
-  int hi = (int)fmin((double)i0, ceil(pi + seg_half_window((double)off)));
+  int lo = (int)fmax(1.0, floor(pl - seg_half_window((double)(off + slack), window_sd)));
+  int hi = (int)fmin((double)i0, ceil(pi + seg_half_window((double)off, window_sd)));
   if (hi < floor_state || lo > hi) return false;
   // stop once the state is below the floor with 3 sd to spare: the window cap
   // (4096) would otherwise keep hi above a low floor forever; a job that is
@@ -186,8 +187,8 @@ __host__ __device__ inline bool seg_geom(int i0, long long off, int floor_state,
   const unsigned M = smear_host((unsigned)(pi > 1.0 ? (int)pi : 1));
   const double L = 0.176 * ((double)M + 1.0);
   int Lp = 256;
-  while (Lp * 2 <= L && Lp < kSegMaxLen) Lp *= 2;
-  const double pe = seg_pred_state(i0, (double)(off + slack + Lp)) - seg_half_window((double)(off + slack + Lp));
+  while (Lp * 2 <= L && Lp < max_len) Lp *= 2;
+  const double pe = seg_pred_state(i0, (double)(off + slack + Lp)) - seg_half_window((double)(off + slack + Lp), window_sd);
   if (lo < bbA || pe < (double)bbA) Lp = Lp < kSegCrossLen ? Lp : kSegCrossLen;
   t->len = Lp;
   return true;

@@ -53,6 +53,7 @@ __global__ void k_iota(int* __restrict__ a, int64_t n) {
 // counter per key hit by every warp serialises at L2: 5x slower at cfg3).
 constexpr int kListTileRows = 2048;  // rows per CTA tile (512 threads x 4)
 constexpr int kListThreads = 512;
+constexpr int kStageNodes = 127;     // staged refresh walk: internal nodes (depth <= 7)
 
 // Leaf of row i in tree `tree` over its bin codes (trees.py:318-330): an
 // invalid node or a missing code stops the walk.
@@ -90,10 +91,52 @@ __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, i
                                                                 long long* __restrict__ lq,
                                                                 const CodeT* __restrict__ codes, int d, int code_off,
                                                                 TreeArrays ta, int walk_tree, int n_internal,
-                                                                int depth) {
+                                                                int depth, int stage_slots) {
   __shared__ int s_base[2];
   constexpr int R = kListTileRows / kListThreads;
   __shared__ int s_wc[2 * R * (kListThreads / 32)];  // per (class, row group, warp): count, then rank base
+  // staged walk (stage_slots > 0, n_internal <= kStageNodes): the code columns
+  // of the previous tree's distinct cut features are copied into shared
+  // memory per tile with coalesced 16-byte loads, and every row walks the tree
+  // there.  The gather walk below spends ~58 instructions and one dependent
+  // global load per level and row (cfg3: 247 us per tree, issue-bound).
+  extern __shared__ __align__(16) unsigned char s_cols[];  // [slot][kListTileRows] codes
+  __shared__ int s_rec[kStageNodes];    // node -> (slot << 16) | cut, -1: the walk stops
+  __shared__ int s_feat[kStageNodes];   // slot -> feature; scratch: node -> owner node
+  __shared__ int s_nslots;
+  const bool staged = stage_slots > 0 && nw_prev && walk_tree >= 0;
+  if (staged) {
+    const int64_t e0 = (int64_t)walk_tree * n_internal;
+    const int me = threadIdx.x;
+    int f = -1, cut = 0, owner = -1;
+    if (me < n_internal && __ldg(&ta.valid[e0 + me])) {
+      f = __ldg(&ta.feature[e0 + me]);
+      cut = __ldg(&ta.cut[e0 + me]);
+      owner = me;  // the first valid node with this feature owns its slot
+      for (int j = 0; j < me; ++j)
+        if (__ldg(&ta.valid[e0 + j]) && __ldg(&ta.feature[e0 + j]) == f) {
+          owner = j;
+          break;
+        }
+    }
+    if (me < n_internal) s_feat[me] = owner;
+    __syncthreads();
+    int slot = 0;
+    if (me < n_internal && owner >= 0)
+      for (int j = 0; j < owner; ++j) slot += (s_feat[j] == j);
+    if (me == 0) {
+      int c = 0;
+      for (int j = 0; j < n_internal; ++j) c += (s_feat[j] == j);
+      s_nslots = c;
+    }
+    __syncthreads();
+    if (me < n_internal) {
+      s_rec[me] = owner >= 0 ? ((slot << 16) | cut) : -1;
+      if (owner == me) s_feat[slot] = f;
+    }
+    __syncthreads();
+  }
+  const int64_t code_tiles = (n + kTile - 1) >> kTileLog;
   for (int64_t t0 = (int64_t)blockIdx.x * kListTileRows; t0 < n; t0 += (int64_t)gridDim.x * kListTileRows) {
     int loc[R];
     long long qs[R];
@@ -107,7 +150,40 @@ __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, i
       wr[k] = (in && w) ? w[i] : 1.0;
       mw[k] = in ? mask[i >> 5] : 0u;
     }
-    if (nw_prev && walk_tree >= 0) {
+    if (staged) {
+      constexpr int kVecPerCol = kTile * (int)sizeof(CodeT) / 16;               // 16-byte vectors per code-tile column
+      constexpr int kColsPerTile = kListTileRows / kTile;                        // code tiles per CTA tile
+      const int nvec = s_nslots * kColsPerTile * kVecPerCol;
+      const int64_t T0 = t0 >> kTileLog;
+      for (int idx = threadIdx.x; idx < nvec; idx += kListThreads) {
+        const int v = idx % kVecPerCol, h = (idx / kVecPerCol) % kColsPerTile, sl = idx / (kVecPerCol * kColsPerTile);
+        if (T0 + h >= code_tiles) continue;
+        const uint4* src = reinterpret_cast<const uint4*>(codes + ((T0 + h) * d + s_feat[sl]) * (int64_t)kTile) + v;
+        reinterpret_cast<uint4*>(s_cols)[(sl * kColsPerTile + h) * kVecPerCol + v] = __ldg(src);
+      }
+      __syncthreads();
+      const CodeT* sc = reinterpret_cast<const CodeT*>(s_cols);
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int r = k * kListThreads + threadIdx.x;
+        const int64_t i = t0 + r;
+        if (i < n) {
+          int nd = 0;
+          for (int l = 0; l < depth; ++l) {
+            const int rec = s_rec[nd];
+            if (rec < 0) break;
+            const int c = (int)sc[(rec >> 16) * kListTileRows + r] + code_off;
+            if (c == 0) break;
+            nd = 2 * nd + 1 + (c > (rec & 0xffff) ? 1 : 0);
+          }
+          fr[k] = __dadd_rn(fr[k], nw_prev[nd]);
+          F[i] = fr[k];
+        }
+      }
+      // s_cols is rewritten only after the list phase's barriers (or, without
+      // lists, after the barrier below)
+      if (!lrow) __syncthreads();
+    } else if (nw_prev && walk_tree >= 0) {
       // the R rows' walks in lockstep: independent gather chains overlap
       int nd[R];
       bool live[R];

@@ -110,6 +110,20 @@ def test_gpu_subsample_masks_large_blocks(seed, a, b, rate, T):
     _check_masks(seed, a, b, rate, T)
 
 
+# narrow windows and short segments: most starts miss their window, so the
+# chain falls back to exact walks all the time; the result must not change
+# (windows only decide how much work is parallel).  Also the throughput plan
+# (>= 4M rows: 16384-draw segments, 3-sd windows) on an uneven pair of blocks.
+@pytest.mark.parametrize("seed,a,b,rate,T,sd,seg_len", [(11, 300_000, 700_000, 0.5, 3, "0.5", "4096"),
+                                                        (12, 1_500_000, 900_000, 0.37, 2, "1.0", "16384"),
+                                                        (13, 3_100_000, 1_200_000, 0.5, 4, None, None)])
+def test_gpu_subsample_masks_window_misses(seed, a, b, rate, T, sd, seg_len, monkeypatch):
+    if sd is not None:
+        monkeypatch.setenv("BB_SEG_SD", sd)
+        monkeypatch.setenv("BB_SEG_LEN", seg_len)
+    _check_masks(seed, a, b, rate, T)
+
+
 def _check_masks(seed, a, b, rate, T):
     cfg = _lib.FitConfigC(**_lib.pcg_config(seed))
     words = (a + b + 31) // 32

@@ -193,6 +193,24 @@ struct Arena {
   }
 };
 
+// Kernel launch with programmatic stream serialization (common.cuh pdl_wait):
+// the kernel may be scheduled while the previous kernel of the stream drains.
+template <typename... KArgs, typename... Args>
+static void launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  BB_CUDA(cudaLaunchKernelEx(&cfg, kern, KArgs(std::forward<Args>(args))...));
+}
+
 static int grid_for(int64_t n, int threads, int sm, int per_sm = 8) {
   const int64_t want = ceil_div(n, threads);
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm * per_sm));
@@ -1265,7 +1283,10 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   const int lh_nw = (s.d <= 32 || !lh_nw16) ? 8 : 16;
   const int lh_pitch = s.d <= 32 ? 8 : 16;  // words per row of rc
   const int lh_groups = lh_nw == 8 && s.d > 32 ? 2 : 1;
-  const int lh_grid = lh_nw == 8 ? 2 * (c.sm_count - hist_reserve()) : c.sm_count - hist_reserve();
+  // BB_LH_WAVES > 1: that many CTAs per SM slot, scheduled as SMs come free
+  // (SMs held by mask CTAs take fewer histogram CTAs) at one more flush each
+  static const int lh_waves = getenv("BB_LH_WAVES") ? std::max(1, atoi(getenv("BB_LH_WAVES"))) : 1;
+  const int lh_grid = lh_waves * (lh_nw == 8 ? 2 * (c.sm_count - hist_reserve()) : c.sm_count - hist_reserve());
   const int hp_env = hist_path_env();
   const bool lists = sizeof(CodeT) == 1 && s.d <= 64 && s.depth <= 8 && (hp_env == 0 || hp_env == 5) &&
                      2 * (1 << (s.depth - 1)) <= lh_grid && !getenv("BB_HIST_WARP") && !getenv("BB_HIST_GLOBAL_GROUPS");
@@ -1337,8 +1358,16 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   const int gridAL = std::max(2 * (1 << std::max(0, s.depth - 1)), resident(k_advance_list<CodeT>, 0));
   const auto t0 = std::chrono::steady_clock::now();
   try {
+    // programmatic dependent launch on the tree loop's kernels (BB_PDL=0: plain launches)
+    // BB_PDL bits: 1 refresh, 2 histogram, 4 split, 8 advance, 16 node weights
+    const int pdl_mask = !lists ? 0 : (getenv("BB_PDL") ? atoi(getenv("BB_PDL")) : 0);
+    const bool pdl_r = pdl_mask & 1, pdl_h = pdl_mask & 2, pdl_s = pdl_mask & 4, pdl_a = pdl_mask & 8, pdl_n = pdl_mask & 16;
     const bool tl_on = getenv("BB_TIMELINE") != nullptr;  // debug: main-stream waits for masks
     std::vector<cudaEvent_t> tl;
+    if (getenv("BB_MASKS_FIRST") && s.T <= kSlots) {  // debug: every mask before the first tree (tree loop timed alone)
+      feed.ahead(s.T);
+      BB_CUDA(cudaDeviceSynchronize());
+    }
     for (int t = 0; t < s.T; ++t) {
       NvtxRange tree_range("tree");
       feed.ahead(t);
@@ -1356,10 +1385,9 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         BB_CUDA(cudaEventRecord(tl.back(), st));  // ... and tree t's mask ready
       }
       if (lists) BB_CUDA(cudaMemsetAsync(cnt, 0, (size_t)2 * s.n_nodes * 4, st));
-      k_update_refresh<NodeT, CodeT><<<gridR, kListThreads, stage_smem, st>>>(
-          n, s.n_sig, F, node, w_cb, q, mask, t > 0 ? ta.nw + (size_t)(t - 1) * s.n_nodes : nullptr, two_s, cnt,
-          lrow[0], lq[0], codes, s.d, code_off, ta, (lists && t > 0) ? t - 1 : -1, s.n_internal, s.depth,
-          stage_slots);
+      launch_k(pdl_r, k_update_refresh<NodeT, CodeT>, gridR, kListThreads, stage_smem, st, n, s.n_sig, F, node, w_cb, q,
+               mask, t > 0 ? ta.nw + (size_t)(t - 1) * s.n_nodes : nullptr, two_s, cnt, lrow[0], lq[0], codes, s.d,
+               code_off, ta, (lists && t > 0) ? t - 1 : -1, s.n_internal, s.depth, stage_slots);
       BB_LAUNCH_CHECK();
       stats.launches += 1;
       for (int layer = 1; layer <= s.depth; ++layer) {
@@ -1374,13 +1402,11 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         if (lists) {
           const int lb = (layer - 1) & 1;
           if (lh_nw == 8)
-            k_hist_list<8><<<lh_grid, kLhThreads, lh_smem_bytes<8>(), st>>>(rc, lrow[lb], lq[lb], cnt, layer, p.sib,
-                                                                          s.n_sig, s.d, s.B, code_off, p.nodes, hist,
-                                                                          lh_pitch, lh_groups);
+            launch_k(pdl_h, k_hist_list<8>, lh_grid, kLhThreads, lh_smem_bytes<8>(), st, rc, lrow[lb], lq[lb], cnt, layer,
+                     p.sib, s.n_sig, s.d, s.B, code_off, p.nodes, hist, lh_pitch, lh_groups);
           else
-            k_hist_list<16><<<lh_grid, kLhThreads, lh_smem_bytes<16>(), st>>>(rc, lrow[lb], lq[lb], cnt, layer, p.sib,
-                                                                            s.n_sig, s.d, s.B, code_off, p.nodes, hist,
-                                                                            16, 1);
+            launch_k(pdl_h, k_hist_list<16>, lh_grid, kLhThreads, lh_smem_bytes<16>(), st, rc, lrow[lb], lq[lb], cnt, layer,
+                     p.sib, s.n_sig, s.d, s.B, code_off, p.nodes, hist, 16, 1);
           BB_LAUNCH_CHECK();
         } else {
           launch_layer_hist<CodeT, NodeT>(p, fl_plans[layer], c.sm_count, codes, code_off, node, q, n, s.n_sig, s.d,
@@ -1394,18 +1420,17 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         const int n_fc_want = std::max(1, std::min(s.d, (2 * c.sm_count + nodes - 1) / nodes));
         const int fc_size = (int)ceil_div(s.d, n_fc_want);
         const int n_fc = (int)ceil_div(s.d, fc_size);
-        k_split<256><<<dim3(nodes, n_fc), 256, 0, st>>>(hist, s.d, s.B, p.start, nodes, fc_size,
-                                                       layer == s.depth ? 1 : 0, scale, t, s.n_internal, ta,
-                                                       bounds_dev, sc, par, p.sib,
-                                                       (layer < s.depth && plans[layer + 1].sib) ? 1 : 0);
+        launch_k(pdl_s && !c.comm.active(), k_split<256>, dim3(nodes, n_fc), 256, 0, st, hist, s.d, s.B, p.start, nodes,
+                 fc_size, layer == s.depth ? 1 : 0, scale, t, s.n_internal, ta, bounds_dev, sc, par, p.sib,
+                 (layer < s.depth && plans[layer + 1].sib) ? 1 : 0);
         BB_LAUNCH_CHECK();
         const bool last = layer == s.depth;
         if (last && p.sib) BB_CUDA(cudaMemsetAsync(hist, 0, (size_t)2 * nodes * s.d * s.B * 8, st));
         if (lists) {
           // the layer's listed active rows only (kernels_hist_list.cuh)
-          k_advance_list<CodeT><<<gridAL, kListThreads, 0, st>>>(
-              codes, s.d, code_off, lrow[(layer - 1) & 1], lq[(layer - 1) & 1], cnt, lrow[layer & 1], lq[layer & 1],
-              layer, t, s.n_internal, ta, last ? 1 : 0, s.n_sig, sums, s.n_nodes, F, w_cb, two_s);
+          launch_k(pdl_a, k_advance_list<CodeT>, gridAL, kListThreads, 0, st, codes, s.d, code_off, lrow[(layer - 1) & 1],
+                   lq[(layer - 1) & 1], cnt, lrow[layer & 1], lq[layer & 1], layer, t, s.n_internal, ta, last ? 1 : 0,
+                   s.n_sig, sums, s.n_nodes, q);
         } else {
           k_advance<CodeT, NodeT><<<last ? gridLL : gridL, kListThreads, last ? (size_t)32 * s.n_nodes : 0, st>>>(
               codes, s.d, code_off, node, n, s.n_sig, p.start, t, s.n_internal, ta, last ? 1 : 0, s.n_nodes, q, mask,
@@ -1415,8 +1440,8 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
       }
       BB_CUDA(cudaEventRecord(feed.freed[slot], st));
       c.comm.all_reduce(sums, (size_t)2 * s.n_nodes * 2, kNcclI64, kNcclSum, st);  // sharded fits
-      k_node_weights<<<1, 256, (size_t)2 * s.n_nodes * 2 * 8, st>>>(sums, s.n_nodes, s.depth, scale, cfg.shrinkage, t,
-                                                                    ta);
+      launch_k(pdl_n && !c.comm.active(), k_node_weights, 1, 256, (size_t)2 * s.n_nodes * 2 * 8, st, sums, s.n_nodes,
+               s.depth, scale, cfg.shrinkage, t, ta);
       BB_LAUNCH_CHECK();
       stats.launches += 1;
       if (out->leaves) {

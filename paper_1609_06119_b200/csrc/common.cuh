@@ -201,6 +201,15 @@ __host__ __device__ __forceinline__ int64_t code_index(int64_t row, int f, int d
   return ((row >> kTileLog) * d + f) * (int64_t)kTile + (row & (kTile - 1));
 }
 
+// ------------------------------------------- programmatic dependent launch
+// A kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization
+// (bb_capi.cu launch_k) may be scheduled while its predecessor in the stream
+// still runs: it must call pdl_wait() before touching anything the
+// predecessor wrote (no-op for a plain launch), and pdl_launch() lets its own
+// successor be scheduled early in turn.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // --------------------------------------------------------------- misc
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

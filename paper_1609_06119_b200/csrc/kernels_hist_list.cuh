@@ -123,6 +123,12 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
   __shared__ int s_ns;
   __shared__ int s_seg, s_r0, s_r1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // zero the histogram limbs (before the dependency wait: overlaps the
+  // previous kernel's tail under programmatic dependent launch)
+  for (int i = threadIdx.x; i < lh_hist_bytes<NW>() / 16; i += kLhThreads)
+    reinterpret_cast<uint4*>(hb)[i] = make_uint4(0u, 0u, 0u, 0u);
+  pdl_wait();
+  pdl_launch();
   if (threadIdx.x == 0) {
     const int ns = lh_segments(cnt, layer, sib, n_sig, segs);
     s_ns = ns;
@@ -151,9 +157,6 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
     s_r0 = (int)r0;
     s_r1 = (int)r1;
   }
-  // zero the histogram limbs
-  for (int i = threadIdx.x; i < lh_hist_bytes<NW>() / 16; i += kLhThreads)
-    reinterpret_cast<uint4*>(hb)[i] = make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
   if (s_seg < 0) return;
   const int4 sg = segs[s_seg];
@@ -327,8 +330,7 @@ __global__ void __launch_bounds__(kListThreads) k_advance_list(
     const CodeT* __restrict__ codes, int d, int code_off, const int* __restrict__ lrow_in,
     const long long* __restrict__ lq_in, int* __restrict__ cnt, int* __restrict__ lrow_out,
     long long* __restrict__ lq_out, int layer, int tree, int n_internal, TreeArrays ta, int last_layer,
-    long long n_sig, unsigned long long* __restrict__ sums, int n_nodes, const double* __restrict__ F,
-    const double* __restrict__ w, double two_s) {
+    long long n_sig, unsigned long long* __restrict__ sums, int n_nodes, const long long* __restrict__ q_resp) {
   constexpr int R = kListTileRows / kListThreads;
   constexpr int NWARP = kListThreads / 32;
   __shared__ int4 segs[kLhMaxSegs];
@@ -339,6 +341,8 @@ __global__ void __launch_bounds__(kListThreads) k_advance_list(
   __shared__ unsigned long long s_sum[3][2];  // (node, left, right) x (eff, resp), two's complement sums
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int start = (1 << (layer - 1)) - 1, nodes = start + 1;
+  pdl_wait();
+  pdl_launch();
   if (threadIdx.x == 0) {
     const int ns = lh_segments(cnt, layer, 0, n_sig, segs);
     long long Rt = 0;
@@ -405,11 +409,7 @@ __global__ void __launch_bounds__(kListThreads) k_advance_list(
       side[k] = rowv[k] < 0 ? -1 : (cv[k] == 0 ? 2 : (cv[k] > cut ? 1 : 0));
       if (side[k] == 2 || (last_layer && side[k] >= 0)) {
         // fixed-point (eff, resp) of the row at its final node (k_advance's last-layer rule)
-        const int64_t i = rowv[k];
-        const int lab = row_label(i, n_sig);
-        const double r = residual_of(F[i], lab);
-        const double wi = w ? w[i] : 1.0;
-        const long long qr = __double2ll_rn(__dmul_rn(__dmul_rn(wi, r), two_s));
+        const long long qr = __ldg(q_resp + rowv[k]);  // rint(w r 2^S), written by the refresh
         const int slot = side[k] == 2 ? 0 : 1 + side[k];
         acc_e[slot] += qv[k];
         acc_r[slot] += qr;

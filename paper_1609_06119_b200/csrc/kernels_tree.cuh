@@ -105,6 +105,8 @@ __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, i
   __shared__ int s_feat[kStageNodes];   // slot -> feature; scratch: node -> owner node
   __shared__ int s_nslots;
   const bool staged = stage_slots > 0 && nw_prev && walk_tree >= 0;
+  pdl_wait();
+  pdl_launch();
   if (staged) {
     const int64_t e0 = (int64_t)walk_tree * n_internal;
     const int me = threadIdx.x;
@@ -233,7 +235,10 @@ __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, i
         const double bw = boost_weight_of(r);
         const bool act = (mw[k] >> (i & 31)) & 1u;
         const long long qv = act ? __double2ll_rn(__dmul_rn(__dmul_rn(wr[k], bw), two_s)) : 0ll;
-        q[i] = qv;
+        // row-list fits keep q in the lists; q[] then holds the active rows'
+        // fixed-point RESPONSE rint(w r 2^S), read by k_advance_list when a row
+        // reaches its final node (trees.py:231-244) instead of a second exp
+        q[i] = !lrow ? qv : (act ? __double2ll_rn(__dmul_rn(__dmul_rn(wr[k], r), two_s)) : 0ll);
         if (walk_tree < 0) node[i] = 0;
         qs[k] = qv;
         if (lrow && act) loc[k] = i < n_sig ? 0 : 1;  // class, ranked below
@@ -767,6 +772,8 @@ __global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restric
                                                    int n_internal, TreeArrays ta, const double* __restrict__ bounds,
                                                    SplitScratch sc, unsigned long long* __restrict__ par_u, int sib,
                                                    int keep) {
+  pdl_wait();
+  pdl_launch();
   long long* hist = reinterpret_cast<long long*>(hist_u);
   long long* par = reinterpret_cast<long long*>(par_u);  // previous layer [2][nodes/2][d][B] (sib)
   const int node = blockIdx.x;
@@ -1169,6 +1176,8 @@ __global__ void __launch_bounds__(kListThreads, 4) k_advance(const CodeT* __rest
 __global__ void k_node_weights(unsigned long long* __restrict__ sums_u, int n_nodes, int depth, double scale,
                                double shrinkage, int tree, TreeArrays ta) {
   extern __shared__ long long s_tot[];  // [2 cls][n_nodes][2]
+  pdl_wait();
+  pdl_launch();
   long long* sums = reinterpret_cast<long long*>(sums_u);
   const int m = 2 * n_nodes * 2;
   for (int k = threadIdx.x; k < m; k += blockDim.x) {

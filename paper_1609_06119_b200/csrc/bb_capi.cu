@@ -1359,6 +1359,10 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   const auto t0 = std::chrono::steady_clock::now();
   try {
     // programmatic dependent launch on the tree loop's kernels (BB_PDL=0: plain launches)
+    // sibling subtraction mode: 2 = the smaller child is built (row-list fits on
+    // one device; a sharded fit builds the left child on every rank, the local
+    // counts would disagree), 1 = the left child (BB_SIB_SMALL=0)
+    const int sib_mode = lists && !c.comm.active() && !(getenv("BB_SIB_SMALL") && atoi(getenv("BB_SIB_SMALL")) == 0) ? 2 : 1;
     // BB_PDL bits: 1 refresh, 2 histogram, 4 split, 8 advance, 16 node weights
     const int pdl_mask = !lists ? 0 : (getenv("BB_PDL") ? atoi(getenv("BB_PDL")) : 0);
     const bool pdl_r = pdl_mask & 1, pdl_h = pdl_mask & 2, pdl_s = pdl_mask & 4, pdl_a = pdl_mask & 8, pdl_n = pdl_mask & 16;
@@ -1403,10 +1407,10 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
           const int lb = (layer - 1) & 1;
           if (lh_nw == 8)
             launch_k(pdl_h, k_hist_list<8>, lh_grid, kLhThreads, lh_smem_bytes<8>(), st, rc, lrow[lb], lq[lb], cnt, layer,
-                     p.sib, s.n_sig, s.d, s.B, code_off, p.nodes, hist, lh_pitch, lh_groups);
+                     p.sib ? sib_mode : 0, s.n_sig, s.d, s.B, code_off, p.nodes, hist, lh_pitch, lh_groups);
           else
             launch_k(pdl_h, k_hist_list<16>, lh_grid, kLhThreads, lh_smem_bytes<16>(), st, rc, lrow[lb], lq[lb], cnt, layer,
-                     p.sib, s.n_sig, s.d, s.B, code_off, p.nodes, hist, 16, 1);
+                     p.sib ? sib_mode : 0, s.n_sig, s.d, s.B, code_off, p.nodes, hist, 16, 1);
           BB_LAUNCH_CHECK();
         } else {
           launch_layer_hist<CodeT, NodeT>(p, fl_plans[layer], c.sm_count, codes, code_off, node, q, n, s.n_sig, s.d,
@@ -1421,8 +1425,8 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         const int fc_size = (int)ceil_div(s.d, n_fc_want);
         const int n_fc = (int)ceil_div(s.d, fc_size);
         launch_k(pdl_s && !c.comm.active(), k_split<256>, dim3(nodes, n_fc), 256, 0, st, hist, s.d, s.B, p.start, nodes,
-                 fc_size, layer == s.depth ? 1 : 0, scale, t, s.n_internal, ta, bounds_dev, sc, par, p.sib,
-                 (layer < s.depth && plans[layer + 1].sib) ? 1 : 0);
+                 fc_size, layer == s.depth ? 1 : 0, scale, t, s.n_internal, ta, bounds_dev, sc, par,
+                 p.sib ? sib_mode : 0, (layer < s.depth && plans[layer + 1].sib) ? 1 : 0, cnt);
         BB_LAUNCH_CHECK();
         const bool last = layer == s.depth;
         if (last && p.sib) BB_CUDA(cudaMemsetAsync(hist, 0, (size_t)2 * nodes * s.d * s.B * 8, st));
@@ -2681,7 +2685,7 @@ int bb_split(bb_ctx* ctx, const int64_t* hist, int32_t d, int32_t levels, int32_
     const int fc_size = (int)ceil_div(d, n_fc_want);
     const int n_fc = (int)ceil_div(d, fc_size);
     k_split<256><<<dim3(nodes, n_fc), 256, 0, st>>>(hd, d, B, start, nodes, fc_size, final_layer, std::ldexp(1.0, -shift),
-                                                   0, n_internal, ta, bd, sc, nullptr, 0, 0);
+                                                   0, n_internal, ta, bd, sc, nullptr, 0, 0, nullptr);
     BB_LAUNCH_CHECK();
     BB_CUDA(cudaMemcpyAsync(out_valid, ta.valid + start, nodes, cudaMemcpyDeviceToHost, st));
     BB_CUDA(cudaMemcpyAsync(out_feature, ta.feature + start, (size_t)nodes * 4, cudaMemcpyDeviceToHost, st));

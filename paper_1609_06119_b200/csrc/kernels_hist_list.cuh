@@ -70,6 +70,16 @@ __host__ __device__ constexpr int lh_smem_bytes() { return lh_hist_bytes<NW>() +
 // the parents' counts; the left child fills it from the start, the right
 // child (built only without sibling subtraction) from the end.
 // seg = {list offset, rows, layer-local node index, class}
+// Sibling subtraction over the SMALLER child: of the children (c, c + 1) of a
+// split node the histogram launch builds the one with fewer active rows
+// (right only if strictly fewer; counts are heap-indexed [node][class]).
+// Integer sums are exact, so parent - built is the sibling bit for bit.
+__device__ __forceinline__ bool lh_build_right(const int* __restrict__ cnt, int left_child) {
+  const int l = __ldcg(cnt + 2 * left_child) + __ldcg(cnt + 2 * left_child + 1);
+  const int r = __ldcg(cnt + 2 * left_child + 2) + __ldcg(cnt + 2 * left_child + 3);
+  return r < l;
+}
+
 __device__ __forceinline__ int lh_segments(const int* __restrict__ cnt, int layer, int sib, long long n_sig,
                                            int4* segs) {
   int ns = 0;
@@ -84,11 +94,12 @@ __device__ __forceinline__ int lh_segments(const int* __restrict__ cnt, int laye
     for (int p = ps; p < ps + np; ++p) {
       const int cp = __ldcg(cnt + 2 * p + k);
       const int c = 2 * p + 1;
-      segs[ns++] = make_int4(off, __ldcg(cnt + 2 * c + k), c - st, k);
-      if (!sib) {
-        const int cr = __ldcg(cnt + 2 * (c + 1) + k);
-        segs[ns++] = make_int4(off + cp - cr, cr, c + 1 - st, k);
-      }
+      const int cr = __ldcg(cnt + 2 * (c + 1) + k);
+      // sib == 2: the child with fewer active rows (both classes) is built, its
+      // sibling is parent - built in k_split (same rule there: lh_build_right)
+      const bool build_right = sib == 2 && lh_build_right(cnt, c);
+      if (!build_right) segs[ns++] = make_int4(off, __ldcg(cnt + 2 * c + k), c - st, k);
+      if (!sib || build_right) segs[ns++] = make_int4(off + cp - cr, cr, c + 1 - st, k);
       off += cp;
     }
   }

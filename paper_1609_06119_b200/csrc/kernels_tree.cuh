@@ -771,7 +771,7 @@ __global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restric
                                                    int nodes, int fc_size, int final_layer, double scale, int tree,
                                                    int n_internal, TreeArrays ta, const double* __restrict__ bounds,
                                                    SplitScratch sc, unsigned long long* __restrict__ par_u, int sib,
-                                                   int keep) {
+                                                   int keep, const int* __restrict__ cnt) {
   pdl_wait();
   pdl_launch();
   long long* hist = reinterpret_cast<long long*>(hist_u);
@@ -794,7 +794,15 @@ __global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restric
   // exact), or empty if the parent was not split.  A right child's CTA
   // zeroes the parent it consumed; a non-final layer keeps its histograms as
   // the next layer's parents, a final one is cleared by the host (memset).
-  const bool right = sib && (node & 1);
+  // sib == 2 (row-list fits): the child with fewer active rows was built
+  // (kernels_hist_list.cuh lh_build_right); `right` = this node is the derived one
+  bool built_right = false;
+  if (sib == 2) {
+    const int lc = start + (node & ~1);
+    built_right = (__ldcg(cnt + 2 * lc + 2) + __ldcg(cnt + 2 * lc + 3)) < (__ldcg(cnt + 2 * lc) + __ldcg(cnt + 2 * lc + 1));
+  }
+  const bool right = sib && (((node & 1) != 0) != built_right);
+  const int sibn = node ^ 1;  // the built sibling of a derived node
   const int pnode = node >> 1, pnodes = nodes >> 1;
   const bool pvalid = right && ta.valid[(int64_t)tree * n_internal + ((start - 1) >> 1) + pnode] != 0;
   if (per > 8) {
@@ -806,8 +814,8 @@ __global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restric
     for (int f = fbeg; f < fend; ++f) {
       long long* hs = hist + ((int64_t)node * d + f) * B;
       long long* hb = hist + (((int64_t)nodes + node) * d + f) * B;
-      long long* ls = right ? hist + ((int64_t)(node - 1) * d + f) * B : nullptr;
-      long long* lb = right ? hist + (((int64_t)nodes + node - 1) * d + f) * B : nullptr;
+      long long* ls = right ? hist + ((int64_t)sibn * d + f) * B : nullptr;
+      long long* lb = right ? hist + (((int64_t)nodes + sibn) * d + f) * B : nullptr;
       long long* ps = right ? par + ((int64_t)pnode * d + f) * B : nullptr;
       long long* pb = right ? par + (((int64_t)pnodes + pnode) * d + f) * B : nullptr;
       auto val = [&](int c, long long& a, long long& b) {
@@ -902,8 +910,8 @@ __global__ void __launch_bounds__(THREADS) k_split(unsigned long long* __restric
     long long ts = 0, tb = 0;
     const int c0 = threadIdx.x * per;
     if (right) {
-      long long* ls = hist + ((int64_t)(node - 1) * d + f) * B;
-      long long* lb = hist + (((int64_t)nodes + node - 1) * d + f) * B;
+      long long* ls = hist + ((int64_t)sibn * d + f) * B;
+      long long* lb = hist + (((int64_t)nodes + sibn) * d + f) * B;
       long long* ps = par + ((int64_t)pnode * d + f) * B;
       long long* pb = par + (((int64_t)pnodes + pnode) * d + f) * B;
       for (int j = 0; j < per; ++j) {

@@ -96,6 +96,14 @@ __global__ void k_select_init(SelectState<K> st, int B) {
   }
 }
 
+// 16-bit hash of a group prefix for k_select_hist's membership filter
+template <typename K>
+__device__ __forceinline__ unsigned int select_filter_hash(K pre) {
+  unsigned int x = (unsigned int)pre;
+  if (sizeof(K) == 8) x ^= (unsigned int)((unsigned long long)pre >> 32) * 0x85EBCA6Bu;
+  return (x * 0x9E3779B1u) >> 16;
+}
+
 // Histogram one digit.  resolved = number of high key bits already fixed
 // for every group; db = digit bits this pass.
 template <typename K>
@@ -127,31 +135,79 @@ __global__ void __launch_bounds__(256) k_select_hist(const K* __restrict__ keys,
     key_pinf = (K)0xFFF0000000000000ull;
   }
   const unsigned int dmask = (1u << db) - 1u;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const K k = col[i];
-    int g = -1;
-    if (k > key_ninf && k < key_pinf) {
-      if (resolved == 0) {
-        g = 0;
-      } else {
-        const K pre = k >> (KB - resolved);
-        int lo = 0, hi = ng - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (__ldg(&gp[mid]) < pre) lo = mid + 1; else hi = mid;
-        }
-        if (__ldg(&gp[lo]) == pre) g = lo;
-      }
+  // Group lookup.  Up to 12 resolved bits: an exact bitmap of the groups'
+  // prefixes, the group index is the prefix's rank among the set bits (groups
+  // are sorted by prefix).  Beyond: a 64K-bit one-hash filter rejects the keys
+  // of no group (from the third pass on > 99 % of a column: only the target
+  // order statistics' buckets are refined) before the binary search.
+  __shared__ unsigned int s_bm[2048];
+  __shared__ int s_pre[128];
+  const bool exact = resolved > 0 && resolved <= 12;
+  if (resolved > 0) {
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) s_bm[i] = 0u;
+    __syncthreads();
+    for (int i = threadIdx.x; i < ng; i += blockDim.x) {
+      const K pre = __ldg(&gp[i]);
+      const unsigned int h = exact ? (unsigned int)pre : select_filter_hash<K>(pre);
+      atomicOr(&s_bm[h >> 5], 1u << (h & 31));
     }
-    const unsigned int digit = (g >= 0) ? (unsigned int)((k >> (KB - resolved - db)) & dmask) : 0u;
-    const int bin = (g >= 0) ? (g << db) + (int)digit : -1;
-    // warp aggregation of equal bins (heavy ties: discrete features)
-    const unsigned int active = __activemask();
-    const unsigned int peers = __match_any_sync(active, bin);
-    const int leader = __ffs(peers) - 1;
-    if (bin >= 0 && (threadIdx.x & 31) == leader) {
-      const unsigned int c = __popc(peers);
-      if (use_smem) atomicAdd(&s_hist[bin], c); else atomicAdd(&gh[bin], c);
+    __syncthreads();
+    if (exact && threadIdx.x < 128) {
+      int c = 0;
+      for (int w = 0; w < (int)threadIdx.x; ++w) c += __popc(s_bm[w]);
+      s_pre[threadIdx.x] = c;
+    }
+    __syncthreads();
+  }
+  // kSelU keys per thread and round, loaded before any is processed: one
+  // 4-byte load in flight per thread bounds a full-occupancy SM at ~10 GB/s
+  // (measured 0.8 TB/s per pass on the whole GPU before)
+  constexpr int kSelU = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); w0 < n; w0 += kSelU * stride) {
+    K kk[kSelU];
+#pragma unroll
+    for (int u = 0; u < kSelU; ++u) {
+      const int64_t i = w0 + u * stride + lane;
+      kk[u] = i < n ? col[i] : key_pinf;  // out of range: treated as non-finite (no group)
+    }
+#pragma unroll
+    for (int u = 0; u < kSelU; ++u) {
+      if (w0 + u * stride >= n) break;  // warp-uniform
+      const K k = kk[u];
+      int g = -1;
+      if (k > key_ninf && k < key_pinf) {
+        if (resolved == 0) {
+          g = 0;
+        } else if (exact) {
+          const unsigned int pre = (unsigned int)(k >> (KB - resolved));
+          const unsigned int w = s_bm[pre >> 5], b = pre & 31u;
+          if ((w >> b) & 1u) g = s_pre[pre >> 5] + __popc(w & ((1u << b) - 1u));
+        } else {
+          const K pre = k >> (KB - resolved);
+          const unsigned int h = select_filter_hash<K>(pre);
+          if ((s_bm[h >> 5] >> (h & 31)) & 1u) {
+            int lo = 0, hi = ng - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (__ldg(&gp[mid]) < pre) lo = mid + 1; else hi = mid;
+            }
+            if (__ldg(&gp[lo]) == pre) g = lo;
+          }
+        }
+      }
+      const unsigned int digit = (g >= 0) ? (unsigned int)((k >> (KB - resolved - db)) & dmask) : 0u;
+      const int bin = (g >= 0) ? (g << db) + (int)digit : -1;
+      // warp aggregation of equal bins (heavy ties: discrete features)
+      if (__any_sync(0xffffffffu, bin >= 0)) {
+        const unsigned int peers = __match_any_sync(0xffffffffu, bin);
+        const int leader = __ffs(peers) - 1;
+        if (bin >= 0 && lane == leader) {
+          const unsigned int c = __popc(peers);
+          if (use_smem) atomicAdd(&s_hist[bin], c); else atomicAdd(&gh[bin], c);
+        }
+      }
     }
   }
   if (use_smem) {
@@ -431,22 +487,38 @@ __global__ void __launch_bounds__(256) k_codes(const K* __restrict__ keys, int64
     __syncthreads();
   }
   const K* col = keys + (int64_t)f * n;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const K k = col[i];
-    int code;
-    if (k == 0) {
-      code = 0;  // NaN
-    } else {
-      // upper_bound: number of boundary keys <= k
-      int lo = 0, hi = nt;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (sb[mid] <= k) lo = mid + 1; else hi = mid;
-      }
-      code = lo + 1;
+  // kCodeU rows per thread and round: their key / position loads are issued
+  // together and the upper-bound searches (fixed step count, branch-free) run
+  // in lockstep, so several memory and shared-memory latencies overlap
+  constexpr int kCodeU = 4;
+  int top = 1;
+  while (top <= nt) top <<= 1;  // smallest power of two > nt
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += kCodeU * stride) {
+    K kk[kCodeU];
+    int64_t pp[kCodeU];
+    int lo[kCodeU];
+#pragma unroll
+    for (int u = 0; u < kCodeU; ++u) {
+      const int64_t i = i0 + u * stride;
+      kk[u] = i < n ? col[i] : (K)0;
+      pp[u] = i < n ? (int64_t)pos[i] : -1;
+      lo[u] = 0;
     }
-    const int64_t p = pos[i];
-    codes[tiled ? code_index(p, f, d) : (int64_t)f * code_stride + p] = (CodeT)(code - code_off);
+    // upper_bound: number of boundary keys <= k
+    for (int step = top >> 1; step >= 1; step >>= 1) {
+#pragma unroll
+      for (int u = 0; u < kCodeU; ++u) {
+        const int m = lo[u] + step - 1;
+        if (m < nt && sb[m] <= kk[u]) lo[u] += step;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kCodeU; ++u) {
+      if (pp[u] < 0) continue;
+      const int code = kk[u] == 0 ? 0 : lo[u] + 1;  // key 0: NaN
+      codes[tiled ? code_index(pp[u], f, d) : (int64_t)f * code_stride + pp[u]] = (CodeT)(code - code_off);
+    }
   }
 }
 

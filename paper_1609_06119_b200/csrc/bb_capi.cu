@@ -651,11 +651,13 @@ static SegPlan build_seg_plan(int n, long long slack, bool throughput_plan) {
   // Plan shape.  Large fits (>= 4M rows) are bound by the tree kernels, which
   // share the SMs with phase 1: shorter segments and 3-sd windows cut the
   // phase-1 work (cfg3: 720 -> 663 ms per fit; a start outside its window only
-  // costs an exact walk of that segment).  Small fits are bound by the chain:
-  // long segments (fewer lookups) and 5-sd windows (no walks on the critical
-  // path; cfg2 at 3 sd: 101 -> 112 ms).  BB_SEG_LEN / BB_SEG_SD override.
+  // costs an exact walk of that segment).  Small fits are bound by the mask
+  // pipeline's latency: 5-sd windows (no exact walks on the critical
+  // path; cfg2 at 3 sd: 101 -> 112 ms) of 8192 draws (cfg2: 60 ms per fit; 67 ms
+  // at 16384 and 101 ms at 32768 draws, whose phase-1 warps the chain then
+  // waits for).  BB_SEG_LEN / BB_SEG_SD override.
   const int max_len = getenv("BB_SEG_LEN") ? std::max(256, std::min(kSegMaxLen, atoi(getenv("BB_SEG_LEN"))))
-                                           : (throughput_plan ? 16384 : kSegMaxLen);
+                                           : (throughput_plan ? 16384 : 8192);
   const double window_sd = getenv("BB_SEG_SD") ? atof(getenv("BB_SEG_SD")) : (throughput_plan ? 3.0 : (double)BB_SEG_WINDOW_SD);
   while (seg_geom(n - 1, off, kSegTail, &t, 2 * slack, max_len, window_sd)) {
     t.rec_off = P.n_rec;

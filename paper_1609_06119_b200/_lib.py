@@ -16,9 +16,10 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# BB_LIB_VARIANT=check loads the device-bounds-check build (make -C csrc check)
-LIB_PATH = os.path.join(_HERE, "libfastbdt_b200_check.so" if os.environ.get("BB_LIB_VARIANT") == "check"
-                        else "libfastbdt_b200.so")
+# BB_LIB_VARIANT=check loads the device-bounds-check build (make -C csrc check);
+# any other value loads libfastbdt_b200_<value>.so (tuning builds)
+_VARIANT = os.environ.get("BB_LIB_VARIANT")
+LIB_PATH = os.path.join(_HERE, f"libfastbdt_b200_{_VARIANT}.so" if _VARIANT else "libfastbdt_b200.so")
 
 BB_OK, BB_EINVAL, BB_ECUDA, BB_ESTATE = 0, 1, 2, 3
 BB_F32, BB_F64 = 0, 1

@@ -52,7 +52,10 @@ constexpr int kSegCrossLen = 1024; // draws per segment in band-crossing zones
 constexpr int kAnchorSlackMin = 512;   // a job's segments start at its predicted first draw + a slack of
 constexpr int kAnchorSlackMax = 4000;  // 5 sd of a job's draw count, clamped to this range
 constexpr int kSub = 512;          // states per phase-1 sub-window (one warp)
-constexpr int kSubPerCta = 8;      // sub-windows per phase-1 CTA (= warps per k_seg_pass CTA)
+#ifndef BB_SUB_PER_CTA
+#define BB_SUB_PER_CTA 8
+#endif
+constexpr int kSubPerCta = BB_SUB_PER_CTA;      // sub-windows per phase-1 CTA (= warps per k_seg_pass CTA)
 constexpr int kSegMaxSub = 64;     // sub-windows per segment (max)
 // half-window cap (states): 5 sd of a 29M-draw stretch (a 20M-row class
 // block, cfg5) is ~13.5k states; with the cap below that, a deviated path

@@ -106,6 +106,63 @@ __device__ __forceinline__ int lh_segments(const int* __restrict__ cnt, int laye
   return ns;
 }
 
+// CTA -> (segment, row range).  The G CTAs of a launch are split over the
+// non-empty segments so that the LARGEST per-CTA row count is minimal: k_s =
+// ceil(rows_s / T) CTAs for the smallest T with sum_s k_s <= G (binary search;
+// needs G >= the number of non-empty segments, which the host guarantees).
+// The first version gave 1 + floor((G - E) rows_s / R) CTAs: up to one CTA per
+// segment stayed idle and mid-sized segments ran up to ~30 % over the mean.
+// Called by all 32 lanes of warp 0; out = {segment or -1, r0, r1}.
+__device__ __forceinline__ void lh_assign(const int4* __restrict__ segs, int ns, int G, int cta, int lane, int* out) {
+  constexpr int Q = kLhMaxSegs / 32;
+  const unsigned FULL = 0xffffffffu;
+  int rows[Q];
+  int mx = 0, ne = 0;
+  long long tot = 0;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int s = lane + 32 * q;
+    rows[q] = s < ns ? segs[s].y : 0;
+    mx = max(mx, rows[q]);
+    tot += rows[q];
+    ne += rows[q] > 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+    tot += __shfl_xor_sync(FULL, tot, o);
+    ne += __shfl_xor_sync(FULL, ne, o);
+  }
+  if (lane == 0) out[0] = -1;
+  if (ne == 0) return;
+  const int nq = (ns + 31) >> 5;
+  int lo = (int)max(1ll, (tot + G - 1) / G), hi = mx;
+  while (lo < hi) {
+    const int mid = (int)(((long long)lo + hi) >> 1);
+    int c = 0;
+    for (int q = 0; q < nq; ++q) c += (rows[q] + mid - 1) / mid;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    if (c <= G) hi = mid; else lo = mid + 1;
+  }
+  const int T = lo;
+  int base = 0;
+  for (int q = 0; q < nq; ++q) {
+    const int k = (rows[q] + T - 1) / T;
+    int incl = k;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int first = base + incl - k;
+    if (k > 0 && cta >= first && cta < first + k) {
+      const int j = cta - first;
+      out[0] = lane + 32 * q;
+      out[1] = (int)((long long)rows[q] * j / k);
+      out[2] = (int)((long long)rows[q] * (j + 1) / k);
+    }
+    base += __shfl_sync(FULL, incl, 31);
+  }
+}
+
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -132,7 +189,7 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
   uint32_t* bufs = reinterpret_cast<uint32_t*>(lh_sm + lh_hist_bytes<NW>());  // [warp][2][32 rows][NW]
   int4* segs = reinterpret_cast<int4*>(lh_sm + lh_hist_bytes<NW>() + lh_buf_bytes<NW>());
   __shared__ int s_ns;
-  __shared__ int s_seg, s_r0, s_r1;
+  __shared__ int s_asg[3];  // segment, first row, end row of this CTA
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // zero the histogram limbs (before the dependency wait: overlaps the
   // previous kernel's tail under programmatic dependent launch)
@@ -140,39 +197,14 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
     reinterpret_cast<uint4*>(hb)[i] = make_uint4(0u, 0u, 0u, 0u);
   pdl_wait();
   pdl_launch();
-  if (threadIdx.x == 0) {
-    const int ns = lh_segments(cnt, layer, sib, n_sig, segs);
-    s_ns = ns;
-    // CTAs per non-empty segment: 1 + share of the rest by rows
-    long long R = 0;
-    int E = 0;
-    for (int s = 0; s < ns; ++s) {
-      R += segs[s].y;
-      E += segs[s].y > 0;
-    }
-    const int G = nctas, Gp = G > E ? G - E : 0;
-    int cum = 0, seg = -1;
-    long long r0 = 0, r1 = 0;
-    for (int s = 0; s < ns && seg < 0; ++s) {
-      if (segs[s].y == 0) continue;
-      const int k = 1 + (int)((long long)Gp * segs[s].y / (R > 0 ? R : 1));
-      if (cta < cum + k) {
-        const int j = cta - cum;
-        seg = s;
-        r0 = (long long)segs[s].y * j / k;
-        r1 = (long long)segs[s].y * (j + 1) / k;
-      }
-      cum += k;
-    }
-    s_seg = seg;
-    s_r0 = (int)r0;
-    s_r1 = (int)r1;
-  }
+  if (threadIdx.x == 0) s_ns = lh_segments(cnt, layer, sib, n_sig, segs);
   __syncthreads();
-  if (s_seg < 0) return;
-  const int4 sg = segs[s_seg];
+  if (warp == 0) lh_assign(segs, s_ns, nctas, cta, lane, s_asg);
+  __syncthreads();
+  if (s_asg[0] < 0) return;
+  const int4 sg = segs[s_asg[0]];
   BB_DCHECK(sg.x >= 0 && sg.y >= 0 && sg.z >= 0 && sg.z < nodes && (sg.w == 0 || sg.w == 1));
-  const int r_begin = s_r0, r_end = s_r1;
+  const int r_begin = s_asg[1], r_end = s_asg[2];
   const int* lr = lrow + sg.x;
   const long long* lqs = lq + sg.x;
   uint32_t* wbuf = bufs + warp * 32 * NW;
@@ -345,7 +377,7 @@ __global__ void __launch_bounds__(kListThreads) k_advance_list(
   constexpr int R = kListTileRows / kListThreads;
   constexpr int NWARP = kListThreads / 32;
   __shared__ int4 segs[kLhMaxSegs];
-  __shared__ int s_seg, s_r0, s_r1;
+  __shared__ int s_ns, s_asg[3];
   __shared__ int s_reg[2 * kAdvMaxNodes];
   __shared__ int s_wc[2 * R * NWARP];  // per (child side, row group, warp): count, then rank base
   __shared__ int s_base[2];
@@ -355,30 +387,7 @@ __global__ void __launch_bounds__(kListThreads) k_advance_list(
   pdl_wait();
   pdl_launch();
   if (threadIdx.x == 0) {
-    const int ns = lh_segments(cnt, layer, 0, n_sig, segs);
-    long long Rt = 0;
-    int E = 0;
-    for (int q = 0; q < ns; ++q) {
-      Rt += segs[q].y;
-      E += segs[q].y > 0;
-    }
-    const int G = gridDim.x, Gp = G > E ? G - E : 0;
-    int cum = 0, seg = -1;
-    long long r0 = 0, r1 = 0;
-    for (int q = 0; q < ns && seg < 0; ++q) {
-      if (segs[q].y == 0) continue;
-      const int k = 1 + (int)((long long)Gp * segs[q].y / (Rt > 0 ? Rt : 1));
-      if ((int)blockIdx.x < cum + k) {
-        const int j = (int)blockIdx.x - cum;
-        seg = q;
-        r0 = (long long)segs[q].y * j / k;
-        r1 = (long long)segs[q].y * (j + 1) / k;
-      }
-      cum += k;
-    }
-    s_seg = seg;
-    s_r0 = (int)r0;
-    s_r1 = (int)r1;
+    s_ns = lh_segments(cnt, layer, 0, n_sig, segs);
     if (!last_layer) {  // regions of the next layer's lists: class-major prefix of this layer's counts
       int off = 0;
       for (int k = 0; k < 2; ++k)
@@ -390,8 +399,11 @@ __global__ void __launch_bounds__(kListThreads) k_advance_list(
   }
   if (threadIdx.x < 6) s_sum[threadIdx.x >> 1][threadIdx.x & 1] = 0ull;
   __syncthreads();
-  if (s_seg < 0) return;
-  const int4 sg = segs[s_seg];
+  if (warp == 0) lh_assign(segs, s_ns, (int)gridDim.x, (int)blockIdx.x, lane, s_asg);
+  __syncthreads();
+  if (s_asg[0] < 0) return;
+  const int s_r0 = s_asg[1], s_r1 = s_asg[2];
+  const int4 sg = segs[s_asg[0]];
   const int c = start + sg.z, cls = sg.w;
   const int64_t e_tc = (int64_t)tree * n_internal + c;
   const bool vld = ta.valid[e_tc] != 0;

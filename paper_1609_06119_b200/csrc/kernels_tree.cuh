@@ -155,31 +155,59 @@ __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, i
     if (staged) {
       constexpr int kVecPerCol = kTile * (int)sizeof(CodeT) / 16;               // 16-byte vectors per code-tile column
       constexpr int kColsPerTile = kListTileRows / kTile;                        // code tiles per CTA tile
-      const int nvec = s_nslots * kColsPerTile * kVecPerCol;
       const int64_t T0 = t0 >> kTileLog;
-      for (int idx = threadIdx.x; idx < nvec; idx += kListThreads) {
-        const int v = idx % kVecPerCol, h = (idx / kVecPerCol) % kColsPerTile, sl = idx / (kVecPerCol * kColsPerTile);
-        if (T0 + h >= code_tiles) continue;
-        const uint4* src = reinterpret_cast<const uint4*>(codes + ((T0 + h) * d + s_feat[sl]) * (int64_t)kTile) + v;
-        reinterpret_cast<uint4*>(s_cols)[(sl * kColsPerTile + h) * kVecPerCol + v] = __ldg(src);
+      // thread -> (vector v of code-tile column h); the slot advances by a
+      // constant per round (kListThreads is a multiple of the vectors per slot)
+      constexpr int kVecPerSlot = kVecPerCol * kColsPerTile;
+      static_assert(kListThreads % kVecPerSlot == 0 || kVecPerSlot % kListThreads == 0, "staging map");
+      if (kListThreads >= kVecPerSlot) {
+        constexpr int kSlotStep = kListThreads / kVecPerSlot > 0 ? kListThreads / kVecPerSlot : 1;
+        const int v = threadIdx.x % kVecPerCol, h = (threadIdx.x / kVecPerCol) % kColsPerTile;
+        if (T0 + h < code_tiles) {
+          const uint4* col0 = reinterpret_cast<const uint4*>(codes + (T0 + h) * d * (int64_t)kTile) + v;
+          uint4* dst0 = reinterpret_cast<uint4*>(s_cols) + h * kVecPerCol + v;
+          const int ns = s_nslots;
+          for (int sl = threadIdx.x / kVecPerSlot; sl < ns; sl += kSlotStep)
+            dst0[sl * kVecPerSlot] = __ldg(col0 + s_feat[sl] * (kTile * (int)sizeof(CodeT) / 16));
+        }
+      } else {
+        const int nvec = s_nslots * kVecPerSlot;
+        for (int idx = threadIdx.x; idx < nvec; idx += kListThreads) {
+          const int v = idx % kVecPerCol, h = (idx / kVecPerCol) % kColsPerTile, sl = idx / kVecPerSlot;
+          if (T0 + h >= code_tiles) continue;
+          const uint4* src = reinterpret_cast<const uint4*>(codes + ((T0 + h) * d + s_feat[sl]) * (int64_t)kTile) + v;
+          reinterpret_cast<uint4*>(s_cols)[(sl * kColsPerTile + h) * kVecPerCol + v] = __ldg(src);
+        }
       }
       __syncthreads();
       const CodeT* sc = reinterpret_cast<const CodeT*>(s_cols);
+      {
+        // the R rows' walks in lockstep (branch-free: a stopped row keeps its
+        // node), so the shared-memory latencies of a level overlap
+        int nd[R];
+        bool live[R];
 #pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const int r = k * kListThreads + threadIdx.x;
-        const int64_t i = t0 + r;
-        if (i < n) {
-          int nd = 0;
-          for (int l = 0; l < depth; ++l) {
-            const int rec = s_rec[nd];
-            if (rec < 0) break;
-            const int c = (int)sc[(rec >> 16) * kListTileRows + r] + code_off;
-            if (c == 0) break;
-            nd = 2 * nd + 1 + (c > (rec & 0xffff) ? 1 : 0);
+        for (int k = 0; k < R; ++k) {
+          nd[k] = 0;
+          live[k] = true;
+        }
+        for (int l = 0; l < depth; ++l) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            const int r = k * kListThreads + threadIdx.x;
+            const int rec = s_rec[nd[k]];
+            const int c = (int)sc[(max(rec, 0) >> 16) * kListTileRows + r] + code_off;
+            live[k] = live[k] && rec >= 0 && c != 0;
+            nd[k] = live[k] ? 2 * nd[k] + 1 + (c > (rec & 0xffff) ? 1 : 0) : nd[k];
           }
-          fr[k] = __dadd_rn(fr[k], nw_prev[nd]);
-          F[i] = fr[k];
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          const int64_t i = t0 + k * kListThreads + threadIdx.x;
+          if (i < n) {
+            fr[k] = __dadd_rn(fr[k], nw_prev[nd[k]]);
+            F[i] = fr[k];
+          }
         }
       }
       // s_cols is rewritten only after the list phase's barriers (or, without

@@ -1290,19 +1290,36 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   static const int lh_waves = getenv("BB_LH_WAVES") ? std::max(1, atoi(getenv("BB_LH_WAVES"))) : 1;
   const int lh_grid = lh_waves * (lh_nw == 8 ? 2 * (c.sm_count - hist_reserve()) : c.sm_count - hist_reserve());
   const int hp_env = hist_path_env();
-  const bool lists = sizeof(CodeT) == 1 && s.d <= 64 && s.depth <= 8 && (hp_env == 0 || hp_env == 5) &&
-                     2 * (1 << (s.depth - 1)) <= lh_grid && !getenv("BB_HIST_WARP") && !getenv("BB_HIST_GLOBAL_GROUPS");
+  const bool lists8 = sizeof(CodeT) == 1 && s.d <= 64 && s.depth <= 8 && (hp_env == 0 || hp_env == 5) &&
+                      2 * (1 << (s.depth - 1)) <= lh_grid && !getenv("BB_HIST_WARP") && !getenv("BB_HIST_GLOBAL_GROUPS");
+  // u16 codes (more than 256 bins, or 256 bins with missing values): the
+  // 16-feature-group list kernel (k_hist_list16), up to 1024 bins
+  const int l16_groups = (int)ceil_div(s.d, kL16Feat);
+  const bool lists16 = sizeof(CodeT) == 2 && s.B <= kL16Bins && s.depth <= 8 && (hp_env == 0 || hp_env == 5) &&
+                       2 * (1 << (s.depth - 1)) * l16_groups <= kLhMaxSegs && !getenv("BB_HIST_WARP") &&
+                       !getenv("BB_HIST_GLOBAL_GROUPS") && !(getenv("BB_LIST16") && atoi(getenv("BB_LIST16")) == 0);
+  const bool lists = lists8 || lists16;
+  uint16_t* rc16 = nullptr;
   uint32_t* rc = nullptr;
   int* lrow[2] = {nullptr, nullptr};
   long long* lq[2] = {nullptr, nullptr};
   int* cnt = nullptr;
   if (lists) {
-    rc = A.alloc<uint32_t>((size_t)npad * lh_pitch);
     for (int b = 0; b < 2; ++b) {
       lrow[b] = A.alloc<int>(npad);
       lq[b] = A.alloc<long long>(npad);
     }
     cnt = A.alloc<int>((size_t)2 * s.n_nodes);
+  }
+  if (lists16) {
+    rc16 = A.alloc<uint16_t>((size_t)npad * kL16Feat * l16_groups);
+    BB_CUDA(cudaFuncSetAttribute(k_hist_list16, cudaFuncAttributeMaxDynamicSharedMemorySize, kL16SmemBytes));
+    k_rowcodes16<<<dim3((unsigned)ceil_div(n, kTile), l16_groups), 256, 0, st>>>(
+        reinterpret_cast<const uint16_t*>(codes), n, s.d, l16_groups, rc16);
+    BB_LAUNCH_CHECK();
+  }
+  if (lists8) {
+    rc = A.alloc<uint32_t>((size_t)npad * lh_pitch);
     const int tiles = (int)ceil_div(n, kTile);
     const uint8_t* c8 = reinterpret_cast<const uint8_t*>(codes);
     BB_CUDA(cudaFuncSetAttribute(k_hist_list<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, lh_smem_bytes<8>()));
@@ -1407,7 +1424,13 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         if (prof) hist_event();
         if (lists) {
           const int lb = (layer - 1) & 1;
-          if (lh_nw == 8)
+          if (lists16) {
+            const int items = (p.sib ? p.nodes : 2 * p.nodes) * l16_groups;
+            const int g16 = std::max(c.sm_count - hist_reserve(), items);
+            launch_k(pdl_h, k_hist_list16, g16, kLhThreads, kL16SmemBytes, st, reinterpret_cast<const uint4*>(rc16),
+                     2 * l16_groups, lrow[lb], lq[lb], cnt, layer, p.sib ? sib_mode : 0, s.n_sig, s.d, s.B, p.nodes, hist,
+                     l16_groups);
+          } else if (lh_nw == 8)
             launch_k(pdl_h, k_hist_list<8>, lh_grid, kLhThreads, lh_smem_bytes<8>(), st, rc, lrow[lb], lq[lb], cnt, layer,
                      p.sib ? sib_mode : 0, s.n_sig, s.d, s.B, code_off, p.nodes, hist, lh_pitch, lh_groups);
           else

@@ -40,7 +40,7 @@ namespace bb {
 constexpr int kLhWarps = 16;
 constexpr int kLhThreads = 32 * kLhWarps;
 constexpr int kLhFlushRows = 32767;
-constexpr int kLhMaxSegs = 256;
+constexpr int kLhMaxSegs = 512;
 #ifndef BB_LH_PF
 #define BB_LH_PF 4
 #endif
@@ -523,6 +523,211 @@ __global__ void __launch_bounds__(256) k_rowcodes(const uint8_t* __restrict__ co
     uint4* dst = reinterpret_cast<uint4*>(rc + row * NW);
 #pragma unroll
     for (int j = 0; j < NW / 4; ++j) dst[j] = make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]);
+  }
+}
+
+// ------------------------------------------------ u16 codes (B <= 1024)
+// The same row-list histogram for 2-byte codes (more than 256 bins, or 256
+// bins with missing values): features in GROUPS of 16.  A CTA takes one
+// (segment, feature group) item (or a row range of one), keeps the group's
+// limbs [bin][16 features][lo, hi] (1024 x 32 words = 128 KB) in shared memory
+// and reads 32 bytes per listed row: the group's codes from a row-major copy
+// (rc16, row pitch 32 B x groups).  Lane owns a row.  Step (a, b), a < 8,
+// b < 4: lane l takes word w = (l/4 + a) mod 8 of its row (features 2w, 2w+1)
+// and (half h, limb) = ((l mod 4) + b) mod 4: the 32 lanes cover every (w, h,
+// limb) once, so the row reads (bank 8 (l mod 4) + w, row pitch 8 words) and
+// the atomics (bank 4w + 2h + limb, 32 words per bin) are conflict-free for any
+// codes.  Stored slot = code - 1 (code 0, a missing value, is skipped: its
+// slot is never read, trees.py:181-186).
+constexpr int kL16Feat = 16;
+constexpr int kL16Bins = 1024;
+constexpr int kL16HistBytes = kL16Bins * 2 * kL16Feat * 4;                      // 128 KB
+constexpr int kL16ChunkBins = 256;                                              // bins per flush round
+constexpr int kL16StagePitch = kL16ChunkBins + 2;                               // int64 per staged feature row
+constexpr int kL16BufBytes = kL16Feat * kL16StagePitch * 8 > kLhWarps * 32 * 8 * 4 ? kL16Feat * kL16StagePitch * 8
+                                                                                 : kLhWarps * 32 * 8 * 4;
+constexpr int kL16SmemBytes = kL16HistBytes + kL16BufBytes + 16 * kLhMaxSegs + 64;
+
+__global__ void __launch_bounds__(kLhThreads, 1)
+    k_hist_list16(const uint4* __restrict__ rc16, int pitch16, const int* __restrict__ lrow,
+                  const long long* __restrict__ lq, const int* __restrict__ cnt, int layer, int sib, long long n_sig,
+                  int d, int B, int nodes, unsigned long long* __restrict__ hist, int ngroups) {
+  // rc16: row-major codes, pitch16 uint4 (16 bytes) per row = 2 per feature group
+  extern __shared__ __align__(16) unsigned char lh_sm[];
+  unsigned char* hb = lh_sm;
+  uint32_t* bufs = reinterpret_cast<uint32_t*>(lh_sm + kL16HistBytes);  // [warp][32 rows][8 words]
+  int4* segs = reinterpret_cast<int4*>(lh_sm + kL16HistBytes + kL16BufBytes);
+  __shared__ int s_ns;
+  __shared__ int s_asg[3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kL16HistBytes / 16; i += kLhThreads)
+    reinterpret_cast<uint4*>(hb)[i] = make_uint4(0u, 0u, 0u, 0u);
+  pdl_wait();
+  pdl_launch();
+  if (threadIdx.x == 0) {
+    // items = (segment, group): expanded in place, the group in the node field's high half
+    const int ns = lh_segments(cnt, layer, sib, n_sig, segs);
+    for (int v = ns * ngroups - 1; v >= 0; --v) {
+      const int4 sg = segs[v / ngroups];
+      segs[v] = make_int4(sg.x, sg.y, sg.z | ((v % ngroups) << 16), sg.w);
+    }
+    s_ns = ns * ngroups;
+  }
+  __syncthreads();
+  if (s_ns <= (int)gridDim.x) {
+    if (warp == 0) lh_assign(segs, s_ns, (int)gridDim.x, (int)blockIdx.x, lane, s_asg);
+  } else if (threadIdx.x == 0) {  // more items than CTAs' share: one whole item per CTA (grid = items)
+    const int it = (int)blockIdx.x;
+    s_asg[0] = (it < s_ns && segs[it].y > 0) ? it : -1;
+    s_asg[1] = 0;
+    s_asg[2] = it < s_ns ? segs[it].y : 0;
+  }
+  __syncthreads();
+  if (s_asg[0] < 0) return;
+  const int4 sg = segs[s_asg[0]];
+  const int node = sg.z & 0xffff, grp = sg.z >> 16;
+  BB_DCHECK(node < nodes && grp < ngroups);
+  const int r_begin = s_asg[1], r_end = s_asg[2];
+  const int* lr = lrow + sg.x;
+  const long long* lqs = lq + sg.x;
+  const int fg = min(kL16Feat, d - kL16Feat * grp);  // features of this group
+  uint32_t* wbuf = bufs + warp * 32 * 8;
+  // per-lane constants of the (a, b) schedule
+  const int w0 = lane >> 2;
+  uint32_t cb[4], psel[4];
+  bool hi_limb[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int hl = ((lane & 3) + b) & 3;
+    const int h = hl & 1, limb = hl >> 1;
+    cb[b] = (uint32_t)(8 * h + 4 * limb);
+    psel[b] = h ? 0x4432u : 0x4410u;  // the half word into the low 16 bits
+    hi_limb[b] = limb != 0;
+  }
+  for (int p0 = r_begin; p0 < r_end; p0 += kLhFlushRows) {
+    const int p1 = min(r_end, p0 + kLhFlushRows);
+    const int nsl = (p1 - p0 + 31) >> 5;
+    const int nj = nsl > warp ? (nsl - warp + kLhWarps - 1) / kLhWarps : 0;
+    constexpr int PF = 4;  // slices in flight per warp (2 x 16 bytes per lane each)
+    auto entry = [&](int j, int& row, long long& qq) {
+      const int sl = warp + kLhWarps * j;
+      const int e = p0 + 32 * sl + lane;
+      row = -1;
+      qq = 0;
+      if (sl < nsl && e < p1) {
+        row = __ldg(lr + e);
+        qq = __ldg(lqs + e);
+      }
+    };
+    auto fetch = [&](int row, uint4& x0, uint4& x1) {  // the lane's own row: one 32-byte sector
+      x0 = make_uint4(0u, 0u, 0u, 0u);
+      x1 = x0;
+      if (row >= 0) {
+        const uint4* src = rc16 + (size_t)row * pitch16 + 2 * grp;
+        x0 = __ldg(src);
+        x1 = __ldg(src + 1);
+      }
+    };
+    long long qv[PF], qn[PF];
+    int rn[PF];
+    uint4 xa[PF], xb[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      int r0;
+      entry(u, r0, qv[u]);
+      fetch(r0, xa[u], xb[u]);
+      entry(u + PF, rn[u], qn[u]);
+    }
+    for (int j = 0; j < nj; j += PF) {
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        if (j + u < nj) {
+          uint4* rowp4 = reinterpret_cast<uint4*>(wbuf + lane * 8);
+          rowp4[0] = xa[u];
+          rowp4[1] = xb[u];
+          __syncwarp();
+          fetch(rn[u], xa[u], xb[u]);
+          const long long qq = qv[u];
+          qv[u] = qn[u];
+          entry(j + u + 2 * PF, rn[u], qn[u]);
+          const uint32_t qlo = (uint32_t)((unsigned long long)qq & 0xffffull);
+          const uint32_t qhi = (uint32_t)(int)(qq >> 16);
+          uint32_t val[4];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) val[b] = hi_limb[b] ? qhi : qlo;
+          const uint32_t* rowp = wbuf + lane * 8;
+#pragma unroll
+          for (int a = 0; a < 8; ++a) {
+            const int w = (w0 + a) & 7;
+            const uint32_t word = rowp[w];
+            const uint32_t wpart = 16u * (uint32_t)w - 128u;  // slot = code - 1
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const uint32_t code = __byte_perm(word, 0u, psel[b]);
+              const uint32_t off = code * 128u + (wpart + cb[b]);
+              BB_DCHECK(code <= (uint32_t)kL16Bins);
+              if (code != 0u) atomicAdd(reinterpret_cast<uint32_t*>(hb + off), val[b]);
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+    // ---- flush in rounds of 256 bins: int64 rows [feature][bin] staged in
+    // the drained buffers, one bulk reduction per feature row
+    const uint32_t* hw = reinterpret_cast<const uint32_t*>(hb);
+    long long* stg = reinterpret_cast<long long*>(bufs);
+    for (int c0 = 0; c0 < B; c0 += kL16ChunkBins) {
+      const int cn = min(kL16ChunkBins, B - c0);
+      const int f = lane & 15;
+      for (int bin = 2 * warp + (lane >> 4); bin < cn; bin += 2 * kLhWarps) {
+        const uint2 v = *reinterpret_cast<const uint2*>(hw + (size_t)(c0 + bin) * 32 + 2 * f);
+        stg[(size_t)f * kL16StagePitch + bin] = (long long)(int)v.y * 65536ll + (long long)v.x;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if ((int)threadIdx.x < fg)
+        bulk_reduce_add_u64(hist + (((size_t)sg.w * nodes + node) * d + kL16Feat * grp + threadIdx.x) * B + c0,
+                            stg + (size_t)threadIdx.x * kL16StagePitch, (unsigned)cn * 8u);
+      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
+      __syncthreads();
+    }
+    if (p1 < r_end) {
+      for (int i = threadIdx.x; i < kL16HistBytes / 16; i += kLhThreads)
+        reinterpret_cast<uint4*>(hb)[i] = make_uint4(0u, 0u, 0u, 0u);
+      __syncthreads();
+    }
+  }
+}
+
+// Row-major copy of the tiled column-major u16 codes: rc16[row][16 * groups]
+// (features >= d zero = missing).  One CTA per (1024-row tile, feature group).
+__global__ void __launch_bounds__(256) k_rowcodes16(const uint16_t* __restrict__ codes, int64_t n, int d, int ngroups,
+                                                    uint16_t* __restrict__ rc16) {
+  __shared__ __align__(16) uint16_t col[kL16Feat][kTile];
+  const int64_t tile = blockIdx.x;
+  const int grp = blockIdx.y;
+  const int f0 = kL16Feat * grp, fg = min(kL16Feat, d - f0);
+  for (int i = threadIdx.x; i < fg * (kTile / 8); i += blockDim.x) {
+    const int f = i / (kTile / 8), v = i % (kTile / 8);
+    reinterpret_cast<uint4*>(&col[f][0])[v] =
+        __ldg(reinterpret_cast<const uint4*>(codes + (tile * d + f0 + f) * (int64_t)kTile) + v);
+  }
+  __syncthreads();
+  const int pitch = kL16Feat * ngroups;
+  for (int r = threadIdx.x; r < kTile; r += blockDim.x) {
+    const int64_t row = tile * kTile + r;
+    if (row >= n) break;
+    uint32_t wv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t lo = 2 * j < fg ? col[2 * j][r] : 0u, hi = 2 * j + 1 < fg ? col[2 * j + 1][r] : 0u;
+      wv[j] = lo | (hi << 16);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(rc16 + row * pitch + f0);
+    dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
   }
 }
 

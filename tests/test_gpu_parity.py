@@ -886,3 +886,37 @@ def test_fit_staged_upload_matches_plain_copy(monkeypatch):
         np.testing.assert_array_equal(ta.cut_bin, tb.cut_bin)
         np.testing.assert_array_equal(ta.node_weight, tb.node_weight)
     np.testing.assert_array_equal(a.fit_info["scores"], b.fit_info["scores"])
+
+
+# ------------------------------------------------------------------ u16 row-list histogram (k_hist_list16)
+@pytest.mark.parametrize("levels,nan,d,depth", [(8, True, 37, 4), (9, False, 21, 5), (10, False, 16, 3),
+                                                (10, True, 50, 4), (9, False, 100, 6)])
+def test_fit_list16_vs_fixed_point_oracle(levels, nan, d, depth, monkeypatch):
+    """2-byte codes (256 bins with missing values, 512 and 1024 bins) run the
+    16-feature-group row-list histogram: ragged last groups, with and without
+    sibling subtraction, negative weights; exact against the fixed-point oracle
+    and identical to the round-1 kernels (BB_LIST16=0)."""
+    rng = np.random.default_rng(levels * 100 + d)
+    n = 40_000
+    X = rng.normal(size=(n, d)).astype(np.float32)
+    X[:, 1] = np.round(X[:, 1] * 3) / 3  # ties
+    y = (X[:, 0] - 0.7 * X[:, min(5, d - 1)] + rng.normal(size=n) > 0).astype(int)
+    w = rng.exponential(size=n) * np.where(rng.random(n) < 0.1, -0.5, 1.0)
+    if nan:
+        X[rng.random(X.shape) < 0.04] = np.nan
+    cfg = FitConfig(n_trees=5, depth=depth, shrinkage=0.2, subsample=0.5, binning_levels=levels, seed=4)
+    forest = fit_forest(X, y, w, cfg, return_leaves=True)
+    ref = oracle.fit_forest(X, y, w, fixed_point=True, record_leaves=True, n_trees=5, depth=depth, shrinkage=0.2,
+                            subsample=0.5, levels=levels, seed=4)
+    monkeypatch.setenv("BB_LIST16", "0")
+    old = fit_forest(X, y, w, cfg, return_leaves=True)
+    for t in range(5):
+        tr = forest.trees[t]
+        np.testing.assert_array_equal(tr.valid, ref.valid[t])
+        np.testing.assert_array_equal(tr.feature, ref.feature[t])
+        np.testing.assert_array_equal(tr.cut_bin, ref.cut_bin[t])
+        np.testing.assert_array_equal(forest.fit_info["leaves"][t], ref.leaves[t].astype(np.uint16))
+        np.testing.assert_allclose(tr.node_weight, ref.node_weight[t], rtol=1e-12, atol=1e-15)
+        np.testing.assert_array_equal(tr.feature, old.trees[t].feature)
+        np.testing.assert_array_equal(tr.cut_bin, old.trees[t].cut_bin)
+        np.testing.assert_array_equal(tr.node_weight, old.trees[t].node_weight)

@@ -537,16 +537,23 @@ __global__ void __launch_bounds__(256) k_rowcodes(const uint8_t* __restrict__ co
 // and (half h, limb) = ((l mod 4) + b) mod 4: the 32 lanes cover every (w, h,
 // limb) once, so the row reads (bank 8 (l mod 4) + w, row pitch 8 words) and
 // the atomics (bank 4w + 2h + limb, 32 words per bin) are conflict-free for any
-// codes.  Stored slot = code - 1 (code 0, a missing value, is skipped: its
-// slot is never read, trees.py:181-186).
+// codes.  rc16 holds SLOTS: code - 1, and kL16Bins (a dummy bin row that is
+// never flushed) for a missing value (code 0: its slot is never read,
+// trees.py:181-186) and for the padding features of the last group, so the
+// accumulation is branch-free.
 constexpr int kL16Feat = 16;
 constexpr int kL16Bins = 1024;
-constexpr int kL16HistBytes = kL16Bins * 2 * kL16Feat * 4;                      // 128 KB
+constexpr int kL16HistBytes = (kL16Bins + 1) * 2 * kL16Feat * 4;                // 128 KB + the dummy bin row
+constexpr uint32_t kL16Dummy2 = (uint32_t)kL16Bins * 0x00010001u;               // two dummy slots
 constexpr int kL16ChunkBins = 256;                                              // bins per flush round
 constexpr int kL16StagePitch = kL16ChunkBins + 2;                               // int64 per staged feature row
 constexpr int kL16BufBytes = kL16Feat * kL16StagePitch * 8 > kLhWarps * 32 * 8 * 4 ? kL16Feat * kL16StagePitch * 8
                                                                                  : kLhWarps * 32 * 8 * 4;
 constexpr int kL16SmemBytes = kL16HistBytes + kL16BufBytes + 16 * kLhMaxSegs + 64;
+
+__device__ __forceinline__ void red_shared_add_u32(uint32_t saddr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
 
 __global__ void __launch_bounds__(kLhThreads, 1)
     k_hist_list16(const uint4* __restrict__ rc16, int pitch16, const int* __restrict__ lrow,
@@ -593,6 +600,7 @@ __global__ void __launch_bounds__(kLhThreads, 1)
   const int fg = min(kL16Feat, d - kL16Feat * grp);  // features of this group
   uint32_t* wbuf = bufs + warp * 32 * 8;
   // per-lane constants of the (a, b) schedule
+  const uint32_t hb_s = smem_u32(hb);
   const int w0 = lane >> 2;
   uint32_t cb[4], psel[4];
   bool hi_limb[4];
@@ -620,7 +628,7 @@ __global__ void __launch_bounds__(kLhThreads, 1)
       }
     };
     auto fetch = [&](int row, uint4& x0, uint4& x1) {  // the lane's own row: one 32-byte sector
-      x0 = make_uint4(0u, 0u, 0u, 0u);
+      x0 = make_uint4(kL16Dummy2, kL16Dummy2, kL16Dummy2, kL16Dummy2);  // no row: q = 0 into the dummy bin row
       x1 = x0;
       if (row >= 0) {
         const uint4* src = rc16 + (size_t)row * pitch16 + 2 * grp;
@@ -660,13 +668,12 @@ __global__ void __launch_bounds__(kLhThreads, 1)
           for (int a = 0; a < 8; ++a) {
             const int w = (w0 + a) & 7;
             const uint32_t word = rowp[w];
-            const uint32_t wpart = 16u * (uint32_t)w - 128u;  // slot = code - 1
+            const uint32_t wpart = hb_s + 16u * (uint32_t)w;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-              const uint32_t code = __byte_perm(word, 0u, psel[b]);
-              const uint32_t off = code * 128u + (wpart + cb[b]);
-              BB_DCHECK(code <= (uint32_t)kL16Bins);
-              if (code != 0u) atomicAdd(reinterpret_cast<uint32_t*>(hb + off), val[b]);
+              const uint32_t slot = __byte_perm(word, 0u, psel[b]);
+              BB_DCHECK(slot <= (uint32_t)kL16Bins);
+              red_shared_add_u32(slot * 128u + (wpart + cb[b]), val[b]);
             }
           }
           __syncwarp();
@@ -701,8 +708,8 @@ __global__ void __launch_bounds__(kLhThreads, 1)
   }
 }
 
-// Row-major copy of the tiled column-major u16 codes: rc16[row][16 * groups]
-// (features >= d zero = missing).  One CTA per (1024-row tile, feature group).
+// Row-major copy of the tiled column-major u16 codes as histogram slots:
+// rc16[row][16 * groups].  One CTA per (1024-row tile, feature group).
 __global__ void __launch_bounds__(256) k_rowcodes16(const uint16_t* __restrict__ codes, int64_t n, int d, int ngroups,
                                                     uint16_t* __restrict__ rc16) {
   __shared__ __align__(16) uint16_t col[kL16Feat][kTile];
@@ -722,7 +729,9 @@ __global__ void __launch_bounds__(256) k_rowcodes16(const uint16_t* __restrict__
     uint32_t wv[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const uint32_t lo = 2 * j < fg ? col[2 * j][r] : 0u, hi = 2 * j + 1 < fg ? col[2 * j + 1][r] : 0u;
+      // slot = code - 1; missing values and padding features: the dummy bin row
+      const uint32_t cl = 2 * j < fg ? col[2 * j][r] : 0u, ch = 2 * j + 1 < fg ? col[2 * j + 1][r] : 0u;
+      const uint32_t lo = cl ? cl - 1u : (uint32_t)kL16Bins, hi = ch ? ch - 1u : (uint32_t)kL16Bins;
       wv[j] = lo | (hi << 16);
     }
     uint4* dst = reinterpret_cast<uint4*>(rc16 + row * pitch + f0);

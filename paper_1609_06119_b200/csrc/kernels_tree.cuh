@@ -138,6 +138,14 @@ __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, i
     }
     __syncthreads();
   }
+  const bool gather_rec = !staged && nw_prev && walk_tree >= 0 && n_internal <= kStageNodes;
+  if (gather_rec) {
+    if ((int)threadIdx.x < n_internal) {
+      const int64_t e = (int64_t)walk_tree * n_internal + threadIdx.x;
+      s_rec[threadIdx.x] = __ldg(&ta.valid[e]) ? ((__ldg(&ta.feature[e]) << 16) | __ldg(&ta.cut[e])) : -1;
+    }
+    __syncthreads();
+  }
   const int64_t code_tiles = (n + kTile - 1) >> kTileLog;
   for (int64_t t0 = (int64_t)blockIdx.x * kListTileRows; t0 < n; t0 += (int64_t)gridDim.x * kListTileRows) {
     int loc[R];
@@ -213,6 +221,37 @@ __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, i
       // s_cols is rewritten only after the list phase's barriers (or, without
       // lists, after the barrier below)
       if (!lrow) __syncthreads();
+    } else if (gather_rec) {
+      // gather walk over packed node records in shared memory (feature << 16 |
+      // cut): the R rows in lockstep, branch-free, one global code per level
+      int nd[R];
+      bool live[R];
+      int64_t base[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int64_t i = t0 + k * kListThreads + threadIdx.x;
+        nd[k] = 0;
+        live[k] = i < n;
+        base[k] = (i >> kTileLog) * d * (int64_t)kTile + (i & (kTile - 1));
+      }
+      for (int l = 0; l < depth; ++l) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          const int rec = s_rec[nd[k]];
+          live[k] = live[k] && rec >= 0;
+          const int c = live[k] ? (int)codes[base[k] + (int64_t)(rec >> 16) * kTile] + code_off : 0;
+          live[k] = live[k] && c != 0;
+          nd[k] = live[k] ? 2 * nd[k] + 1 + (c > (rec & 0xffff) ? 1 : 0) : nd[k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int64_t i = t0 + k * kListThreads + threadIdx.x;
+        if (i < n) {
+          fr[k] = __dadd_rn(fr[k], nw_prev[nd[k]]);
+          F[i] = fr[k];
+        }
+      }
     } else if (nw_prev && walk_tree >= 0) {
       // the R rows' walks in lockstep: independent gather chains overlap
       int nd[R];

@@ -346,7 +346,10 @@ __global__ void __launch_bounds__(kLhThreads, NW == 8 ? 2 : 1)
           bulk_reduce_add_u64(hist + (((size_t)sg.w * nodes + sg.z) * dtot + fbase + ff) * B,
                               stg + (size_t)threadIdx.x * spitch, (unsigned)B * 8u);
       }
-      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
+      // the staging rows may be rewritten once the reductions have READ them;
+      // only the last round waits for the reductions themselves
+      if (round == 0) asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+      else asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
       __syncthreads();
     }
     if (p1 < r_end) {
@@ -697,7 +700,8 @@ __global__ void __launch_bounds__(kLhThreads, 1)
       if ((int)threadIdx.x < fg)
         bulk_reduce_add_u64(hist + (((size_t)sg.w * nodes + node) * d + kL16Feat * grp + threadIdx.x) * B + c0,
                             stg + (size_t)threadIdx.x * kL16StagePitch, (unsigned)cn * 8u);
-      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
+      if (c0 + kL16ChunkBins < B) asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+      else asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
       __syncthreads();
     }
     if (p1 < r_end) {

@@ -409,7 +409,9 @@ def run_b200(args, rank, world, local):
     avg_launch_ms = hist_ms / max(1, hist_launches)
     achieved = per_launch_bytes / (avg_launch_ms / 1e3) / 1e9 if avg_launch_ms > 0 else None
     peak, peak_kind = measured_peak()
-    hist_kernel = "k_hist_list" if (1 << spec["binning_levels"]) <= 256 and d <= 64 else "k_layer_hist_w/g"
+    B_ = 1 << spec["binning_levels"]
+    hist_kernel = ("k_hist_list" if B_ <= 256 and d <= 64 else "k_hist_list16" if 256 < B_ <= 1024 else
+                   "k_layer_hist_w/g")
     del Xd, yd, wd
     torch.cuda.empty_cache()
 

@@ -1425,8 +1425,7 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
         if (lists) {
           const int lb = (layer - 1) & 1;
           if (lists16) {
-            const int items = (p.sib ? p.nodes : 2 * p.nodes) * l16_groups;
-            const int g16 = std::max(c.sm_count - hist_reserve(), items);
+            const int g16 = c.sm_count - hist_reserve();  // more (segment, group) items than CTAs: row-balanced parts
             launch_k(pdl_h, k_hist_list16, g16, kLhThreads, kL16SmemBytes, st, reinterpret_cast<const uint4*>(rc16),
                      2 * l16_groups, lrow[lb], lq[lb], cnt, layer, p.sib ? sib_mode : 0, s.n_sig, s.d, s.B, p.nodes, hist,
                      l16_groups);

@@ -584,25 +584,30 @@ __global__ void __launch_bounds__(kLhThreads, 1)
     s_ns = ns * ngroups;
   }
   __syncthreads();
+  // One item (or a row range of one) per CTA while the items fit the grid;
+  // otherwise (deep layers x many groups) the concatenated items' rows are cut
+  // into gridDim.x equal contiguous parts and a CTA walks the items of its part
+  // (one flush per item touched; rows, not items, are balanced).
+  __shared__ long long s_part[2];  // partition mode: rows of the part still to do, -1 in item mode
   if (s_ns <= (int)gridDim.x) {
     if (warp == 0) lh_assign(segs, s_ns, (int)gridDim.x, (int)blockIdx.x, lane, s_asg);
-  } else if (threadIdx.x == 0) {  // more items than CTAs' share: one whole item per CTA (grid = items)
-    const int it = (int)blockIdx.x;
-    s_asg[0] = (it < s_ns && segs[it].y > 0) ? it : -1;
-    s_asg[1] = 0;
-    s_asg[2] = it < s_ns ? segs[it].y : 0;
+    if (threadIdx.x == 0) s_part[0] = -1;
+  } else if (threadIdx.x == 0) {
+    long long tot = 0;
+    for (int v = 0; v < s_ns; ++v) tot += segs[v].y;
+    const long long lo = tot * (long long)blockIdx.x / gridDim.x, hi = tot * ((long long)blockIdx.x + 1) / gridDim.x;
+    long long cum = 0;
+    int v = 0;
+    while (v < s_ns && cum + segs[v].y <= lo) cum += segs[v++].y;
+    s_asg[0] = (hi > lo && v < s_ns) ? v : -1;
+    s_asg[1] = (int)(lo - cum);
+    s_asg[2] = v < s_ns ? (int)min((long long)segs[v].y, hi - cum) : 0;
+    s_part[0] = hi - lo;
   }
   __syncthreads();
   if (s_asg[0] < 0) return;
-  const int4 sg = segs[s_asg[0]];
-  const int node = sg.z & 0xffff, grp = sg.z >> 16;
-  BB_DCHECK(node < nodes && grp < ngroups);
-  const int r_begin = s_asg[1], r_end = s_asg[2];
-  const int* lr = lrow + sg.x;
-  const long long* lqs = lq + sg.x;
-  const int fg = min(kL16Feat, d - kL16Feat * grp);  // features of this group
-  uint32_t* wbuf = bufs + warp * 32 * 8;
-  // per-lane constants of the (a, b) schedule
+  int item = s_asg[0], r_begin = s_asg[1], r_end = s_asg[2];
+  long long part_left = s_part[0];
   const uint32_t hb_s = smem_u32(hb);
   const int w0 = lane >> 2;
   uint32_t cb[4], psel[4];
@@ -615,6 +620,14 @@ __global__ void __launch_bounds__(kLhThreads, 1)
     psel[b] = h ? 0x4432u : 0x4410u;  // the half word into the low 16 bits
     hi_limb[b] = limb != 0;
   }
+  uint32_t* wbuf = bufs + warp * 32 * 8;
+  for (;;) {  // the items of this CTA (one in item mode)
+  const int4 sg = segs[item];
+  const int node = sg.z & 0xffff, grp = sg.z >> 16;
+  BB_DCHECK(node < nodes && grp < ngroups);
+  const int* lr = lrow + sg.x;
+  const long long* lqs = lq + sg.x;
+  const int fg = min(kL16Feat, d - kL16Feat * grp);  // features of this group
   for (int p0 = r_begin; p0 < r_end; p0 += kLhFlushRows) {
     const int p1 = min(r_end, p0 + kLhFlushRows);
     const int nsl = (p1 - p0 + 31) >> 5;
@@ -709,6 +722,17 @@ __global__ void __launch_bounds__(kLhThreads, 1)
         reinterpret_cast<uint4*>(hb)[i] = make_uint4(0u, 0u, 0u, 0u);
       __syncthreads();
     }
+  }
+  // next item of the part (partition mode)
+  if (part_left < 0) break;
+  part_left -= r_end - r_begin;
+  do ++item; while (item < s_ns && segs[item].y == 0);
+  if (part_left <= 0 || item >= s_ns) break;
+  r_begin = 0;
+  r_end = (int)min((long long)segs[item].y, part_left);
+  for (int i = threadIdx.x; i < kL16HistBytes / 16; i += kLhThreads)
+    reinterpret_cast<uint4*>(hb)[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
   }
 }
 

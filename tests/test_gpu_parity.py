@@ -306,7 +306,7 @@ def _forced_from_golden(g, gap_tol=1e-9, noise_tol=1e-9):
     return forced
 
 
-def _check_fit_vs_golden(forest, g, rows_X, forced_ok=True):
+def _check_fit_vs_golden(forest, g, rows_X, forced_ok=True, tight=True):
     T = int(g["n_trees"])
     np.testing.assert_array_equal(np.stack([b.boundaries for b in forest.binnings]), g["boundaries"])
     for t in range(T):
@@ -317,9 +317,20 @@ def _check_fit_vs_golden(forest, g, rows_X, forced_ok=True):
         np.testing.assert_array_equal(tr.threshold, g["threshold"][t], err_msg=f"tree {t}")
         lv = forest.fit_info["leaves"][t].astype(np.int16)
         assert sha(lv) == g["leaf_hashes"][t], f"leaf ids differ at tree {t}"
-        # node weights come from fixed-point sums: not a bit-exact quantity;
-        # the contract on them is the probability bar below
-        np.testing.assert_allclose(tr.node_weight, g["node_weight"][t], rtol=1e-3, atol=1e-6)
+        # node weights and gains come from fixed-point sums: not bit-exact
+        # quantities (the contract on them is the probability bar below).
+        # Measured max relative error over the goldens (tools/divergence.py,
+        # profiles/r02_divergence.txt): node weight 3.5e-6, gain 1.5e-10
+        # (the randomized small fits - negative weights, near-empty nodes,
+        # cancelling sums - keep the loose bound: tight=False)
+        if not tight:
+            np.testing.assert_allclose(tr.node_weight, g["node_weight"][t], rtol=1e-3, atol=1e-6)
+            continue
+        np.testing.assert_allclose(tr.node_weight, g["node_weight"][t], rtol=1e-4, atol=1e-7)
+        if "gain" in g:
+            ok = np.asarray(tr.valid, bool) & np.isfinite(g["gain"][t])
+            scale = float(np.max(np.abs(g["gain"][t][ok]))) if ok.any() else 0.0
+            np.testing.assert_allclose(tr.gain[ok], g["gain"][t][ok], rtol=1e-6, atol=1e-9 * scale)
     p = predict_batch(forest, rows_X)
     assert np.max(np.abs(p - g["pred"])) <= PROB_TOL
 
@@ -367,7 +378,7 @@ def test_small_fits_vs_reference_golden(golden_dir):
         forest = fit_forest(g["X"], g["y"], g.get("w"), cfg, forced_cuts=forced, return_leaves=True)
         assert forest.f0 == float(g["f0"]), i
         try:
-            _check_fit_vs_golden(forest, g, g["X"][g["pred_rows"]])
+            _check_fit_vs_golden(forest, g, g["X"][g["pred_rows"]], tight=False)
         except AssertionError as e:
             raise AssertionError(f"case {i}: {e}") from None
     print("forced nodes across small cases:", forced_total)

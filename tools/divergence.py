@@ -30,6 +30,21 @@ for name, fixture, n in [("cfg3", "cfg3_proxy_fit.npz", 200_000), ("cfg2", "cfg2
             gap = float(aud[0][2]) if aud else float("nan")
             first = (t, node, gap)
             break
+    # node weights / gains of the trees that agree: max relative error vs the
+    # reference's float64 values (the GPU's come from fixed-point sums)
+    t_end = int(T) if first is None else first[0]
+    nw_err = g_err = 0.0
+    for t in range(t_end):
+        ref_nw = g["node_weight"][t]
+        den = np.maximum(np.abs(ref_nw), 1e-300)
+        ok = np.abs(ref_nw) > 1e-12
+        if ok.any():
+            nw_err = max(nw_err, float(np.max(np.abs(f.trees[t].node_weight - ref_nw)[ok] / den[ok])))
+        if "gain" in g.files:
+            ref_g = g["gain"][t]
+            okg = np.asarray(f.trees[t].valid, bool) & np.isfinite(ref_g) & (np.abs(ref_g) > 1e-12)
+            if okg.any():
+                g_err = max(g_err, float(np.max(np.abs(f.trees[t].gain - ref_g)[okg] / np.abs(ref_g)[okg])))
     rows = g["pred_rows"]
     p = predict_batch(f, X[rows])
     lab = y[rows]
@@ -37,4 +52,6 @@ for name, fixture, n in [("cfg3", "cfg3_proxy_fit.npz", 200_000), ("cfg2", "cfg2
     d_auc = roc_auc(p, lab, wr) - roc_auc(g["pred"], lab, wr)
     print(f"{fixture}: {int(T)} trees free-running; first divergent "
           f"{'none' if first is None else f'tree {first[0]} node {first[1]} (reference gain gap {first[2]:.2e})'}; "
-          f"max|dp| {np.max(np.abs(p - g['pred'])):.3e}; dAUC {d_auc:+.3e} on {rows.size} rows", flush=True)
+          f"max|dp| {np.max(np.abs(p - g['pred'])):.3e}; dAUC {d_auc:+.3e} on {rows.size} rows; "
+          f"max rel err over {t_end} agreeing trees: node weight {nw_err:.2e}"
+          f"{'' if 'gain' not in g.files else f', gain {g_err:.2e}'}", flush=True)

@@ -1292,10 +1292,12 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   const int hp_env = hist_path_env();
   const bool lists8 = sizeof(CodeT) == 1 && s.d <= 64 && s.depth <= 8 && (hp_env == 0 || hp_env == 5) &&
                       2 * (1 << (s.depth - 1)) <= lh_grid && !getenv("BB_HIST_WARP") && !getenv("BB_HIST_GLOBAL_GROUPS");
-  // u16 codes (more than 256 bins, or 256 bins with missing values): the
-  // 16-feature-group list kernel (k_hist_list16), up to 1024 bins
+  // u16 codes (more than 256 bins, or 256 bins with missing values) and u8
+  // codes of more than 64 features: the 16-feature-group list kernel
+  // (k_hist_list16), up to 1024 bins
   const int l16_groups = (int)ceil_div(s.d, kL16Feat);
-  const bool lists16 = sizeof(CodeT) == 2 && s.B <= kL16Bins && s.depth <= 8 && (hp_env == 0 || hp_env == 5) &&
+  const bool lists16 = ((sizeof(CodeT) == 2 && s.B <= kL16Bins) || (sizeof(CodeT) == 1 && s.d > 64)) && s.depth <= 8 &&
+                       (hp_env == 0 || hp_env == 5) &&
                        2 * (1 << (s.depth - 1)) * l16_groups <= kLhMaxSegs && !getenv("BB_HIST_WARP") &&
                        !getenv("BB_HIST_GLOBAL_GROUPS") && !(getenv("BB_LIST16") && atoi(getenv("BB_LIST16")) == 0);
   const bool lists = lists8 || lists16;
@@ -1314,8 +1316,8 @@ static void run_trees(Ctx& c, Arena& A, const FitShape& s, const CodeT* codes, i
   if (lists16) {
     rc16 = A.alloc<uint16_t>((size_t)npad * kL16Feat * l16_groups);
     BB_CUDA(cudaFuncSetAttribute(k_hist_list16, cudaFuncAttributeMaxDynamicSharedMemorySize, kL16SmemBytes));
-    k_rowcodes16<<<dim3((unsigned)ceil_div(n, kTile), l16_groups), 256, 0, st>>>(
-        reinterpret_cast<const uint16_t*>(codes), n, s.d, l16_groups, rc16);
+    k_rowcodes16<CodeT><<<dim3((unsigned)ceil_div(n, kTile), l16_groups), 256, 0, st>>>(codes, n, s.d, l16_groups,
+                                                                                       code_off, rc16);
     BB_LAUNCH_CHECK();
   }
   if (lists8) {

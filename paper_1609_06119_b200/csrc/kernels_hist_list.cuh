@@ -738,14 +738,16 @@ __global__ void __launch_bounds__(kLhThreads, 1)
 
 // Row-major copy of the tiled column-major u16 codes as histogram slots:
 // rc16[row][16 * groups].  One CTA per (1024-row tile, feature group).
-__global__ void __launch_bounds__(256) k_rowcodes16(const uint16_t* __restrict__ codes, int64_t n, int d, int ngroups,
-                                                    uint16_t* __restrict__ rc16) {
-  __shared__ __align__(16) uint16_t col[kL16Feat][kTile];
+template <typename CodeT>  // u16 codes, or u8 codes of more than 64 features (stored code + code_off = code)
+__global__ void __launch_bounds__(256) k_rowcodes16(const CodeT* __restrict__ codes, int64_t n, int d, int ngroups,
+                                                    int code_off, uint16_t* __restrict__ rc16) {
+  __shared__ __align__(16) CodeT col[kL16Feat][kTile];
   const int64_t tile = blockIdx.x;
   const int grp = blockIdx.y;
   const int f0 = kL16Feat * grp, fg = min(kL16Feat, d - f0);
-  for (int i = threadIdx.x; i < fg * (kTile / 8); i += blockDim.x) {
-    const int f = i / (kTile / 8), v = i % (kTile / 8);
+  constexpr int kVec = kTile * (int)sizeof(CodeT) / 16;  // 16-byte vectors per column
+  for (int i = threadIdx.x; i < fg * kVec; i += blockDim.x) {
+    const int f = i / kVec, v = i % kVec;
     reinterpret_cast<uint4*>(&col[f][0])[v] =
         __ldg(reinterpret_cast<const uint4*>(codes + (tile * d + f0 + f) * (int64_t)kTile) + v);
   }
@@ -758,7 +760,8 @@ __global__ void __launch_bounds__(256) k_rowcodes16(const uint16_t* __restrict__
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       // slot = code - 1; missing values and padding features: the dummy bin row
-      const uint32_t cl = 2 * j < fg ? col[2 * j][r] : 0u, ch = 2 * j + 1 < fg ? col[2 * j + 1][r] : 0u;
+      const uint32_t cl = 2 * j < fg ? (uint32_t)col[2 * j][r] + (uint32_t)code_off : 0u;
+      const uint32_t ch = 2 * j + 1 < fg ? (uint32_t)col[2 * j + 1][r] + (uint32_t)code_off : 0u;
       const uint32_t lo = cl ? cl - 1u : (uint32_t)kL16Bins, hi = ch ? ch - 1u : (uint32_t)kL16Bins;
       wv[j] = lo | (hi << 16);
     }

@@ -901,7 +901,8 @@ def test_fit_staged_upload_matches_plain_copy(monkeypatch):
 
 # ------------------------------------------------------------------ u16 row-list histogram (k_hist_list16)
 @pytest.mark.parametrize("levels,nan,d,depth", [(8, True, 37, 4), (9, False, 21, 5), (10, False, 16, 3),
-                                                (10, True, 50, 4), (9, False, 100, 6)])
+                                                (10, True, 50, 4), (9, False, 100, 6),
+                                                (8, False, 100, 4), (7, True, 70, 3)])  # u8 codes, > 64 features
 def test_fit_list16_vs_fixed_point_oracle(levels, nan, d, depth, monkeypatch):
     """2-byte codes (256 bins with missing values, 512 and 1024 bins) run the
     16-feature-group row-list histogram: ragged last groups, with and without

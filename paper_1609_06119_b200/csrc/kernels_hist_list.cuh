@@ -451,15 +451,10 @@ __global__ void __launch_bounds__(kListThreads) k_advance_list(
           if (side[k] == sd) rowv[k] = (rowv[k] & 0x7fffffff), side[k] = sd + 4 * __popc(m & ((1u << lane) - 1u));
         }
       __syncthreads();
-      if (threadIdx.x < 2) {
-        const int sd = threadIdx.x;
-        int run = 0;
-        for (int e = 0; e < R * NWARP; ++e) {
-          const int x = s_wc[sd * R * NWARP + e];
-          s_wc[sd * R * NWARP + e] = run;
-          run += x;
-        }
-        s_base[sd] = run ? atomicAdd(cnt + 2 * (2 * c + 1 + sd) + cls, run) : 0;
+      if (threadIdx.x < 64) {  // warp sd: exclusive scan of side sd's (row group, warp) counts
+        const int sd = threadIdx.x >> 5;
+        const int run = warp_excl_scan_64(s_wc + sd * R * NWARP, lane);
+        if (lane == 0) s_base[sd] = run ? atomicAdd(cnt + 2 * (2 * c + 1 + sd) + cls, run) : 0;
       }
       __syncthreads();
 #pragma unroll

@@ -45,6 +45,22 @@ __global__ void k_iota(int* __restrict__ a, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) a[i] = (int)i;
 }
 
+// In-place exclusive scan of 64 counters in shared memory by one warp (two
+// per lane); returns the total to every lane.
+__device__ __forceinline__ int warp_excl_scan_64(int* a, int lane) {
+  const int x0 = a[2 * lane], x1 = a[2 * lane + 1];
+  int incl = x0 + x1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int excl = incl - (x0 + x1);
+  a[2 * lane] = excl;
+  a[2 * lane + 1] = excl + x0;
+  return __shfl_sync(0xffffffffu, incl, 31);
+}
+
 // ---------------------------------------------------------------- refresh
 // F += gamma_prev[node] (score update of the previous tree, all rows), then
 // responses, boost weights and the quantised effective weight of tree t.
@@ -53,6 +69,7 @@ __global__ void k_iota(int* __restrict__ a, int64_t n) {
 // counter per key hit by every warp serialises at L2: 5x slower at cfg3).
 constexpr int kListTileRows = 2048;  // rows per CTA tile (512 threads x 4)
 constexpr int kListThreads = 512;
+static_assert(kListTileRows / kListThreads * (kListThreads / 32) == 64, "warp_excl_scan_64: 64 (row group, warp) counters");
 constexpr int kStageNodes = 127;     // staged refresh walk: internal nodes (depth <= 7)
 
 // Leaf of row i in tree `tree` over its bin codes (trees.py:318-330): an
@@ -326,15 +343,10 @@ __global__ void __launch_bounds__(kListThreads, 3) k_update_refresh(int64_t n, i
     }
     if (!lrow) continue;
     __syncthreads();
-    if (threadIdx.x < 2) {  // exclusive scan of class c's (k, warp) counts in row order
-      const int c = threadIdx.x;
-      int run = 0;
-      for (int e = 0; e < R * (kListThreads / 32); ++e) {
-        const int x = s_wc[c * R * (kListThreads / 32) + e];
-        s_wc[c * R * (kListThreads / 32) + e] = run;
-        run += x;
-      }
-      s_base[c] = run ? atomicAdd(cnt + c, run) : 0;
+    if (threadIdx.x < 64) {  // warp c: exclusive scan of class c's (k, warp) counts in row order
+      const int c = threadIdx.x >> 5;
+      const int run = warp_excl_scan_64(s_wc + c * R * (kListThreads / 32), threadIdx.x & 31);
+      if ((threadIdx.x & 31) == 0) s_base[c] = run ? atomicAdd(cnt + c, run) : 0;
     }
     __syncthreads();
 #pragma unroll

@@ -932,3 +932,20 @@ def test_fit_list16_vs_fixed_point_oracle(levels, nan, d, depth, monkeypatch):
         np.testing.assert_array_equal(tr.feature, old.trees[t].feature)
         np.testing.assert_array_equal(tr.cut_bin, old.trees[t].cut_bin)
         np.testing.assert_array_equal(tr.node_weight, old.trees[t].node_weight)
+
+
+def test_predict_pinned_host_rows_bypass_staging():
+    """Rows that are already pinned (cudaHostAlloc / torch pin_memory) are
+    passed to the DMA engine directly; same result as pageable rows."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(21)
+    Xs = rng.normal(size=(10_000, 8))
+    y = (Xs[:, 0] - Xs[:, 2] + rng.normal(size=10_000) > 0).astype(int)
+    forest = fit_forest(Xs, y, None, FitConfig(n_trees=10, depth=3, binning_levels=5, seed=9))
+    n = 400_000  # 12.8 MB of float32 rows: above the staging threshold
+    Xp = torch.empty((n, 8), dtype=torch.float32, pin_memory=True)
+    X = Xp.numpy()
+    X[:] = rng.normal(size=(n, 8)).astype(np.float32)
+    p_pinned = predict_batch(forest, X)
+    p_pageable = predict_batch(forest, X.copy())
+    np.testing.assert_array_equal(p_pinned, p_pageable)

@@ -2449,13 +2449,13 @@ int bb_predict(bb_ctx* ctx, const bb_forest* fo, const void* X, int32_t x_dtype,
     // ---- pipelined host rows: chunk i's upload (copy stream), kernels (st)
     // and read-back (second copy stream) overlap chunks i+1 / i-1
     constexpr int K = PinnedRing::kBufs;
-    const size_t out_chunk = HostStager::kChunk / 4;
-    int64_t rows_c = (int64_t)std::min(HostStager::kChunk / row_bytes, out_chunk / 8);
+    const size_t out_chunk = HostStager::chunk() / 4;
+    int64_t rows_c = (int64_t)std::min(HostStager::chunk() / row_bytes, out_chunk / 8);
     rows_c = std::max<int64_t>(1024, rows_c / 1024 * 1024);
     HostStager& hs = c.stage;
-    hs.in.ensure(std::max(HostStager::kChunk, (size_t)rows_c * row_bytes));
-    if (out_prob) hs.out.ensure(std::max(HostStager::kChunk, (size_t)rows_c * 8));
-    if (out_score) hs.out2.ensure(std::max(HostStager::kChunk, (size_t)rows_c * 8));
+    hs.in.ensure(std::max(HostStager::chunk(), (size_t)rows_c * row_bytes));
+    if (out_prob) hs.out.ensure(std::max(HostStager::chunk(), (size_t)rows_c * 8));
+    if (out_score) hs.out2.ensure(std::max(HostStager::chunk(), (size_t)rows_c * 8));
     PipeStreams ps(c.device);
     const int64_t chunks = ceil_div(n, rows_c);
     cudaEvent_t ev_k[K];

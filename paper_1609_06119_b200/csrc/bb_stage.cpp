@@ -134,16 +134,25 @@ PinnedRing::~PinnedRing() {
 }
 
 // ---------------------------------------------------------------- stager
+size_t HostStager::chunk() {
+  static const size_t v = [] {
+    int mb = 16;
+    if (const char* e = getenv("BB_STAGE_CHUNK_MB")) mb = atoi(e);
+    return (size_t)std::max(1, std::min(mb, 256)) << 20;
+  }();
+  return v;
+}
+
 void HostStager::h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (bytes == 0) return;
   if (bytes < kMinStaged || getenv("BB_NO_STAGING") || host_pointer_is_pinned(src)) {
     cu(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync H2D");
     return;
   }
-  in.ensure(kChunk);
+  in.ensure(chunk());
   int b = 0;
-  for (size_t off = 0; off < bytes; off += kChunk, b = (b + 1) % PinnedRing::kBufs) {
-    const size_t len = std::min(kChunk, bytes - off);
+  for (size_t off = 0; off < bytes; off += chunk(), b = (b + 1) % PinnedRing::kBufs) {
+    const size_t len = std::min(chunk(), bytes - off);
     cu(cudaEventSynchronize(in.ev(b)), "cudaEventSynchronize");  // this chunk's previous DMA has left the buffer
     parallel_memcpy(in.buf(b), (const char*)src + off, len);
     cu(cudaMemcpyAsync((char*)dst + off, in.buf(b), len, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync H2D");
@@ -158,17 +167,17 @@ void HostStager::d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) 
     cu(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     return;
   }
-  out.ensure(kChunk);
+  out.ensure(chunk());
   constexpr int K = PinnedRing::kBufs;
-  const size_t chunks = (bytes + kChunk - 1) / kChunk;
+  const size_t chunks = (bytes + chunk() - 1) / chunk();
   auto drain = [&](size_t j) {
-    const size_t off = j * kChunk, len = std::min(kChunk, bytes - off);
+    const size_t off = j * chunk(), len = std::min(chunk(), bytes - off);
     cu(cudaEventSynchronize(out.ev((int)(j % K))), "cudaEventSynchronize");
     parallel_memcpy((char*)dst + off, out.buf((int)(j % K)), len);
   };
   for (size_t i = 0; i < chunks; ++i) {
     if (i >= (size_t)K) drain(i - K);
-    const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+    const size_t off = i * chunk(), len = std::min(chunk(), bytes - off);
     cu(cudaMemcpyAsync(out.buf((int)(i % K)), (const char*)src + off, len, cudaMemcpyDeviceToHost, st),
        "cudaMemcpyAsync D2H");
     cu(cudaEventRecord(out.ev((int)(i % K)), st), "cudaEventRecord");

@@ -42,7 +42,7 @@ class PinnedRing {
 // per-context staging state (created lazily, reused by every call)
 class HostStager {
  public:
-  static constexpr size_t kChunk = (size_t)16 << 20;     // bytes per pinned chunk
+  static size_t chunk();  // bytes per pinned chunk (BB_STAGE_CHUNK_MB, default 16)
   static constexpr size_t kMinStaged = (size_t)8 << 20;  // below this: plain cudaMemcpyAsync
   // dst (device) <- src (host).  On return every byte of src has been read
   // (the caller may free it) and the DMAs are enqueued on st.
